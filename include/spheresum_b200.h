@@ -1,0 +1,153 @@
+/*
+ * spheresum_b200 — C-ABI of the B200-native spherical barycentric-Lagrange
+ * tree code (arXiv 2401.07361). Plain pointers and sizes only; no exceptions
+ * and no C++/torch types cross this boundary.
+ *
+ * Every entry point replaces one reference interface (namespace spheresum,
+ * proj/include/spheresum/ in the reference). The mapping is given beside
+ * each declaration. The C++ drop-in (see include/spheresum_b200/)
+ * and the Python package (paper_2401_07361_b200) sit on top of this header.
+ *
+ * Layouts: positions are N x 3 fp64 AoS unit vectors (the bytes of
+ * std::vector<UnitVector3>, geometry.hpp:50-66), strengths q_j = zeta_j A_j are
+ * N fp64, outputs are N x D fp64 AoS (PotentialField<D>, treecode.hpp:32-33):
+ * D = 3 for the Biot-Savart velocity, D = 1 for the log-kernel stream function.
+ * All particle arrays are in the caller's (original) order.
+ *
+ * Error convention: every function returns an ssum_status. Non-zero codes
+ * mirror the reference's exception taxonomy (errors.hpp:10-33), plus CUDA.
+ * The message of the last failure is available from ssum_last_error().
+ *
+ * Threading: a context is not thread-safe; use one host thread per context.
+ * A context owns one device, one CUDA stream and all device buffers, and it
+ * holds the persistent face-tree geometry (FaceTree semantics: node geometry
+ * survives across calls and only grows, face_tree.cpp:42,73-76).
+ */
+#ifndef SPHERESUM_B200_H_
+#define SPHERESUM_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ssum_ctx ssum_ctx;
+
+typedef enum {
+  SSUM_OK = 0,
+  SSUM_CONFIG = 1,       /* ConfigError           (treecode.cpp:13-20)            */
+  SSUM_GEOMETRY = 2,     /* GeometryError         (face_tree.cpp:85, geometry.cpp) */
+  SSUM_SINGULAR = 3,     /* SingularKernelError   (kernels.hpp:19,27-29)          */
+  SSUM_CONDITIONING = 4, /* ConditioningError     (sbb.cpp:89-93)                 */
+  SSUM_INVALID = 5,      /* std::invalid_argument (sbb.cpp:15,78,145)             */
+  SSUM_CUDA = 6,         /* CUDA runtime failure (no reference equivalent)        */
+  SSUM_NCCL = 7,         /* reserved for collective failures                      */
+  SSUM_NOMEM = 8,        /* device or host allocation failure                     */
+  SSUM_INTERNAL = 9
+} ssum_status;
+
+typedef enum {
+  SSUM_BIOT_SAVART = 0,   /* BiotSavartKernel   (kernels.hpp:52-61), dim 3, prefactor -1/(4 pi) */
+  SSUM_LOG_POTENTIAL = 1  /* LogPotentialKernel (kernels.hpp:44-50), dim 1, prefactor 1          */
+} ssum_kernel;
+
+/* TraversalConfig (treecode.hpp:13-20) with the same ranges (validate,
+ * treecode.cpp:13-20). pc_only = 1 selects the particle-cluster-only traversal
+ * (BASELINE config 2; not in the reference): CP -> PP and CC -> PC. */
+typedef struct {
+  double theta;    /* MAC, in (0, 1]                         */
+  int n_threshold; /* bin size above which a node is a cluster */
+  int degree;      /* SBB interpolation degree, [1, 20]       */
+  int max_depth;   /* deepest tree level, [1, 40]             */
+  int pc_only;     /* 0 = full dual traversal, 1 = PC-only    */
+} ssum_config;
+
+/* TreecodeStats (treecode.hpp:75-80) plus device-side detail. The three
+ * *_seconds fields ACCUMULATE (+=) like the reference's; everything else is
+ * overwritten by each call. */
+typedef struct {
+  double bin_seconds;
+  double traversal_seconds;
+  double eval_seconds;
+  uint64_t interaction_counts[4]; /* indexed PP, PC, CP, CC (InteractionKind)      */
+  double h2d_seconds, d2h_seconds;  /* host-pointer entry points only             */
+  uint64_t kernel_evals[4];       /* PP pairs (excl. self), PC, CP, CC evaluations */
+  int64_t node_count, leaf_count, weight_nodes, fit_nodes;
+  int64_t gpu_launches;           /* kernels launched by the last call            */
+  double pp_pc_ms, cp_cc_fit_ms, upward_ms, finish_ms; /* device time per pass     */
+} ssum_stats;
+
+/* ---- context ------------------------------------------------------------ */
+int ssum_create(int device, ssum_ctx** out);
+void ssum_destroy(ssum_ctx* ctx);
+const char* ssum_last_error(const ssum_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the
+ * context's own stream. */
+int ssum_set_stream(ssum_ctx* ctx, void* cuda_stream);
+/* Drop the persistent tree geometry (a freshly constructed FaceTree,
+ * face_tree.cpp:9-16). */
+int ssum_tree_reset(ssum_ctx* ctx);
+
+/* ---- summation ---------------------------------------------------------- */
+/* treecode_sum<K> (treecode.hpp:93-97, treecode.cpp:266-413): bins into the
+ * context's tree, traverses, evaluates. Host pointers; copies are inside. */
+int ssum_treecode_sum(ssum_ctx* ctx, int kernel, const ssum_config* cfg, const double* xyz,
+                      const double* q, int64_t n, double* out, ssum_stats* stats);
+/* Same, with DEVICE pointers (inputs already resident in HBM). Synchronous on
+ * return unless stats == NULL and the stream is external (then only stream-ordered). */
+int ssum_treecode_sum_device(ssum_ctx* ctx, int kernel, const ssum_config* cfg,
+                             const double* d_xyz, const double* d_q, int64_t n, double* d_out,
+                             ssum_stats* stats);
+/* direct_sum<K> (treecode.hpp:84-86, treecode.cpp:246-264): exact O(N^2). */
+int ssum_direct_sum(ssum_ctx* ctx, int kernel, const double* xyz, const double* q, int64_t n,
+                    double* out);
+int ssum_direct_sum_device(ssum_ctx* ctx, int kernel, const double* d_xyz, const double* d_q,
+                           int64_t n, double* d_out);
+
+/* ---- tree and interaction lists (host views, reference numbering) ------- */
+/* FaceTree::bin_particles (face_tree.hpp:42, face_tree.cpp:73-88). */
+int ssum_bin_particles(ssum_ctx* ctx, const double* xyz, int64_t n, int n_threshold,
+                       int max_depth);
+/* Node count of the context's tree (FaceTree::node_count, face_tree.hpp:47). */
+int ssum_tree_node_count(ssum_ctx* ctx, int* count);
+/* Export the binned tree with the reference's node ids. Any pointer may be
+ * NULL. tri: 9 doubles per node (v1, v2, v3); center: 3; radius: 1;
+ * bin_offsets: node_count + 1; bin_ids: ascending particle ids per node
+ * (TreeNode::bin); leaf_of: n (FaceTree::leaf_of_particle). */
+int ssum_tree_export(ssum_ctx* ctx, int* level, int* parent, int* child_base, double* tri,
+                     double* center, double* radius, int64_t* bin_offsets, int* bin_ids,
+                     int* leaf_of);
+/* dual_traversal (treecode.hpp:44-45, treecode.cpp:69-77) on the binned tree:
+ * (target, source, kind) triples in the reference's emission order and node
+ * numbering. Writes min(count, cap) triples; *count receives the total. */
+int ssum_dual_traversal(ssum_ctx* ctx, const ssum_config* cfg, int* tsk, int64_t cap,
+                        int64_t* count);
+
+/* ---- Lagrangian RK4 (absent from the reference code) ---- */
+/* In place on host arrays: xyz (N x 3), zeta (N); area (N) fixed. Each stage
+ * evaluates u with treecode_sum<BiotSavartKernel> (direct_sum if direct != 0)
+ * on the context's (reused) tree, dzeta/dt = -2 omega u_z, stage and final
+ * positions renormalised. Device-resident between stages. */
+int ssum_rk4(ssum_ctx* ctx, const ssum_config* cfg, double* xyz, double* zeta,
+             const double* area, int64_t n, double dt, int steps, double omega, int direct,
+             ssum_stats* stats);
+
+/* ---- fixtures (BASELINE.json configs; host-side generators) -------------- */
+/* make_icosa_mesh(level).vertices() / node_patch_areas() (icosa_mesh.cpp:37-133). */
+int64_t ssum_mesh_vertex_count(int level);
+int ssum_make_icosa_mesh(int level, double* xyz, double* area);
+/* BASELINE Rossby-Haurwitz R=4 vorticity (omega = K = 1):
+ * zeta = 2 sin(lat) - 30 sin(lat) cos^4(lat) cos(4 lon). */
+int ssum_rh4_vorticity(const double* xyz, int64_t n, double* zeta);
+/* BASELINE config 3: seeded points (half uniform, half in a 10 deg cap at lat
+ * 40, lon 0), Gaussian vortex minus its weighted mean, A = 4 pi / N. The
+ * near-duplicate policy resamples any point whose 1 - x.y <= 1e-12 against an
+ * earlier point. */
+int ssum_make_random_cap(int64_t n, uint64_t seed, double* xyz, double* zeta, double* area);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPHERESUM_B200_H_ */

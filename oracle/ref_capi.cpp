@@ -342,8 +342,10 @@ int ref_rk4(double* xyz, double* zeta, const double* area, int64_t n, double the
     for (int step = 0; step < steps; ++step) {
       for (int s = 0; s < 4; ++s) {
         for (size_t i = 0; i < N; ++i) {
-          if (s == 0) {
-            pts[i] = UnitVector3(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+          if (s == 0) {  // the state is already unit (renormalised at the end of each step)
+            pts[i].x = xyz[3 * i];
+            pts[i].y = xyz[3 * i + 1];
+            pts[i].z = xyz[3 * i + 2];
             sz[i] = zeta[i];
           } else {
             const double* kp = &k[s - 1][3 * i];

@@ -1,0 +1,446 @@
+// extern "C" boundary (include/spheresum_b200.h): context lifetime, the
+// treecode/direct entry points, tree and list export in the reference's
+// numbering, and the device-resident RK4 driver. Internal ssum::Error
+// exceptions stop here and become status codes; nothing throws across the ABI.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace ssum {
+
+void sorted_interactions(Ctx& c, std::vector<int4>& out);
+
+void check_flags(Ctx& c, const char* where) {
+  int f = 0;
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (f & kFlagGeometry) throw Error(SSUM_GEOMETRY, std::string(where) + ": degenerate geometry");
+  if (f & kFlagSingular)
+    throw Error(SSUM_SINGULAR, std::string(where) + ": kernel evaluated at its singularity (1 - x.y <= 1e-14)");
+}
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+double secs(clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+// TraversalConfig::validate (treecode.cpp:13-20)
+void validate(const ssum_config* cfg) {
+  if (!cfg) throw Error(SSUM_CONFIG, "null config");
+  if (!(cfg->theta > 0.0 && cfg->theta <= 1.0)) throw Error(SSUM_CONFIG, "theta must be in (0, 1]");
+  if (cfg->n_threshold < 1) throw Error(SSUM_CONFIG, "n_threshold must be >= 1");
+  if (cfg->degree < 1 || cfg->degree > kMaxDegree) throw Error(SSUM_CONFIG, "degree must be in [1, 20]");
+  if (cfg->max_depth < 1 || cfg->max_depth > 40) throw Error(SSUM_CONFIG, "max_depth must be in [1, 40]");
+}
+
+void check_kernel(int kernel) {
+  if (kernel != SSUM_BIOT_SAVART && kernel != SSUM_LOG_POTENTIAL) throw Error(SSUM_INVALID, "unknown kernel id");
+}
+
+void check_n(int64_t n) {
+  if (n < 0 || n > 0x3fffffff) throw Error(SSUM_INVALID, "particle count out of range");
+}
+
+template <class F>
+int guarded(ssum_ctx* h, F&& f) {
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c) return SSUM_INVALID;
+  try {
+    cudaSetDevice(c->device);
+    f(*c);
+    return SSUM_OK;
+  } catch (const Error& e) {
+    c->last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    c->last_error = "host allocation failed";
+    return SSUM_NOMEM;
+  } catch (const std::exception& e) {
+    c->last_error = e.what();
+    return SSUM_INTERNAL;
+  }
+}
+
+// The full device path: bin, traverse, evaluate. Inputs/outputs on the device.
+void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q, int64_t n,
+                     double* d_out, ssum_stats* st) {
+  const int64_t l0 = c.launches;
+  const auto t0 = clk::now();
+  tree_bin(c, d_xyz, n, cfg.n_threshold, cfg.max_depth);
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  const auto t1 = clk::now();
+  traverse_and_build_lists(c, cfg, false);
+  const auto t2 = clk::now();
+  evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
+  const auto t3 = clk::now();
+  if (st) {
+    st->bin_seconds += secs(t0, t1);
+    st->traversal_seconds += secs(t1, t2);
+    st->eval_seconds += secs(t2, t3);
+    for (int k = 0; k < 4; ++k) {
+      st->interaction_counts[k] = c.lists.counts[k];
+      st->kernel_evals[k] = c.lists.evals[k];
+    }
+    st->node_count = c.nodes.count;
+    st->leaf_count = static_cast<int64_t>(c.bins.leaves.size());
+    st->weight_nodes = c.lists.n_weight;
+    st->fit_nodes = c.lists.n_fit;
+    st->gpu_launches = c.launches - l0;
+  }
+}
+
+// Reference node ids: roots 0..19; each bin_particles call appends the quads
+// it creates in the order distribute() visits their parents (depth-first
+// preorder, face_tree.cpp:39-71). Returns dev -> ref.
+std::vector<int> reference_ids(const HostTree& h) {
+  const int nn = static_cast<int>(h.level.size());
+  std::vector<int> pre(size_t(nn), -1);
+  int r = 0;
+  std::vector<int> stack;
+  for (int f = 19; f >= 0; --f) stack.push_back(f);
+  while (!stack.empty()) {
+    const int id = stack.back();
+    stack.pop_back();
+    pre[id] = r++;
+    const int cb = h.child_base[id];
+    if (cb >= 0)
+      for (int q = 3; q >= 0; --q) stack.push_back(cb + q);
+  }
+  std::vector<int> quads;  // first child of every quad
+  for (int id = 20; id < nn; id += 4) quads.push_back(id);
+  std::stable_sort(quads.begin(), quads.end(), [&](int a, int b) {
+    if (h.created_call[a] != h.created_call[b]) return h.created_call[a] < h.created_call[b];
+    return pre[h.parent[a]] < pre[h.parent[b]];
+  });
+  std::vector<int> ref(static_cast<size_t>(nn));
+  for (int f = 0; f < 20; ++f) ref[f] = f;
+  int next = 20;
+  for (const int q : quads)
+    for (int k = 0; k < 4; ++k) ref[q + k] = next++;
+  return ref;
+}
+
+void upload(Ctx& c, DBuf<double>& buf, const double* h, size_t count, ssum_stats* st) {
+  const auto t0 = clk::now();
+  buf.ensure(std::max<size_t>(count, 1));
+  if (count) SSUM_CUDA_CHECK(cudaMemcpyAsync(buf.p, h, count * 8, cudaMemcpyHostToDevice, c.stream));
+  if (st) {
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    st->h2d_seconds += secs(t0, clk::now());
+  }
+}
+
+void download(Ctx& c, double* h, const double* d, size_t count, ssum_stats* st) {
+  const auto t0 = clk::now();
+  if (count) SSUM_CUDA_CHECK(cudaMemcpyAsync(h, d, count * 8, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (st) st->d2h_seconds += secs(t0, clk::now());
+}
+
+__global__ void k_rk4_stage(int64_t n, int stage, double cs, const double* __restrict__ x0,
+                            const double* __restrict__ z0, const double* __restrict__ area,
+                            const double* __restrict__ kprev, const double* __restrict__ kzprev,
+                            double* __restrict__ xs, double* __restrict__ q, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double zs;
+  if (stage == 0) {
+    xs[3 * i] = x0[3 * i];
+    xs[3 * i + 1] = x0[3 * i + 1];
+    xs[3 * i + 2] = x0[3 * i + 2];
+    zs = z0[i];
+  } else {
+    int bad = 0;
+    const d3 v{add_rn(x0[3 * i], mul_rn(cs, kprev[3 * i])), add_rn(x0[3 * i + 1], mul_rn(cs, kprev[3 * i + 1])),
+               add_rn(x0[3 * i + 2], mul_rn(cs, kprev[3 * i + 2]))};
+    const d3 u = unit_rn(v, &bad);
+    if (bad) atomicOr(flags, kFlagGeometry);
+    xs[3 * i] = u.x;
+    xs[3 * i + 1] = u.y;
+    xs[3 * i + 2] = u.z;
+    zs = add_rn(z0[i], mul_rn(cs, kzprev[i]));
+  }
+  q[i] = mul_rn(zs, area[i]);
+}
+
+// k_s = u, kz_s = -2 Omega u_z; acc = ((k1 + 2 k2) + 2 k3) + k4 in that order.
+__global__ void k_rk4_accum(int64_t n, int stage, double omega, const double* __restrict__ u, double* __restrict__ k,
+                            double* __restrict__ kz, double* __restrict__ acc, double* __restrict__ accz) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double w = (stage == 1 || stage == 2) ? 2.0 : 1.0;
+  const double kzv = mul_rn(mul_rn(-2.0, omega), u[3 * i + 2]);
+  for (int d = 0; d < 3; ++d) {
+    const double v = u[3 * i + d];
+    k[3 * i + d] = v;
+    acc[3 * i + d] = stage == 0 ? v : add_rn(acc[3 * i + d], mul_rn(w, v));
+  }
+  kz[i] = kzv;
+  accz[i] = stage == 0 ? kzv : add_rn(accz[i], mul_rn(w, kzv));
+}
+
+__global__ void k_rk4_final(int64_t n, double h6, double* __restrict__ x0, double* __restrict__ z0,
+                            const double* __restrict__ acc, const double* __restrict__ accz, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int bad = 0;
+  const d3 v{add_rn(x0[3 * i], mul_rn(h6, acc[3 * i])), add_rn(x0[3 * i + 1], mul_rn(h6, acc[3 * i + 1])),
+             add_rn(x0[3 * i + 2], mul_rn(h6, acc[3 * i + 2]))};
+  const d3 u = unit_rn(v, &bad);
+  if (bad) atomicOr(flags, kFlagGeometry);
+  x0[3 * i] = u.x;
+  x0[3 * i + 1] = u.y;
+  x0[3 * i + 2] = u.z;
+  z0[i] = add_rn(z0[i], mul_rn(h6, accz[i]));
+}
+
+}  // namespace
+}  // namespace ssum
+
+using namespace ssum;
+
+extern "C" {
+
+int ssum_create(int device, ssum_ctx** out) {
+  if (!out) return SSUM_INVALID;
+  *out = nullptr;
+  Ctx* c = nullptr;
+  try {
+    c = new Ctx();
+    c->device = device;
+    SSUM_CUDA_CHECK(cudaSetDevice(device));
+    SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    for (auto& e : c->ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
+    c->d_flags.ensure(64);
+    SSUM_CUDA_CHECK(cudaMemset(c->d_flags.p, 0, 64 * sizeof(int)));
+    tree_init_roots(*c);
+  } catch (const Error& e) {
+    delete c;
+    return e.code;
+  } catch (...) {
+    delete c;
+    return SSUM_INTERNAL;
+  }
+  *out = reinterpret_cast<ssum_ctx*>(c);
+  return SSUM_OK;
+}
+
+void ssum_destroy(ssum_ctx* h) {
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  // DBuf members free their memory through release(); walk the obvious ones.
+  c->pts.release();
+  c->S.release();
+  c->coeff.release();
+  c->wpart.release();
+  c->in_xyz.release();
+  c->in_q.release();
+  c->out_buf.release();
+  c->rk_state.release();
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+const char* ssum_last_error(const ssum_ctx* h) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  return c ? c->last_error.c_str() : "null context";
+}
+
+int ssum_set_stream(ssum_ctx* h, void* stream) {
+  return guarded(h, [&](Ctx& c) { c.stream = stream ? static_cast<cudaStream_t>(stream) : c.own_stream; });
+}
+
+int ssum_tree_reset(ssum_ctx* h) {
+  return guarded(h, [&](Ctx& c) {
+    c.call_index = 0;
+    tree_init_roots(c);
+  });
+}
+
+int ssum_treecode_sum_device(ssum_ctx* h, int kernel, const ssum_config* cfg, const double* d_xyz,
+                             const double* d_q, int64_t n, double* d_out, ssum_stats* st) {
+  return guarded(h, [&](Ctx& c) {
+    validate(cfg);
+    check_kernel(kernel);
+    check_n(n);
+    treecode_device(c, kernel, *cfg, d_xyz, d_q, n, d_out, st);
+  });
+}
+
+int ssum_treecode_sum(ssum_ctx* h, int kernel, const ssum_config* cfg, const double* xyz, const double* q,
+                      int64_t n, double* out, ssum_stats* st) {
+  return guarded(h, [&](Ctx& c) {
+    validate(cfg);
+    check_kernel(kernel);
+    check_n(n);
+    const int D = kernel == SSUM_BIOT_SAVART ? 3 : 1;
+    upload(c, c.in_xyz, xyz, size_t(n) * 3, st);
+    upload(c, c.in_q, q, size_t(n), st);
+    c.out_buf.ensure(std::max<size_t>(size_t(n) * D, 1));
+    treecode_device(c, kernel, *cfg, c.in_xyz.p, c.in_q.p, n, c.out_buf.p, st);
+    download(c, out, c.out_buf.p, size_t(n) * D, st);
+  });
+}
+
+int ssum_direct_sum_device(ssum_ctx* h, int kernel, const double* d_xyz, const double* d_q, int64_t n,
+                           double* d_out) {
+  return guarded(h, [&](Ctx& c) {
+    check_kernel(kernel);
+    check_n(n);
+    direct_sum_device(c, kernel, d_xyz, d_q, n, d_out);
+  });
+}
+
+int ssum_direct_sum(ssum_ctx* h, int kernel, const double* xyz, const double* q, int64_t n, double* out) {
+  return guarded(h, [&](Ctx& c) {
+    check_kernel(kernel);
+    check_n(n);
+    const int D = kernel == SSUM_BIOT_SAVART ? 3 : 1;
+    upload(c, c.in_xyz, xyz, size_t(n) * 3, nullptr);
+    upload(c, c.in_q, q, size_t(n), nullptr);
+    c.out_buf.ensure(std::max<size_t>(size_t(n) * D, 1));
+    direct_sum_device(c, kernel, c.in_xyz.p, c.in_q.p, n, c.out_buf.p);
+    download(c, out, c.out_buf.p, size_t(n) * D, nullptr);
+  });
+}
+
+int ssum_bin_particles(ssum_ctx* h, const double* xyz, int64_t n, int n_threshold, int max_depth) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (n_threshold < 1) throw Error(SSUM_CONFIG, "n_threshold must be >= 1");
+    if (max_depth < 1 || max_depth > 40) throw Error(SSUM_CONFIG, "max_depth must be in [1, 40]");
+    upload(c, c.in_xyz, xyz, size_t(n) * 3, nullptr);
+    tree_bin(c, c.in_xyz.p, n, n_threshold, max_depth);
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int ssum_tree_node_count(ssum_ctx* h, int* count) {
+  return guarded(h, [&](Ctx& c) { *count = c.nodes.count; });
+}
+
+int ssum_tree_export(ssum_ctx* h, int* level, int* parent, int* child_base, double* tri, double* center,
+                     double* radius, int64_t* bin_offsets, int* bin_ids, int* leaf_of) {
+  return guarded(h, [&](Ctx& c) {
+    const HostTree& t = c.host;
+    const int nn = c.nodes.count;
+    const std::vector<int> ref = reference_ids(t);
+    std::vector<int> dev_of(static_cast<size_t>(nn));
+    for (int d = 0; d < nn; ++d) dev_of[ref[d]] = d;
+    for (int r = 0; r < nn; ++r) {
+      const int d = dev_of[r];
+      if (level) level[r] = t.level[d];
+      if (parent) parent[r] = t.parent[d] < 0 ? -1 : ref[t.parent[d]];
+      if (child_base) child_base[r] = t.child_base[d] < 0 ? -1 : ref[t.child_base[d]];
+    }
+    auto fetch = [&](double* dst, const double* src, int w) {
+      if (!dst) return;
+      std::vector<double> tmp(size_t(nn) * w);
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), src, tmp.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+      SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      for (int r = 0; r < nn; ++r) std::memcpy(dst + size_t(r) * w, tmp.data() + size_t(dev_of[r]) * w, size_t(w) * 8);
+    };
+    fetch(tri, c.nodes.tri.p, 9);
+    fetch(center, c.nodes.center.p, 3);
+    fetch(radius, c.nodes.radius.p, 1);
+    const int64_t n = c.bins.n;
+    if (bin_offsets || bin_ids || leaf_of) {
+      std::vector<int> perm(static_cast<size_t>(n)), lf(static_cast<size_t>(n));
+      if (n) {
+        SSUM_CUDA_CHECK(cudaMemcpyAsync(perm.data(), c.bins.perm.p, size_t(n) * 4, cudaMemcpyDeviceToHost, c.stream));
+        SSUM_CUDA_CHECK(cudaMemcpyAsync(lf.data(), c.bins.leaf_of.p, size_t(n) * 4, cudaMemcpyDeviceToHost, c.stream));
+      }
+      SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      if (leaf_of)
+        for (int64_t i = 0; i < n; ++i) leaf_of[i] = ref[lf[size_t(i)]];
+      int64_t o = 0;
+      for (int r = 0; r < nn; ++r) {
+        const int d = dev_of[r];
+        const int cnt = d < static_cast<int>(t.cnt.size()) ? t.cnt[d] : 0;
+        if (bin_offsets) bin_offsets[r] = o;
+        if (bin_ids && cnt > 0) {
+          std::copy(perm.begin() + t.off[d], perm.begin() + t.off[d] + cnt, bin_ids + o);
+          std::sort(bin_ids + o, bin_ids + o + cnt);  // TreeNode::bin is ascending
+        }
+        o += cnt;
+      }
+      if (bin_offsets) bin_offsets[nn] = o;
+    }
+  });
+}
+
+int ssum_dual_traversal(ssum_ctx* h, const ssum_config* cfg, int* tsk, int64_t cap, int64_t* count) {
+  return guarded(h, [&](Ctx& c) {
+    validate(cfg);
+    traverse_and_build_lists(c, *cfg, true);
+    std::vector<int4> list;
+    sorted_interactions(c, list);
+    const std::vector<int> ref = reference_ids(c.host);
+    *count = static_cast<int64_t>(list.size());
+    const int64_t m = std::min<int64_t>(cap, *count);
+    for (int64_t e = 0; e < m; ++e) {
+      tsk[3 * e] = ref[list[size_t(e)].x];
+      tsk[3 * e + 1] = ref[list[size_t(e)].y];
+      tsk[3 * e + 2] = list[size_t(e)].z;
+    }
+  });
+}
+
+int ssum_rk4(ssum_ctx* h, const ssum_config* cfg, double* xyz, double* zeta, const double* area, int64_t n,
+             double dt, int steps, double omega, int direct, ssum_stats* st) {
+  return guarded(h, [&](Ctx& c) {
+    validate(cfg);
+    check_n(n);
+    if (n == 0 || steps <= 0) return;
+    const size_t N = size_t(n);
+    // state layout in rk_state: x0 3N | z0 N | area N | xs 3N | q N | u 3N | k 3N | kz N | acc 3N | accz N
+    c.rk_state.ensure(N * 20);
+    double* x0 = c.rk_state.p;
+    double* z0 = x0 + 3 * N;
+    double* ar = z0 + N;
+    double* xs = ar + N;
+    double* q = xs + 3 * N;
+    double* u = q + N;
+    double* k = u + 3 * N;
+    double* kz = k + 3 * N;
+    double* acc = kz + N;
+    double* accz = acc + 3 * N;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(x0, xyz, 3 * N * 8, cudaMemcpyHostToDevice, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(z0, zeta, N * 8, cudaMemcpyHostToDevice, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(ar, area, N * 8, cudaMemcpyHostToDevice, c.stream));
+    const double cs[4] = {0.0, 0.5 * dt, 0.5 * dt, dt};
+    const int bs = 256;
+    for (int step = 0; step < steps; ++step) {
+      for (int s = 0; s < 4; ++s) {
+        SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
+        k_rk4_stage<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, cs[s], x0, z0, ar, k, kz, xs, q, c.d_flags.p);
+        SSUM_LAUNCH_CHECK();
+        if (direct)
+          direct_sum_device(c, SSUM_BIOT_SAVART, xs, q, n, u);
+        else
+          treecode_device(c, SSUM_BIOT_SAVART, *cfg, xs, q, n, u, st);
+        k_rk4_accum<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, omega, u, k, kz, acc, accz);
+        SSUM_LAUNCH_CHECK();
+        c.launches += 2;
+      }
+      k_rk4_final<<<grid_for(n, bs), bs, 0, c.stream>>>(n, dt / 6.0, x0, z0, acc, accz, c.d_flags.p);
+      SSUM_LAUNCH_CHECK();
+      c.launches++;
+      check_flags(c, "rk4");
+    }
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(xyz, x0, 3 * N * 8, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(zeta, z0, N * 8, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,583 @@
+// Evaluation passes of treecode_sum (treecode.cpp:326-404) on the device.
+//
+//   k_gather       particles into tree order, packed (x, y, z, q) — the
+//                  unified point array's first N entries
+//   k_proxy        Phase 1: lattice proxy points of every proxy node
+//                  (proxy_points, sbb.cpp:46-66) — entries N + slot*p + m
+//   k_up_partial   Phase 2: w_k = sum_j B_k(beta_s(x_j)) q_j over bin chunks
+//   k_up_final     (compute_proxy_weights, treecode.cpp:79-91), then
+//                  w_hat = V^-T w (solve_transposed, sbb.cpp:110-115) into
+//                  the proxy entries' 4th component
+//   k_fit_tiles    Phase 3: CP/CC proxy potentials phi per fit node and the
+//                  fit C = V^-1 phi (treecode.cpp:341-358, sbb.cpp:103-108)
+//   k_leaf_tiles   Phase 4 direct part: PP pairs and PC proxy pairs per leaf
+//                  tile (treecode.cpp:386-396)
+//   k_finish       Phase 4 downward part (add_fitted_value over the path,
+//                  treecode.cpp:143-155,397-401), cross product, prefactor,
+//                  scatter back to the caller's order (:402)
+//
+// Barycentrics use the per-node Cramer constants: beta_k = (x . n_k) / sum,
+// with n_1 = v2 x v3, n_2 = v3 x v1, n_3 = v1 x v2 — algebraically the
+// reference's spherical_barycentric (geometry.cpp:59-69: det cancels).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace ssum {
+
+namespace {
+
+constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
+
+template <int DEG>
+struct Sbb {
+  static constexpr int P = (DEG + 1) * (DEG + 2) / 2;
+};
+
+__device__ __forceinline__ void bary(const double* k, double x0, double x1, double x2, double& b1, double& b2,
+                                     double& b3) {
+  const double r1 = fma(x2, k[2], fma(x1, k[1], x0 * k[0]));
+  const double r2 = fma(x2, k[6], fma(x1, k[5], x0 * k[4]));
+  const double r3 = fma(x2, k[9], fma(x1, k[8], x0 * k[7]));
+  const double inv = 1.0 / ((r1 + r2) + r3);
+  b1 = r1 * inv;
+  b2 = r2 * inv;
+  b3 = r3 * inv;
+}
+
+template <int DEG>
+__device__ __forceinline__ void powers(double b1, double b2, double b3, double* p1, double* p2, double* p3) {
+  p1[0] = p2[0] = p3[0] = 1.0;
+#pragma unroll
+  for (int n = 1; n <= DEG; ++n) {
+    p1[n] = p1[n - 1] * b1;
+    p2[n] = p2[n - 1] * b2;
+    p3[n] = p3[n - 1] * b3;
+  }
+}
+
+__global__ void k_gather(const double* __restrict__ xyz, const double* __restrict__ q, const int* __restrict__ perm,
+                         int64_t n, double4* __restrict__ pts) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int i = perm ? perm[k] : static_cast<int>(k);
+  pts[k] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], q[i]);
+}
+
+// proxy_points (sbb.cpp:46-66): normalise(b1 v1 + b2 v2 + b3 v3), b = (i,j,k)/d
+// in the SBB index order (sbb.cpp:19-23: k ascending, then j ascending).
+__global__ void k_proxy(const int* __restrict__ slot_node, int nslots, int degree, const double* __restrict__ tri,
+                        int64_t N, double4* __restrict__ pts) {
+  const int P = (degree + 1) * (degree + 2) / 2;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= int64_t(nslots) * P) return;
+  const int slot = static_cast<int>(g / P), m = static_cast<int>(g % P);
+  int kk = 0, jj = m;
+  while (jj > degree - kk) {
+    jj -= degree - kk + 1;
+    ++kk;
+  }
+  const int ii = degree - kk - jj;
+  const double d = static_cast<double>(degree);
+  const double b1 = __ddiv_rn(static_cast<double>(ii), d), b2 = __ddiv_rn(static_cast<double>(jj), d),
+               b3 = __ddiv_rn(static_cast<double>(kk), d);
+  const double* t = tri + 9 * slot_node[slot];
+  d3 v;
+  v.x = add_rn(add_rn(mul_rn(t[0], b1), mul_rn(t[3], b2)), mul_rn(t[6], b3));
+  v.y = add_rn(add_rn(mul_rn(t[1], b1), mul_rn(t[4], b2)), mul_rn(t[7], b3));
+  v.z = add_rn(add_rn(mul_rn(t[2], b1), mul_rn(t[5], b2)), mul_rn(t[8], b3));
+  int bad = 0;
+  const d3 u = unit_rn(v, &bad);
+  pts[N + g] = make_double4(u.x, u.y, u.z, 0.0);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Partial proxy weights of one (weight node, particle chunk).
+template <int DEG>
+__global__ void __launch_bounds__(128) k_up_partial(const int4* __restrict__ chunks, const double4* __restrict__ pts,
+                                                    const double* __restrict__ cramer, double* __restrict__ wpart) {
+  constexpr int P = Sbb<DEG>::P;
+  __shared__ double red[4][P];
+  const int4 ch = chunks[blockIdx.x];  // node, begin, count
+  const double* k = cramer + 12 * ch.x;
+  double kc[10];
+#pragma unroll
+  for (int z = 0; z < 10; ++z) kc[z] = k[z];
+  double w[P];
+#pragma unroll
+  for (int m = 0; m < P; ++m) w[m] = 0.0;
+  for (int i = ch.y + threadIdx.x; i < ch.y + ch.z; i += blockDim.x) {
+    const double4 p = pts[i];
+    double b1, b2, b3;
+    bary(kc, p.x, p.y, p.z, b1, b2, b3);
+    double p1[DEG + 1], p2[DEG + 1], p3[DEG + 1];
+    powers<DEG>(b1, b2, b3, p1, p2, p3);
+    int m = 0;
+#pragma unroll
+    for (int kk = 0; kk <= DEG; ++kk) {
+      const double t3 = p3[kk] * p.w;
+#pragma unroll
+      for (int jj = 0; jj <= DEG - kk; ++jj, ++m) w[m] = fma(p1[DEG - kk - jj] * p2[jj], t3, w[m]);
+    }
+  }
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    const double v = warp_sum(w[m]);
+    if (lane == 0) red[wp][m] = v;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < P; m += blockDim.x)
+    wpart[size_t(blockIdx.x) * P + m] = ((red[0][m] + red[1][m]) + red[2][m]) + red[3][m];
+}
+
+// w = sum of the node's chunk partials (in chunk order); w_hat = V^-T w.
+__global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const int2* __restrict__ chunk_range,
+                           const double* __restrict__ wpart, const double* __restrict__ vinv, int P,
+                           const int* __restrict__ pslot, int64_t N, double4* __restrict__ pts) {
+  extern __shared__ double ws[];
+  const int w = blockIdx.x;
+  if (w >= nw) return;
+  const int2 cr = chunk_range[w];
+  for (int m = threadIdx.x; m < P; m += blockDim.x) {
+    double s = 0.0;
+    for (int c = cr.x; c < cr.y; ++c) s += wpart[size_t(c) * P + m];
+    ws[m] = s;
+  }
+  __syncthreads();
+  const int64_t base = N + int64_t(pslot[weight_nodes[w]]) * P;
+  for (int kk = threadIdx.x; kk < P; kk += blockDim.x) {
+    double s = 0.0;
+    for (int m = 0; m < P; ++m) s = fma(vinv[size_t(m) * P + kk], ws[m], s);  // (V^-1)^T row kk
+    pts[base + kk].w = s;
+  }
+}
+
+// Phase 3: one block per fit node, one thread per proxy target.
+template <int KER>
+__global__ void k_fit_tiles(const Tile* __restrict__ tiles, int ntiles, const SrcRange* __restrict__ ranges,
+                            const double4* __restrict__ pts, const int* __restrict__ fit_nodes,
+                            const int* __restrict__ pslot, const double* __restrict__ vinv, int P,
+                            double* __restrict__ coeff) {
+  constexpr int D = KDim<KER>::D;
+  extern __shared__ double4 smem4[];
+  double4* buf = smem4;                                        // blockDim entries
+  double* phi = reinterpret_cast<double*>(smem4 + blockDim.x);  // D * P
+  const int tix = blockIdx.x;
+  if (tix >= ntiles) return;
+  const Tile T = tiles[tix];
+  const int tid = threadIdx.x;
+  const bool active = tid < T.tgt_count;
+  const double4 x = pts[T.tgt_begin + (active ? tid : 0)];
+  Acc<KER> a;
+  a.zero();
+  for (int r = T.list_begin; r < T.list_end; ++r) {
+    const SrcRange R = ranges[r];
+    for (int base = 0; base < R.count; base += blockDim.x) {
+      const int n = min(static_cast<int>(blockDim.x), R.count - base);
+      if (tid < n) buf[tid] = pts[R.begin + base + tid];
+      __syncthreads();
+#pragma unroll 4
+      for (int k = 0; k < n; ++k) pair_far<KER>(x.x, x.y, x.z, buf[k], a);
+      __syncthreads();
+    }
+  }
+  if (active) {
+    if constexpr (KER == kBS) {
+      phi[tid] = x.y * a.s[2] - x.z * a.s[1];
+      phi[P + tid] = x.z * a.s[0] - x.x * a.s[2];
+      phi[2 * P + tid] = x.x * a.s[1] - x.y * a.s[0];
+    } else {
+      phi[tid] = -kInv4Pi * a.s[0];
+    }
+  }
+  __syncthreads();
+  const int slot = pslot[fit_nodes[tix]];
+  for (int kk = tid; kk < P; kk += blockDim.x) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double s = 0.0;
+      for (int m = 0; m < P; ++m) s = fma(vinv[size_t(kk) * P + m], phi[d * P + m], s);
+      coeff[(size_t(slot) * D + d) * P + kk] = s;
+    }
+  }
+}
+
+// Phase 4 direct part: one warp per tile of <= 32 targets.
+template <int KER>
+__global__ void __launch_bounds__(128) k_leaf_tiles(const Tile* __restrict__ tiles, int ntiles,
+                                                    const SrcRange* __restrict__ ranges,
+                                                    const double4* __restrict__ pts, double* __restrict__ S,
+                                                    int* __restrict__ flags) {
+  constexpr int D = KDim<KER>::D;
+  __shared__ double4 buf[4][32];
+  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + wp;
+  if (t >= ntiles) return;
+  const Tile T = tiles[t];
+  const bool active = lane < T.tgt_count;
+  const int i = T.tgt_begin + (active ? lane : 0);
+  const double4 x = pts[i];
+  Acc<KER> a;
+  a.zero();
+  double4* b = buf[wp];
+  for (int r = T.list_begin; r < T.list_end; ++r) {
+    const SrcRange R = ranges[r];
+    for (int base = 0; base < R.count; base += 32) {
+      const int n = min(32, R.count - base);
+      if (lane < n) b[lane] = pts[R.begin + base + lane];
+      __syncwarp();
+      if (R.near) {
+        const int j0 = R.begin + base;
+#pragma unroll 4
+        for (int k = 0; k < n; ++k) pair_near<KER>(x.x, x.y, x.z, b[k], i, j0 + k, a, flags);
+      } else {
+#pragma unroll 4
+        for (int k = 0; k < n; ++k) pair_far<KER>(x.x, x.y, x.z, b[k], a);
+      }
+      __syncwarp();
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) S[size_t(i) * D + d] = a.s[d];
+  }
+}
+
+// Phase 4 downward part + finish.
+template <int KER, int DEG>
+__global__ void k_finish(int64_t n, const double4* __restrict__ pts, const double* __restrict__ S,
+                         const int* __restrict__ pos_leaf, const int* __restrict__ parent,
+                         const int* __restrict__ pslot, const unsigned char* __restrict__ is_fit,
+                         const double* __restrict__ cramer, const double* __restrict__ coeff,
+                         const int* __restrict__ perm, double* __restrict__ out) {
+  constexpr int D = KDim<KER>::D;
+  constexpr int P = Sbb<DEG>::P;
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double4 x = pts[k];
+  double val[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) val[d] = 0.0;
+  for (int a = pos_leaf[k]; a >= 0; a = parent[a]) {
+    if (!is_fit[a]) continue;
+    const double* c = coeff + size_t(pslot[a]) * D * P;
+    double b1, b2, b3;
+    bary(cramer + 12 * a, x.x, x.y, x.z, b1, b2, b3);
+    double p1[DEG + 1], p2[DEG + 1], p3[DEG + 1];
+    powers<DEG>(b1, b2, b3, p1, p2, p3);
+    int m = 0;
+#pragma unroll
+    for (int kk = 0; kk <= DEG; ++kk) {
+#pragma unroll
+      for (int jj = 0; jj <= DEG - kk; ++jj, ++m) {
+        const double B = p1[DEG - kk - jj] * p2[jj] * p3[kk];
+#pragma unroll
+        for (int d = 0; d < D; ++d) val[d] = fma(c[d * P + m], B, val[d]);
+      }
+    }
+  }
+  const int o = perm[k];
+  if constexpr (KER == kBS) {
+    const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
+    const double pref = -kInv4Pi;  // BiotSavartKernel::prefactor (kernels.hpp:54)
+    out[3 * size_t(o)] = pref * ((x.y * s2 - x.z * s1) + val[0]);
+    out[3 * size_t(o) + 1] = pref * ((x.z * s0 - x.x * s2) + val[1]);
+    out[3 * size_t(o) + 2] = pref * ((x.x * s1 - x.y * s0) + val[2]);
+  } else {
+    out[o] = -kInv4Pi * S[k] + val[0];
+  }
+}
+
+template <int KER>
+__global__ void k_direct_finish(int64_t n, const double4* __restrict__ pts, const double* __restrict__ S,
+                                double* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if constexpr (KER == kBS) {
+    const double4 x = pts[k];
+    const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
+    out[3 * k] = -kInv4Pi * (x.y * s2 - x.z * s1);
+    out[3 * k + 1] = -kInv4Pi * (x.z * s0 - x.x * s2);
+    out[3 * k + 2] = -kInv4Pi * (x.x * s1 - x.y * s0);
+  } else {
+    out[k] = -kInv4Pi * S[k];
+  }
+}
+
+__global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (n + 31) / 32;
+  if (t == 0) *range = SrcRange{0, static_cast<int>(n), 1, 0};
+  if (t >= nt) return;
+  const int64_t rem = n - t * 32;
+  tiles[t] = Tile{static_cast<int>(t * 32), static_cast<int>(rem < 32 ? rem : 32), 0, 1};
+}
+
+template <int KER>
+void launch_finish(Ctx& c, int degree, int64_t n, double* d_out) {
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  const int bs = 128;
+#define SSUM_FINISH_CASE(DG)                                                                                  \
+  case DG:                                                                                                   \
+    k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, B.pos_leaf.p, c.nodes.parent.p, \
+                                                             L.pslot.p, L.is_fit.p, c.nodes.cramer.p,        \
+                                                             c.coeff.p, B.perm.p, d_out);                    \
+    break;
+  switch (degree) {
+    SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
+    SSUM_FINISH_CASE(6) SSUM_FINISH_CASE(7) SSUM_FINISH_CASE(8) SSUM_FINISH_CASE(9) SSUM_FINISH_CASE(10)
+    SSUM_FINISH_CASE(11) SSUM_FINISH_CASE(12) SSUM_FINISH_CASE(13) SSUM_FINISH_CASE(14) SSUM_FINISH_CASE(15)
+    SSUM_FINISH_CASE(16) SSUM_FINISH_CASE(17) SSUM_FINISH_CASE(18) SSUM_FINISH_CASE(19) SSUM_FINISH_CASE(20)
+    default:
+      throw Error(SSUM_CONFIG, "degree out of range");
+  }
+#undef SSUM_FINISH_CASE
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+}
+
+void launch_up_partial(Ctx& c, int degree, int nchunks) {
+#define SSUM_UP_CASE(DG)                                                                          \
+  case DG:                                                                                        \
+    k_up_partial<DG><<<nchunks, 128, 0, c.stream>>>(c.wchunks.p, c.pts.p, c.nodes.cramer.p, c.wpart.p); \
+    break;
+  switch (degree) {
+    SSUM_UP_CASE(1) SSUM_UP_CASE(2) SSUM_UP_CASE(3) SSUM_UP_CASE(4) SSUM_UP_CASE(5) SSUM_UP_CASE(6)
+    SSUM_UP_CASE(7) SSUM_UP_CASE(8) SSUM_UP_CASE(9) SSUM_UP_CASE(10) SSUM_UP_CASE(11) SSUM_UP_CASE(12)
+    SSUM_UP_CASE(13) SSUM_UP_CASE(14) SSUM_UP_CASE(15) SSUM_UP_CASE(16) SSUM_UP_CASE(17) SSUM_UP_CASE(18)
+    SSUM_UP_CASE(19) SSUM_UP_CASE(20)
+    default:
+      throw Error(SSUM_CONFIG, "degree out of range");
+  }
+#undef SSUM_UP_CASE
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+}
+
+}  // namespace
+
+// V[m][k] = B_k(b_m) on the lattice (sbb.cpp:80-85), LU with partial pivoting,
+// explicit inverse; ConditioningError when the 1-norm reciprocal condition
+// number is not > 1e-12 (sbb.cpp:89-93).
+void ensure_vinv(Ctx& c, int degree) {
+  if (c.vinv_degree == degree) return;
+  const int P = (degree + 1) * (degree + 2) / 2;
+  std::vector<int> I(static_cast<size_t>(P)), J(static_cast<size_t>(P)), K(static_cast<size_t>(P));
+  {
+    int m = 0;
+    for (int k = 0; k <= degree; ++k)
+      for (int j = 0; j <= degree - k; ++j, ++m) {
+        I[m] = degree - k - j;
+        J[m] = j;
+        K[m] = k;
+      }
+  }
+  const double d = static_cast<double>(degree);
+  std::vector<double> V(size_t(P) * P), A;
+  for (int r = 0; r < P; ++r) {
+    const double b[3] = {I[r] / d, J[r] / d, K[r] / d};
+    for (int col = 0; col < P; ++col) {
+      double v = 1.0;
+      for (int e = 0; e < I[col]; ++e) v *= b[0];
+      double v2 = 1.0;
+      for (int e = 0; e < J[col]; ++e) v2 *= b[1];
+      double v3 = 1.0;
+      for (int e = 0; e < K[col]; ++e) v3 *= b[2];
+      V[size_t(r) * P + col] = v * v2 * v3;
+    }
+  }
+  A = V;
+  std::vector<int> perm(static_cast<size_t>(P));
+  for (int i = 0; i < P; ++i) perm[i] = i;
+  for (int k = 0; k < P; ++k) {
+    int piv = k;
+    double best = std::fabs(A[size_t(k) * P + k]);
+    for (int i = k + 1; i < P; ++i)
+      if (std::fabs(A[size_t(i) * P + k]) > best) {
+        best = std::fabs(A[size_t(i) * P + k]);
+        piv = i;
+      }
+    if (best == 0.0) throw Error(SSUM_CONDITIONING, "proxy Vandermonde is singular");
+    if (piv != k) {
+      for (int j = 0; j < P; ++j) std::swap(A[size_t(k) * P + j], A[size_t(piv) * P + j]);
+      std::swap(perm[k], perm[piv]);
+    }
+    for (int i = k + 1; i < P; ++i) {
+      A[size_t(i) * P + k] /= A[size_t(k) * P + k];
+      const double l = A[size_t(i) * P + k];
+      for (int j = k + 1; j < P; ++j) A[size_t(i) * P + j] -= l * A[size_t(k) * P + j];
+    }
+  }
+  std::vector<double> inv(size_t(P) * P);
+  std::vector<double> y(static_cast<size_t>(P));
+  for (int col = 0; col < P; ++col) {
+    for (int i = 0; i < P; ++i) y[i] = (perm[i] == col) ? 1.0 : 0.0;
+    for (int i = 0; i < P; ++i)
+      for (int k = 0; k < i; ++k) y[i] -= A[size_t(i) * P + k] * y[k];
+    for (int i = P - 1; i >= 0; --i) {
+      for (int k = i + 1; k < P; ++k) y[i] -= A[size_t(i) * P + k] * y[k];
+      y[i] /= A[size_t(i) * P + i];
+    }
+    for (int i = 0; i < P; ++i) inv[size_t(i) * P + col] = y[i];
+  }
+  double an = 0.0, in = 0.0;
+  for (int col = 0; col < P; ++col) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int r = 0; r < P; ++r) {
+      s1 += std::fabs(V[size_t(r) * P + col]);
+      s2 += std::fabs(inv[size_t(r) * P + col]);
+    }
+    an = std::max(an, s1);
+    in = std::max(in, s2);
+  }
+  const double rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
+  if (!(rcond > 1e-12))
+    throw Error(SSUM_CONDITIONING, "proxy Vandermonde too ill-conditioned (rcond " + std::to_string(rcond) + ")");
+  c.vinv.ensure(size_t(P) * P);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.vinv.p, inv.data(), inv.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.vinv_degree = degree;
+}
+
+void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q, int64_t n,
+              double* d_out, ssum_stats* st) {
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  const int degree = cfg.degree;
+  const int P = (degree + 1) * (degree + 2) / 2;
+  const int D = kernel == kBS ? 3 : 1;
+  if (n == 0) return;
+  ensure_vinv(c, degree);
+  const int64_t npts = n + int64_t(L.n_proxy) * P;
+  if (npts > 0x7fffffff) throw Error(SSUM_INVALID, "point count exceeds int32 indexing");
+  c.pts.ensure(size_t(npts));
+  c.S.ensure(size_t(n) * D);
+  c.coeff.ensure(std::max<size_t>(size_t(L.n_proxy) * D * P, 1));
+  const int bs = 256;
+
+  cudaEventRecord(c.ev[0], c.stream);
+  k_gather<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+  if (L.n_proxy > 0) {
+    k_proxy<<<grid_for(int64_t(L.n_proxy) * P, bs), bs, 0, c.stream>>>(c.trav.slot_node.p, L.n_proxy, degree,
+                                                                         c.nodes.tri.p, n, c.pts.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  cudaEventRecord(c.ev[1], c.stream);
+
+  // ---- upward pass: chunk table on the host (weight nodes and their bins)
+  if (L.n_weight > 0) {
+    const int kChunk = 1024;
+    std::vector<int4> chunks;
+    std::vector<int2> crange(static_cast<size_t>(L.n_weight));
+    for (int w = 0; w < L.n_weight; ++w) {
+      const int id = L.h_weight_nodes[w];
+      const int o = c.host.off[id], cn = c.host.cnt[id];
+      crange[w].x = static_cast<int>(chunks.size());
+      for (int b = 0; b < cn; b += kChunk) chunks.push_back(int4{id, o + b, std::min(kChunk, cn - b), 0});
+      crange[w].y = static_cast<int>(chunks.size());
+    }
+    const int nch = static_cast<int>(chunks.size());
+    c.wchunks.ensure(size_t(nch) + size_t(L.n_weight));
+    c.wpart.ensure(size_t(nch) * P);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.wchunks.p, chunks.data(), size_t(nch) * sizeof(int4), cudaMemcpyHostToDevice, c.stream));
+    int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(d_crange, crange.data(), crange.size() * sizeof(int2), cudaMemcpyHostToDevice, c.stream));
+    if (nch > 0) launch_up_partial(c, degree, nch);
+    const int bt = ((P + 31) / 32) * 32;
+    k_up_final<<<L.n_weight, bt, size_t(P) * 8, c.stream>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
+                                                             P, L.pslot.p, n, c.pts.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));  // host vectors above are released
+  }
+  cudaEventRecord(c.ev[2], c.stream);
+
+  // ---- CP/CC + fit
+  if (L.n_fit_tiles > 0) {
+    const int bt = ((P + 31) / 32) * 32;
+    const size_t sm = size_t(bt) * sizeof(double4) + size_t(D) * P * sizeof(double);
+    if (kernel == kBS)
+      k_fit_tiles<kBS><<<L.n_fit_tiles, bt, sm, c.stream>>>(L.fit_tiles.p, L.n_fit_tiles, L.fit_ranges.p, c.pts.p,
+                                                           L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
+    else
+      k_fit_tiles<kLOG><<<L.n_fit_tiles, bt, sm, c.stream>>>(L.fit_tiles.p, L.n_fit_tiles, L.fit_ranges.p, c.pts.p,
+                                                            L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  cudaEventRecord(c.ev[3], c.stream);
+
+  // ---- PP + PC
+  if (L.n_leaf_tiles > 0) {
+    const unsigned g = grid_for(L.n_leaf_tiles, 4);
+    if (kernel == kBS)
+      k_leaf_tiles<kBS><<<g, 128, 0, c.stream>>>(L.leaf_tiles.p, L.n_leaf_tiles, L.leaf_ranges.p, c.pts.p, c.S.p,
+                                                 c.d_flags.p);
+    else
+      k_leaf_tiles<kLOG><<<g, 128, 0, c.stream>>>(L.leaf_tiles.p, L.n_leaf_tiles, L.leaf_ranges.p, c.pts.p, c.S.p,
+                                                  c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  cudaEventRecord(c.ev[4], c.stream);
+
+  // ---- downward + finish
+  if (kernel == kBS)
+    launch_finish<kBS>(c, degree, n, d_out);
+  else
+    launch_finish<kLOG>(c, degree, n, d_out);
+  cudaEventRecord(c.ev[5], c.stream);
+  check_flags(c, "treecode_sum");
+  if (st) {
+    float ms[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ms[k], c.ev[k], c.ev[k + 1]);
+    st->upward_ms = ms[0] + ms[1];
+    st->cp_cc_fit_ms = ms[2];
+    st->pp_pc_ms = ms[3];
+    st->finish_ms = ms[4];
+  }
+}
+
+void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n, double* d_out) {
+  if (n == 0) return;
+  const int D = kernel == kBS ? 3 : 1;
+  const int64_t nt = (n + 31) / 32;
+  c.pts.ensure(size_t(n));
+  c.S.ensure(size_t(n) * D);
+  c.direct_tiles.ensure(size_t(nt));
+  c.direct_range.ensure(1);
+  const int bs = 256;
+  SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
+  k_gather<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, d_q, nullptr, n, c.pts.p);
+  k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
+  SSUM_LAUNCH_CHECK();
+  const unsigned g = grid_for(nt, 4);
+  if (kernel == kBS) {
+    k_leaf_tiles<kBS><<<g, 128, 0, c.stream>>>(c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p,
+                                               c.pts.p, c.S.p, c.d_flags.p);
+    k_direct_finish<kBS><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
+  } else {
+    k_leaf_tiles<kLOG><<<g, 128, 0, c.stream>>>(c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p,
+                                                c.pts.p, c.S.p, c.d_flags.p);
+    k_direct_finish<kLOG><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
+  }
+  SSUM_LAUNCH_CHECK();
+  c.launches += 4;
+  check_flags(c, "direct_sum");
+}
+
+}  // namespace ssum

@@ -1,0 +1,212 @@
+// Internal declarations shared by the .cu translation units of
+// libspheresum_b200.so: the context, device buffers, error plumbing, and the
+// pass entry points (tree build, traversal, evaluation).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spheresum_b200.h"
+#include "geom.cuh"
+
+namespace ssum {
+
+// Internal failure carrying an ssum_status; converted to a return code at the
+// C-ABI boundary (capi.cu). Never crosses extern "C".
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SSUM_CUDA_CHECK(x)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::ssum::Error(SSUM_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) +     \
+                                         " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define SSUM_LAUNCH_CHECK() SSUM_CUDA_CHECK(cudaGetLastError())
+
+constexpr int kMaxDegree = 20;  // kMaxSbbDegree (sbb.hpp:12)
+constexpr int kWarp = 32;
+constexpr double kSingularTol = 1e-14;  // kernels.hpp:13
+
+// Device error flags (bitmask in ctx.d_flags[0]).
+enum : int { kFlagGeometry = 1, kFlagSingular = 2 };
+
+// Growable device array. Contents are NOT preserved on growth unless keep.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n, bool keep = false, cudaStream_t s = 0) {
+    if (n <= cap) return;
+    size_t nc = cap ? cap : 1024;
+    while (nc < n) nc *= 2;
+    T* q = nullptr;
+    SSUM_CUDA_CHECK(cudaMalloc(&q, nc * sizeof(T)));
+    if (keep && p && cap) SSUM_CUDA_CHECK(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) {
+      if (keep) SSUM_CUDA_CHECK(cudaStreamSynchronize(s));
+      cudaFree(p);
+    }
+    p = q;
+    cap = nc;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Persistent node geometry (FaceTree::nodes_, face_tree.hpp:55). Index =
+// device node id (breadth-first allocation); the reference's depth-first ids
+// are reconstructed on export (tree_export in capi.cu).
+struct NodeTable {
+  int count = 0;            // nodes allocated
+  DBuf<double> tri;         // 9 per node: v1, v2, v3
+  DBuf<double> center;      // 3: circumcenter
+  DBuf<double> radius;      // 1
+  DBuf<double> cramer;      // 12: bc = v2 x v3 (3), det (1), n2 = v3 x v1, n3 = v1 x v2 (6), spare (2)
+  DBuf<int> level, parent, child_base, created_call;
+};
+
+// Host mirror of the node structure (ids, levels, links) plus this call's bin
+// counts/offsets. Geometry lives on the device only, except the 20 roots.
+struct HostTree {
+  std::vector<int> level, parent, child_base, created_call;
+  std::vector<int> cnt, off;
+};
+
+// Per-call binned tree (bins as contiguous ranges of the tree-order permutation).
+struct Binned {
+  int64_t n = 0;
+  int max_level = 0;
+  DBuf<int> cnt;            // particles per node
+  DBuf<int> off;            // first tree position of the node's bin
+  DBuf<unsigned char> act;  // per frontier node: 0 leaf, 1 descend
+  DBuf<int> cur;            // per particle: current node during the descent
+  DBuf<int> leaf_of;        // per particle (original order)
+  DBuf<int> perm;           // tree position -> original particle id
+  DBuf<int> pos_leaf;       // tree position -> leaf node
+  DBuf<int> sort_keys, sort_keys2, sort_vals;
+  DBuf<int> d_ids, d_cnt;
+  DBuf<int2> d_pairs;
+  std::vector<std::vector<int>> frontier;  // host copy: non-empty nodes per level (BFS)
+  std::vector<int> leaves;                 // host copy: non-empty leaves
+  DBuf<int> d_leaves;
+};
+
+struct Ctx;
+
+// One tile = up to 32 targets against a list of source ranges.
+struct Tile {
+  int tgt_begin;  // index into the unified point array
+  int tgt_count;  // <= 32
+  int list_begin, list_end;  // into the range list
+};
+// Source range in the unified point array. near != 0 marks a particle range
+// that may contain near-singular or self pairs (PP): the kernel takes the
+// reference-rounded slow path for pairs with 1 - x.y < kNearDen.
+struct SrcRange {
+  int begin;
+  int count;
+  int near;
+  int pad;
+};
+
+struct Lists {
+  int64_t n_inter = 0;
+  uint64_t counts[4] = {0, 0, 0, 0};
+  DBuf<int4> inter;          // emissions: (t, s, kind, 0)
+  DBuf<unsigned long long> key;  // depth-first order key of each emission
+  int n_proxy = 0;           // nodes carrying proxy points (weight or fit nodes)
+  int n_weight = 0, n_fit = 0;
+  DBuf<int> pslot;           // node -> proxy slot or -1
+  DBuf<unsigned char> is_weight, is_fit;
+  DBuf<int> weight_nodes, fit_nodes;  // slot-ordered node lists
+  std::vector<int> h_weight_nodes, h_fit_nodes;
+  int n_leaf_tiles = 0, n_fit_tiles = 0;
+  DBuf<Tile> leaf_tiles, fit_tiles;
+  int64_t n_leaf_ranges = 0, n_fit_ranges = 0;
+  DBuf<SrcRange> leaf_ranges, fit_ranges;
+  uint64_t evals[4] = {0, 0, 0, 0};
+};
+
+// Breadth-first traversal frontier entry: node pair plus depth-first order key.
+struct PairEntry {
+  int t, s;
+  unsigned long long key;
+  int step, pad;
+};
+
+struct TravScratch {
+  DBuf<PairEntry> F0, F1;
+  DBuf<int> action;
+  DBuf<unsigned long long> packed, scan;
+  DBuf<int> gkey, gkey2, gval, sorted_e;
+  DBuf<int2> seg;
+  DBuf<int> flag, flag_scan, slot_node;
+  DBuf<int> nr, nt, nr_off, nt_off;
+  DBuf<unsigned long long> counters;  // [0..3] kinds, [4..7] kernel evals
+};
+
+struct Ctx {
+  int device = 0;
+  TravScratch trav;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int call_index = 0;
+  HostTree host;
+  NodeTable nodes;
+  Binned bins;
+  Lists lists;
+  int64_t launches = 0;
+
+  // scratch
+  DBuf<int> d_flags;                 // [0] error bits
+  int* h_pinned = nullptr;           // small pinned host scratch (64 ints)
+  DBuf<unsigned char> cub_tmp;
+  DBuf<double4> pts;                 // unified points: N particles (tree order) + proxies
+  DBuf<double> S;                    // per tree position accumulated kernel sums (D doubles)
+  DBuf<double> coeff;                // per proxy slot: D x P fit coefficients
+  DBuf<double> wpart;                // upward partial sums
+  DBuf<int4> wchunks;                // upward chunks (slot, begin, count, node)
+  DBuf<double> vinv;                 // P x P inverse Vandermonde (row-major), per degree
+  int vinv_degree = -1;
+  DBuf<double> in_xyz, in_q, out_buf;  // staging for host-pointer entry points
+  DBuf<Tile> direct_tiles;
+  DBuf<SrcRange> direct_range;
+  DBuf<double> rk_state;             // RK4 scratch
+  double* h_stage = nullptr;         // pinned staging
+  size_t h_stage_bytes = 0;
+  cudaEvent_t ev[8];
+};
+
+// ---- passes (tree.cu / traversal.cu / eval.cu) ------------------------------
+void tree_init_roots(Ctx& c);
+void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
+void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
+void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,
+              int64_t n, double* d_out, ssum_stats* st);
+void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,
+                       double* d_out);
+void ensure_vinv(Ctx& c, int degree);
+void rk4_combine(Ctx& c, int stage, int64_t n, double dt, double omega, double* d_x0, double* d_z0,
+                 const double* d_area, double* d_xs, double* d_q, const double* d_u, double* d_kacc,
+                 double* d_kzacc);
+
+// sync + read the device error flags; throws the mapped Error
+void check_flags(Ctx& c, const char* where);
+
+inline unsigned grid_for(int64_t n, int block) { return static_cast<unsigned>((n + block - 1) / block); }
+
+}  // namespace ssum

@@ -1,0 +1,552 @@
+// Dual tree traversal and interaction-list compaction on the device.
+//
+// dual_traversal / traverse / classify / mac_well_separated
+// (treecode.cpp:22-77) are restated breadth-first: every step evaluates the
+// whole frontier of (target, source) node pairs at once. A pair is dropped
+// when either bin is empty (:42), emitted with classify()'s kind when
+// (r_t + r_s)/R < theta with R > 0 (:22-25, :43-45), emitted as PP when both
+// bins are <= N_T (:47-50), and otherwise the node with the larger bin (ties:
+// source, :52) is refined into its 4 children, or the pair falls back to PP
+// when that node has no children or sits at max_depth (:54-57). Each emitted
+// pair carries a depth-first order key (root pair, then 2 bits per
+// refinement) so the reference's emission order can be reproduced on export.
+//
+// The emitted list is then compacted into the evaluation layout:
+//   * leaf tiles  (<= 32 target particles each) with a list of source ranges
+//     gathered over the leaf's root-to-leaf path: PP ranges (particles of the
+//     source bin, contiguous in tree order) and PC ranges (the source node's
+//     proxy points) — treecode.cpp:366-396;
+//   * fit tiles   (the p proxy points of a CP/CC target node) with CP ranges
+//     (particles) and CC ranges (proxy points) — treecode.cpp:341-358;
+//   * proxy slots for every node that needs proxy points (PC/CC sources carry
+//     weights, CP/CC targets carry fit coefficients) — treecode.cpp:289-324.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace ssum {
+
+namespace {
+
+constexpr int kKeyStepBits = 2;
+constexpr int kKeyMaxSteps = 27;  // 9 bits root pair + 2 bits x 27 steps = 63 bits
+
+// classify (treecode.cpp:29-36); pc_only remaps CP -> PP and CC -> PC.
+__device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_only) {
+  const bool tb = nt_ > thr, sb = ns_ > thr;
+  int k = 0;
+  if (tb && sb) k = 3;
+  else if (sb) k = 1;
+  else if (tb) k = 2;
+  if (pc_only) {
+    if (k == 2) k = 0;
+    if (k == 3) k = 1;
+  }
+  return k;
+}
+
+// action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
+__global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* __restrict__ cnt,
+                            const double* __restrict__ center, const double* __restrict__ radius,
+                            const int* __restrict__ level, const int* __restrict__ child_base, double theta,
+                            int thr, int max_depth, int pc_only, int* __restrict__ action,
+                            unsigned long long* __restrict__ packed) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int t = F[k].t, s = F[k].s;
+  const int ct = cnt[t], cs = cnt[s];
+  int a = 0;
+  if (ct > 0 && cs > 0) {
+    const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
+    const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
+    const double R = arc_dist(a3, b3);
+    if (R > 0.0 && div_rn(add_rn(radius[t], radius[s]), R) < theta) {
+      a = 4 | classify_kind(ct, cs, thr, pc_only);
+    } else if (ct <= thr && cs <= thr) {
+      a = 4;  // PP
+    } else {
+      const bool rt = ct > cs;
+      const int r = rt ? t : s;
+      if (child_base[r] < 0 || level[r] >= max_depth)
+        a = 4;  // PP fallback
+      else
+        a = 8 | (rt ? 16 : 0);
+    }
+  }
+  action[k] = a;
+  const unsigned long long emit = (a & 4) ? 1ull : 0ull;
+  const unsigned long long kids = (a & 8) ? 4ull : 0ull;
+  packed[k] = (emit << 32) | kids;
+}
+
+__global__ void k_trav_scatter(const PairEntry* __restrict__ F, int m, const int* __restrict__ action,
+                               const unsigned long long* __restrict__ scan, const int* __restrict__ child_base,
+                               PairEntry* __restrict__ Fnext, int4* __restrict__ E,
+                               unsigned long long* __restrict__ K, long long e_base, int* flags) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int a = action[k];
+  if (!a) return;
+  const unsigned long long sc = scan[k];
+  const PairEntry p = F[k];
+  if (a & 4) {
+    const long long e = e_base + static_cast<long long>(sc >> 32);
+    E[e] = int4{p.t, p.s, a & 3, 0};
+    K[e] = p.key;
+  } else {
+    const int o = static_cast<int>(sc & 0xffffffffull);
+    const bool rt = (a & 16) != 0;
+    const int cb = child_base[rt ? p.t : p.s];
+    const int step = p.step + 1;
+    if (step > kKeyMaxSteps) atomicOr(flags, 4);  // order keys saturated (export only)
+    const int shift = 54 - kKeyStepBits * min(step, kKeyMaxSteps);
+    for (int q = 0; q < 4; ++q) {
+      PairEntry c;
+      c.t = rt ? cb + q : p.t;
+      c.s = rt ? p.s : cb + q;
+      c.key = p.key | (static_cast<unsigned long long>(q) << shift);
+      c.step = step;
+      c.pad = 0;
+      Fnext[o + q] = c;
+    }
+  }
+}
+
+__global__ void k_root_pairs(PairEntry* F) {
+  const int k = threadIdx.x + blockIdx.x * blockDim.x;
+  if (k >= 400) return;
+  PairEntry p;
+  p.t = k / 20;
+  p.s = k % 20;
+  p.key = static_cast<unsigned long long>(k) << 54;
+  p.step = 0;
+  p.pad = 0;
+  F[k] = p;
+}
+
+// Node flags from the emitted list (treecode.cpp:295-317).
+__global__ void k_mark(const int4* __restrict__ E, long long ne, unsigned char* is_weight, unsigned char* is_fit,
+                       int* group_key, int* group_val, unsigned long long* kind_counts) {
+  __shared__ unsigned long long sc[4];
+  if (threadIdx.x < 4) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < ne) {
+    const int4 it = E[e];
+    const int kind = it.z;
+    if (kind == 1 || kind == 3) is_weight[it.y] = 1;
+    if (kind == 2 || kind == 3) is_fit[it.x] = 1;
+    group_key[e] = 2 * it.x + ((kind >= 2) ? 1 : 0);
+    group_val[e] = static_cast<int>(e);
+    atomicAdd(&sc[kind], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && sc[threadIdx.x]) atomicAdd(&kind_counts[threadIdx.x], sc[threadIdx.x]);
+}
+
+__global__ void k_slot_flags(const unsigned char* is_weight, const unsigned char* is_fit, int nn, int* flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nn) flag[k] = (is_weight[k] | is_fit[k]) ? 1 : 0;
+}
+
+__global__ void k_slots(const int* __restrict__ flag, const int* __restrict__ scan, int nn,
+                        const unsigned char* is_weight, const unsigned char* is_fit, int* pslot,
+                        int* slot_node) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nn) return;
+  if (flag[k]) {
+    pslot[k] = scan[k];
+    slot_node[scan[k]] = k;
+  } else {
+    pslot[k] = -1;
+  }
+}
+
+// Segment bounds of the sorted group keys (key = 2*node + class, class 1 = CP/CC):
+// seg[key] = (begin, end) into the sorted emission order.
+__global__ void k_seg_bounds(const int* __restrict__ keys, long long ne, int2* seg) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const int k = keys[i];
+  if (i == 0 || keys[i - 1] != k) seg[k].x = static_cast<int>(i);
+  if (i == ne - 1 || keys[i + 1] != k) seg[k].y = static_cast<int>(i + 1);
+}
+
+// Per leaf: number of PP/PC ranges over its root-to-leaf path, and tiles.
+__global__ void k_leaf_count(const int* __restrict__ leaves, int nl, const int* __restrict__ parent,
+                             const int2* __restrict__ seg, const int* __restrict__ cnt, int* n_ranges,
+                             int* n_tiles) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
+  const int leaf = leaves[k];
+  int r = 0;
+  for (int a = leaf; a >= 0; a = parent[a]) {
+    const int2 sg = seg[2 * a];
+    r += sg.y - sg.x;
+  }
+  n_ranges[k] = r;
+  n_tiles[k] = (cnt[leaf] + kWarp - 1) / kWarp;
+}
+
+__global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* __restrict__ parent,
+                            const int2* __restrict__ seg, const int* __restrict__ sorted_e,
+                            const int4* __restrict__ E, const int* __restrict__ cnt, const int* __restrict__ off,
+                            const int* __restrict__ pslot, const int* __restrict__ range_off,
+                            const int* __restrict__ tile_off, int64_t N, int P, SrcRange* __restrict__ ranges,
+                            Tile* __restrict__ tiles, unsigned long long* __restrict__ evals) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long pp = 0, pc = 0;
+  if (k < nl) {
+    const int leaf = leaves[k];
+    int path[48];
+    int pl = 0;
+    for (int a = leaf; a >= 0 && pl < 48; a = parent[a]) path[pl++] = a;
+    int w = range_off[k];
+    const int w0 = w;
+    unsigned long long src_pp = 0, src_pc = 0;
+    for (int q = pl - 1; q >= 0; --q) {  // root to leaf (treecode.cpp:379,392)
+      const int2 sg = seg[2 * path[q]];
+      for (int i = sg.x; i < sg.y; ++i) {
+        const int4 it = E[sorted_e[i]];
+        SrcRange r;
+        if (it.z == 0) {
+          r.begin = off[it.y];
+          r.count = cnt[it.y];
+          r.near = 1;
+          src_pp += static_cast<unsigned long long>(r.count);
+        } else {
+          r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
+          r.count = P;
+          r.near = 0;
+          src_pc += static_cast<unsigned long long>(P);
+        }
+        r.pad = 0;
+        ranges[w++] = r;
+      }
+    }
+    const int c = cnt[leaf];
+    const int nt = (c + kWarp - 1) / kWarp;
+    for (int j = 0; j < nt; ++j) {
+      Tile t;
+      t.tgt_begin = off[leaf] + j * kWarp;
+      t.tgt_count = min(kWarp, c - j * kWarp);
+      t.list_begin = w0;
+      t.list_end = w;
+      tiles[tile_off[k] + j] = t;
+    }
+    pp = static_cast<unsigned long long>(c) * src_pp - static_cast<unsigned long long>(c);  // self pairs excluded
+    pc = static_cast<unsigned long long>(c) * src_pc;
+  }
+  typedef cub::BlockReduce<unsigned long long, 128> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long spp = BR(tmp).Sum(pp);
+  __syncthreads();
+  const unsigned long long spc = BR(tmp).Sum(pc);
+  if (threadIdx.x == 0) {
+    atomicAdd(&evals[0], spp);
+    atomicAdd(&evals[1], spc);
+  }
+}
+
+__global__ void k_fit_count(const int* __restrict__ fit_nodes, int nf, const int2* __restrict__ seg, int* n_ranges) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nf) return;
+  const int2 sg = seg[2 * fit_nodes[k] + 1];
+  n_ranges[k] = sg.y - sg.x;
+}
+
+__global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2* __restrict__ seg,
+                           const int* __restrict__ sorted_e, const int4* __restrict__ E, const int* __restrict__ cnt,
+                           const int* __restrict__ off, const int* __restrict__ pslot,
+                           const int* __restrict__ range_off, int64_t N, int P, SrcRange* __restrict__ ranges,
+                           Tile* __restrict__ tiles, unsigned long long* __restrict__ evals) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cp = 0, cc = 0;
+  if (k < nf) {
+    const int t = fit_nodes[k];
+    const int2 sg = seg[2 * t + 1];
+    int w = range_off[k];
+    const int w0 = w;
+    for (int i = sg.x; i < sg.y; ++i) {  // emission order (treecode.cpp:347)
+      const int4 it = E[sorted_e[i]];
+      SrcRange r;
+      if (it.z == 2) {
+        r.begin = off[it.y];
+        r.count = cnt[it.y];
+        cp += static_cast<unsigned long long>(P) * static_cast<unsigned long long>(r.count);
+      } else {
+        r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
+        r.count = P;
+        cc += static_cast<unsigned long long>(P) * static_cast<unsigned long long>(P);
+      }
+      r.near = 0;
+      r.pad = 0;
+      ranges[w++] = r;
+    }
+    Tile tl;
+    tl.tgt_begin = static_cast<int>(N + static_cast<int64_t>(pslot[t]) * P);
+    tl.tgt_count = P;
+    tl.list_begin = w0;
+    tl.list_end = w;
+    tiles[k] = tl;
+  }
+  typedef cub::BlockReduce<unsigned long long, 128> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long scp = BR(tmp).Sum(cp);
+  __syncthreads();
+  const unsigned long long scc = BR(tmp).Sum(cc);
+  if (threadIdx.x == 0) {
+    atomicAdd(&evals[2], scp);
+    atomicAdd(&evals[3], scc);
+  }
+}
+
+template <class T>
+void exclusive_scan(Ctx& c, const T* in, T* out, int64_t n) {
+  size_t tmp = 0;
+  SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int>(n), c.stream));
+  c.cub_tmp.ensure(tmp);
+  SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, tmp, in, out, static_cast<int>(n), c.stream));
+  c.launches += 2;
+}
+
+}  // namespace
+
+static TravScratch& scratch(Ctx& c) { return c.trav; }
+
+void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys) {
+  (void)keep_order_keys;
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  TravScratch& S = scratch(c);
+  const int nn = c.nodes.count;
+  const int64_t N = B.n;
+  const int P = (cfg.degree + 1) * (cfg.degree + 2) / 2;
+  const int bs = 256;
+  L.n_inter = 0;
+  for (int k = 0; k < 4; ++k) L.counts[k] = L.evals[k] = 0;
+  L.n_proxy = L.n_weight = L.n_fit = L.n_leaf_tiles = L.n_fit_tiles = 0;
+  L.n_leaf_ranges = L.n_fit_ranges = 0;
+  if (N == 0) return;
+
+  // ---- breadth-first traversal
+  S.F0.ensure(400);
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+  int m = 400;
+  long long ne = 0;
+  L.inter.ensure(1 << 16);
+  L.key.ensure(1 << 16);
+  while (m > 0) {
+    S.action.ensure(size_t(m));
+    S.packed.ensure(size_t(m));
+    S.scan.ensure(size_t(m));
+    k_trav_eval<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
+                                                       c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
+                                                       cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
+                                                       S.packed.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    exclusive_scan(c, S.packed.p, S.scan.p, m);
+    unsigned long long tail[2];
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[0], S.scan.p + (m - 1), 8, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[1], S.packed.p + (m - 1), 8, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    const unsigned long long tot = tail[0] + tail[1];
+    const int next = static_cast<int>(tot & 0xffffffffull);
+    const long long emitted = static_cast<long long>(tot >> 32);
+    L.inter.ensure(size_t(ne + emitted), true, c.stream);
+    L.key.ensure(size_t(ne + emitted), true, c.stream);
+    S.F1.ensure(size_t(std::max(next, 1)));
+    k_trav_scatter<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, m, S.action.p, S.scan.p, c.nodes.child_base.p,
+                                                          S.F1.p, L.inter.p, L.key.p, ne, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    ne += emitted;
+    std::swap(S.F0, S.F1);
+    m = next;
+  }
+  L.n_inter = ne;
+
+  // ---- node flags, kind counts, grouping by (target, class)
+  L.is_weight.ensure(size_t(nn));
+  L.is_fit.ensure(size_t(nn));
+  L.pslot.ensure(size_t(nn));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_weight.p, 0, size_t(nn), c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_fit.p, 0, size_t(nn), c.stream));
+  S.counters.ensure(8);
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), c.stream));
+  const size_t nes = size_t(std::max<long long>(ne, 1));
+  S.gkey.ensure(nes);
+  S.gkey2.ensure(nes);
+  S.gval.ensure(nes);
+  S.sorted_e.ensure(nes);
+  if (ne > 0) {
+    k_mark<<<grid_for(ne, bs), bs, 0, c.stream>>>(L.inter.p, ne, L.is_weight.p, L.is_fit.p, S.gkey.p, S.gval.p,
+                                                   S.counters.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) < 2 * int64_t(nn)) ++end_bit;
+    size_t tmp = 0;
+    SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, S.gkey.p, S.gkey2.p, S.gval.p, S.sorted_e.p,
+                                                    static_cast<int>(ne), 0, end_bit, c.stream));
+    c.cub_tmp.ensure(tmp);
+    SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, tmp, S.gkey.p, S.gkey2.p, S.gval.p, S.sorted_e.p,
+                                                    static_cast<int>(ne), 0, end_bit, c.stream));
+    c.launches += 4;
+  }
+  S.seg.ensure(size_t(2) * nn);
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.seg.p, 0, size_t(2) * nn * sizeof(int2), c.stream));
+  if (ne > 0) {
+    k_seg_bounds<<<grid_for(ne, bs), bs, 0, c.stream>>>(S.gkey2.p, ne, S.seg.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+
+  // ---- proxy slots (weight or fit nodes), slot-ordered node lists
+  S.flag.ensure(size_t(nn));
+  S.flag_scan.ensure(size_t(nn));
+  S.slot_node.ensure(size_t(nn));
+  k_slot_flags<<<grid_for(nn, bs), bs, 0, c.stream>>>(L.is_weight.p, L.is_fit.p, nn, S.flag.p);
+  SSUM_LAUNCH_CHECK();
+  exclusive_scan(c, S.flag.p, S.flag_scan.p, nn);
+  k_slots<<<grid_for(nn, bs), bs, 0, c.stream>>>(S.flag.p, S.flag_scan.p, nn, L.is_weight.p, L.is_fit.p, L.pslot.p,
+                                                  S.slot_node.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches += 2;
+  {
+    int tail[2];
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[0], S.flag_scan.p + (nn - 1), 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[1], S.flag.p + (nn - 1), 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    L.n_proxy = tail[0] + tail[1];
+  }
+  // weight / fit node lists in slot order (host-side compaction of the slot table)
+  {
+    std::vector<int> slot_node(static_cast<size_t>(std::max(L.n_proxy, 1)));
+    std::vector<unsigned char> w(static_cast<size_t>(nn)), f(static_cast<size_t>(nn));
+    if (L.n_proxy > 0)
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(slot_node.data(), S.slot_node.p, size_t(L.n_proxy) * 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(w.data(), L.is_weight.p, size_t(nn), cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(f.data(), L.is_fit.p, size_t(nn), cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    std::vector<int> wn, fn;
+    for (int s = 0; s < L.n_proxy; ++s) {
+      const int id = slot_node[s];
+      if (w[id]) wn.push_back(id);
+      if (f[id]) fn.push_back(id);
+    }
+    L.h_weight_nodes = wn;
+    L.h_fit_nodes = fn;
+    L.n_weight = static_cast<int>(wn.size());
+    L.n_fit = static_cast<int>(fn.size());
+    L.weight_nodes.ensure(std::max<size_t>(wn.size(), 1));
+    L.fit_nodes.ensure(std::max<size_t>(fn.size(), 1));
+    if (!wn.empty())
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(L.weight_nodes.p, wn.data(), wn.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    if (!fn.empty())
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(L.fit_nodes.p, fn.data(), fn.size() * 4, cudaMemcpyHostToDevice, c.stream));
+  }
+
+  // ---- leaf tiles
+  const int nl = static_cast<int>(B.leaves.size());
+  S.nr.ensure(size_t(nl) + 1);
+  S.nt.ensure(size_t(nl) + 1);
+  S.nr_off.ensure(size_t(nl) + 1);
+  S.nt_off.ensure(size_t(nl) + 1);
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.nr.p + nl, 0, 4, c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.nt.p + nl, 0, 4, c.stream));
+  k_leaf_count<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, B.cnt.p, S.nr.p,
+                                                         S.nt.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+  exclusive_scan(c, S.nr.p, S.nr_off.p, nl + 1);
+  exclusive_scan(c, S.nt.p, S.nt_off.p, nl + 1);
+  {
+    int tot[2];
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot[0], S.nr_off.p + nl, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot[1], S.nt_off.p + nl, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    L.n_leaf_ranges = tot[0];
+    L.n_leaf_tiles = tot[1];
+  }
+  L.leaf_ranges.ensure(size_t(std::max<int64_t>(L.n_leaf_ranges, 1)));
+  L.leaf_tiles.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
+  k_leaf_fill<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
+                                                        L.inter.p, B.cnt.p, B.off.p, L.pslot.p, S.nr_off.p, S.nt_off.p,
+                                                        N, P, L.leaf_ranges.p, L.leaf_tiles.p, S.counters.p + 4);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+
+  // ---- fit tiles
+  const int nf = L.n_fit;
+  if (nf > 0) {
+    S.nr.ensure(size_t(nf) + 1);
+    S.nr_off.ensure(size_t(nf) + 1);
+    SSUM_CUDA_CHECK(cudaMemsetAsync(S.nr.p + nf, 0, 4, c.stream));
+    k_fit_count<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.nr.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    exclusive_scan(c, S.nr.p, S.nr_off.p, nf + 1);
+    int tot = 0;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot, S.nr_off.p + nf, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    L.n_fit_ranges = tot;
+    L.fit_ranges.ensure(size_t(std::max(tot, 1)));
+    L.fit_tiles.ensure(size_t(nf));
+    k_fit_fill<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.sorted_e.p, L.inter.p, B.cnt.p,
+                                                         B.off.p, L.pslot.p, S.nr_off.p, N, P, L.fit_ranges.p,
+                                                         L.fit_tiles.p, S.counters.p + 4);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  L.n_fit_tiles = nf;
+  unsigned long long h[8];
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, S.counters.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  for (int k = 0; k < 4; ++k) {
+    L.counts[k] = h[k];
+    L.evals[k] = h[4 + k];
+  }
+}
+
+// Export helper: the emitted list sorted into depth-first (reference) order.
+void sorted_interactions(Ctx& c, std::vector<int4>& out) {
+  Lists& L = c.lists;
+  TravScratch& S = scratch(c);
+  out.clear();
+  const long long ne = L.n_inter;
+  if (ne == 0) return;
+  int fl = 0;
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(&fl, c.d_flags.p, 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (fl & 4) throw Error(SSUM_INTERNAL, "dual_traversal export: refinement depth exceeds the order-key width");
+  DBuf<unsigned long long> k2;
+  DBuf<int> v2;
+  k2.ensure(size_t(ne));
+  v2.ensure(size_t(ne));
+  // values: emission index
+  std::vector<int> idx(static_cast<size_t>(ne));
+  for (long long e = 0; e < ne; ++e) idx[size_t(e)] = static_cast<int>(e);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.gval.p, idx.data(), size_t(ne) * 4, cudaMemcpyHostToDevice, c.stream));
+  size_t tmp = 0;
+  SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, L.key.p, k2.p, S.gval.p, v2.p, static_cast<int>(ne), 0,
+                                                  64, c.stream));
+  c.cub_tmp.ensure(tmp);
+  SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, tmp, L.key.p, k2.p, S.gval.p, v2.p, static_cast<int>(ne),
+                                                  0, 64, c.stream));
+  std::vector<int4> E(static_cast<size_t>(ne));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(E.data(), L.inter.p, size_t(ne) * sizeof(int4), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(idx.data(), v2.p, size_t(ne) * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  k2.release();
+  v2.release();
+  out.resize(size_t(ne));
+  for (long long e = 0; e < ne; ++e) out[size_t(e)] = E[size_t(idx[size_t(e)])];
+}
+
+}  // namespace ssum
