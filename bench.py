@@ -1,0 +1,310 @@
+"""Benchmark: BVE tree-code velocity evaluations/s at N = 2,621,442 (fp64).
+
+Workload (BASELINE.json config 4, one velocity evaluation = one "step"):
+level-9 icosahedral mesh (N = 2,621,442 vertices), BASELINE Rossby-Haurwitz
+R=4 vorticity, Voronoi (node-patch) areas, q = zeta * A; Biot-Savart kernel,
+interpolation degree 8, theta = 0.7, N_T = 64, max_depth = 10. A step is the
+whole treecode_sum: face-tree binning, dual traversal and list compaction,
+upward pass, CP/CC + fit, PP + PC, downward pass — nothing cached between
+steps except the persistent tree geometry (FaceTree semantics).
+
+  value : velocity evals/s with inputs resident in HBM (device pointers),
+          device time per step from CUDA events, L2 flushed between steps.
+  e2e   : the same through the C-ABI host-pointer entry point
+          (ssum_treecode_sum) from pinned host buffers: H2D of xyz+q and D2H
+          of the velocities inside every timed step.
+  roofline : dominant kernel (k_leaf_tiles: PP + PC pairs) — algorithmic
+          flops (13 per pair) / its event-timed duration,
+          against the DFMA peak measured live on this GPU (no fp64 entry in
+          MEASURED_PEAKS.json).
+  cpu_baseline : the unmodified reference (oracle/_ref, compiled from
+          /root/reference/proj/src) on the same input, all host threads.
+
+`--impl reference` times that reference CPU path alone (rank 0).
+Multi-GPU (torchrun): target leaves are partitioned across ranks by
+interaction cost (strong scaling); every rank builds the tree.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "BVE tree-code velocity evals/s (N=2.6M, fp64)"
+UNIT = "velocity_evals/s"
+LEVEL = 9
+CFG = dict(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+WORKLOAD = ("config4: L9 icosahedral mesh N=2,621,442, BASELINE RH4 vorticity, Voronoi areas, "
+            "Biot-Savart, d=8, theta=0.7, N_T=64, max_depth=10; one full treecode_sum per step")
+FLOP_PER_PAIR = 13  # F_BS
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def fixture():
+    import paper_2401_07361_b200 as ss
+
+    xyz, area = ss.make_icosa_mesh(LEVEL)
+    q = ss.rh4_vorticity(xyz) * area
+    return xyz, q, area
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+def reference_step(ol, xyz, q, workers):
+    t0 = time.perf_counter()
+    out, st = ol.ref_treecode(0, xyz, q, CFG["theta"], CFG["n_threshold"], CFG["degree"], CFG["max_depth"],
+                              workers)
+    return time.perf_counter() - t0, out, st
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle_lib as ol
+
+    if not ol.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libspheresum_ref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    xyz, q, area = fixture()
+    n = xyz.shape[0]
+    # warm-up on a level-5 sample (threads, page cache, lattice_fit cache)
+    import paper_2401_07361_b200 as ss
+
+    wx, wa = ss.make_icosa_mesh(5)
+    wq = ss.rh4_vorticity(wx) * wa
+    for _ in range(args.warmup):
+        ol.ref_treecode(0, wx, wq, CFG["theta"], CFG["n_threshold"], CFG["degree"], CFG["max_depth"], cores)
+    times = []
+    budget = 240.0
+    for k in range(args.steps):
+        dt, _, _ = reference_step(ol, xyz, q, cores)
+        times.append(dt)
+        if sum(times) > budget and k + 1 < args.steps:
+            break
+    ms = 1e3 * statistics.mean(times)
+    value = n / (ms * 1e-3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, **CFG, "n": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"full config-4 treecode_sum per step ({len(times)} timed of {args.steps} "
+                                   f"requested, 240 s budget); warm-up steps on a level-5 mesh"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_2401_07361_b200 as ss
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    xyz, q, area = fixture()
+    n = xyz.shape[0]
+    cfg = ss.TraversalConfig(**CFG)
+    dev = torch.device("cuda", local)
+    d_xyz = torch.from_numpy(xyz).to(dev)
+    d_q = torch.from_numpy(q).to(dev)
+    d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    tree = ss.FaceTree(local)
+    tree.set_stream(stream.cuda_stream)
+    if ws > 1:
+        tree.set_partition(rank, ws)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def step(st):
+        ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
+                               d_out.data_ptr(), stats=st)
+
+    for _ in range(max(args.warmup, 3)):
+        step(ss.TreecodeStats())
+    torch.cuda.synchronize()
+    peak = tree.fp64_peak_tflops(5)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    times, pp_ms, launches = [], [], 0
+    stats = None
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            stats = ss.TreecodeStats()
+            step(stats)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            pp_ms.append(stats.pp_pc_ms)
+            launches += stats.gpu_launches
+        barrier()
+    total_ms = sum(times)
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n / (ms_per_step * 1e-3)
+
+    # e2e through the host-pointer C-ABI entry point with pinned buffers
+    h_xyz = torch.from_numpy(xyz).pin_memory()
+    h_q = torch.from_numpy(q).pin_memory()
+    h_out = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
+    e2e_times = []
+    ctree = tree
+    for k in range(min(args.steps, 5) + 1):
+        barrier()
+        t0 = time.perf_counter()
+        ss.treecode_sum(ss.BiotSavartKernel, h_xyz.numpy(), h_q.numpy(), cfg, tree=ctree, out=h_out.numpy())
+        dt = time.perf_counter() - t0
+        if k > 0:
+            e2e_times.append(dt)
+    e2e_s = statistics.mean(e2e_times)
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    pairs = stats.kernel_evals[0] + stats.kernel_evals[1]
+    avg_pp_ms = statistics.mean(pp_ms)
+    achieved = FLOP_PER_PAIR * pairs / (avg_pp_ms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "leaf_tiles_dram.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    all_evals = sum(stats.kernel_evals)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, **CFG, "n": n, "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"target-leaf partition x{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "fp64", "kernel": "k_leaf_tiles (PP+PC)", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": "DFMA-chain probe on this GPU (ssum_fp64_peak); MEASURED_PEAKS.json has no fp64",
+                     "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": pairs, "avg_launch_ms": avg_pp_ms},
+        "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xyz.nbytes + q.nbytes),
+                "d2h_bytes_per_step": int(n * 3 * 8), "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": launches,
+        "interactions_per_s": all_evals / (ms_per_step * 1e-3),
+        "all_kernel_flops_frac": FLOP_PER_PAIR * all_evals / (ms_per_step * 1e-3) / 1e12 / peak,
+        "phase_ms": {"bin": stats.bin_seconds * 1e3, "traversal": stats.traversal_seconds * 1e3,
+                     "eval": stats.eval_seconds * 1e3, "upward": stats.upward_ms, "cp_cc_fit": stats.cp_cc_fit_ms,
+                     "pp_pc": stats.pp_pc_ms, "downward_finish": stats.finish_ms},
+        "kernel_evals": {"pp": stats.kernel_evals[0], "pc": stats.kernel_evals[1], "cp": stats.kernel_evals[2],
+                         "cc": stats.kernel_evals[3]},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle_lib as ol
+
+        if ol.ref_available():
+            cores = os.cpu_count() or 1
+            dt, ref_out, _ = reference_step(ol, xyz, q, cores)
+            mine = h_out.numpy()
+            line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                                    "sample": "one full config-4 treecode_sum (unmodified reference, "
+                                              f"workers={cores}), {dt:.1f} s"}
+            line["parity_rel_l2_vs_reference"] = ol.rel_l2(mine, ref_out)
+        else:
+            line["cpu_baseline"] = None
+    if rank == 0:
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

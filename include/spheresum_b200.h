@@ -124,6 +124,18 @@ int ssum_tree_export(ssum_ctx* ctx, int* level, int* parent, int* child_base, do
 int ssum_dual_traversal(ssum_ctx* ctx, const ssum_config* cfg, int* tsk, int64_t cap,
                         int64_t* count);
 
+/* ---- multi-GPU target partition (no reference equivalent) */
+/* Subsequent treecode evaluations compute only part `part` of `nparts`
+ * cost-balanced contiguous ranges of target leaves (tree order) and write only
+ * those rows of the output; the tree build and upward pass are replicated.
+ * The union over parts is bitwise the nparts = 1 result. */
+int ssum_set_partition(ssum_ctx* ctx, int part, int nparts);
+/* Tree-position range [begin, end) of the last evaluation's part. */
+int ssum_partition_range(ssum_ctx* ctx, int64_t* begin, int64_t* end);
+/* Copy the last binning's permutation (tree position -> caller's particle
+ * index, N ints) into dst, a device pointer if on_device != 0. */
+int ssum_tree_perm(ssum_ctx* ctx, int* dst, int on_device);
+
 /* ---- Lagrangian RK4 (absent from the reference code) ---- */
 /* In place on host arrays: xyz (N x 3), zeta (N); area (N) fixed. Each stage
  * evaluates u with treecode_sum<BiotSavartKernel> (direct_sum if direct != 0)
@@ -132,6 +144,11 @@ int ssum_dual_traversal(ssum_ctx* ctx, const ssum_config* cfg, int* tsk, int64_t
 int ssum_rk4(ssum_ctx* ctx, const ssum_config* cfg, double* xyz, double* zeta,
              const double* area, int64_t n, double dt, int steps, double omega, int direct,
              ssum_stats* stats);
+
+/* ---- measurement --------------------------------------------------------- */
+/* FP64 roofline denominator: DFMA-chain throughput of this device in TFLOP/s
+ * (best of `reps` launches). MEASURED_PEAKS.json has no fp64 entry. */
+int ssum_fp64_peak(ssum_ctx* ctx, int reps, double* tflops);
 
 /* ---- fixtures (BASELINE.json configs; host-side generators) -------------- */
 /* make_icosa_mesh(level).vertices() / node_patch_areas() (icosa_mesh.cpp:37-133). */

@@ -45,7 +45,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "lib", "libspheresum_b200.so")
+    """lib/libspheresum_b200.so, or $SSUM_LIBRARY (tuning variants)."""
+    return os.environ.get("SSUM_LIBRARY") or os.path.join(_HERE, "lib", "libspheresum_b200.so")
 
 
 # ----------------------------------------------------------------- errors
@@ -106,7 +107,8 @@ EXPORTED_SYMBOLS = (
     "ssum_treecode_sum", "ssum_treecode_sum_device", "ssum_direct_sum", "ssum_direct_sum_device",
     "ssum_bin_particles", "ssum_tree_node_count", "ssum_tree_export", "ssum_dual_traversal",
     "ssum_rk4", "ssum_mesh_vertex_count", "ssum_make_icosa_mesh", "ssum_rh4_vorticity",
-    "ssum_make_random_cap",
+    "ssum_make_random_cap", "ssum_fp64_peak", "ssum_set_partition", "ssum_partition_range",
+    "ssum_tree_perm",
 )
 
 
@@ -143,6 +145,10 @@ def load_library():
         "ssum_make_icosa_mesh": (ctypes.c_int, [ctypes.c_int, _P, _P]),
         "ssum_rh4_vorticity": (ctypes.c_int, [_P, _I64, _P]),
         "ssum_make_random_cap": (ctypes.c_int, [_I64, ctypes.c_uint64, _P, _P, _P]),
+        "ssum_fp64_peak": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+        "ssum_set_partition": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
+        "ssum_partition_range": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+        "ssum_tree_perm": (ctypes.c_int, [_P, _P, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -332,6 +338,33 @@ class FaceTree:
     def handle(self):
         return self._h
 
+    def fp64_peak_tflops(self, reps: int = 5) -> float:
+        """Measured DFMA throughput of this device (the FP64 roofline denominator)."""
+        v = ctypes.c_double()
+        self._check(self._lib.ssum_fp64_peak(self._h, int(reps), ctypes.byref(v)))
+        return v.value
+
+    def set_partition(self, part: int, nparts: int) -> None:
+        """Compute only part `part` of `nparts` cost-balanced target ranges
+        (multi-GPU strong scaling); see include/spheresum_b200.h."""
+        self._check(self._lib.ssum_set_partition(self._h, int(part), int(nparts)))
+
+    def partition_range(self) -> Tuple[int, int]:
+        b, e = _I64(), _I64()
+        self._check(self._lib.ssum_partition_range(self._h, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
+    def perm(self, device_ptr: Optional[int] = None) -> Optional[np.ndarray]:
+        """Tree position -> particle index of the last binning (host copy, or
+        into a device buffer when device_ptr is given)."""
+        if device_ptr is not None:
+            self._check(self._lib.ssum_tree_perm(self._h, ctypes.c_void_p(device_ptr), 1))
+            return None
+        out = np.zeros(getattr(self, "_n", 0), np.int32)
+        if out.size:
+            self._check(self._lib.ssum_tree_perm(self._h, _ptr(out), 0))
+        return out
+
     def set_stream(self, stream_ptr: int) -> None:
         self._check(self._lib.ssum_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))
 
@@ -451,11 +484,21 @@ def direct_sum(kernel, positions, strengths, tree: Optional[FaceTree] = None) ->
     return out
 
 
+def _out_buffer(out, n: int, d: int) -> np.ndarray:
+    if out is None:
+        return np.zeros((n, d))
+    if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != n * d:
+        raise ValueError(f"out must be a C-contiguous float64 array with {n * d} entries")
+    return out
+
+
 def treecode_sum(kernel, positions, strengths, cfg: TraversalConfig, tree: Optional[FaceTree] = None,
-                 workers: int = 1, stats: Optional[TreecodeStats] = None) -> np.ndarray:
+                 workers: int = 1, stats: Optional[TreecodeStats] = None,
+                 out: Optional[np.ndarray] = None) -> np.ndarray:
     """treecode_sum<K> (treecode.cpp:266-413): bins into `tree` (mutated),
     traverses, evaluates; returns (N, dim) = prefactor * sum. `workers` is
-    accepted for signature parity and ignored (the device is the worker pool)."""
+    accepted for signature parity and ignored (the device is the worker pool).
+    `out` may supply the (pinned) result buffer."""
     del workers
     k = _kernel_id(kernel)
     cfg.validate()
@@ -463,7 +506,7 @@ def treecode_sum(kernel, positions, strengths, cfg: TraversalConfig, tree: Optio
     n = p.shape[0]
     q = _as_vector(strengths, n, "strengths")
     d = 3 if k == 0 else 1
-    out = np.zeros((n, d))
+    out = _out_buffer(out, n, d)
     t = tree or _default_tree()
     c = cfg._c()
     s = stats._to_c() if stats is not None else _Stats()

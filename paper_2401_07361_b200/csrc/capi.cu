@@ -84,7 +84,7 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
     st->eval_seconds += secs(t2, t3);
     for (int k = 0; k < 4; ++k) {
       st->interaction_counts[k] = c.lists.counts[k];
-      st->kernel_evals[k] = c.lists.evals[k];
+      st->kernel_evals[k] = c.lists.local_evals[k];  // this part's work (all of it when unpartitioned)
     }
     st->node_count = c.nodes.count;
     st->leaf_count = static_cast<int64_t>(c.bins.leaves.size());
@@ -257,6 +257,31 @@ const char* ssum_last_error(const ssum_ctx* h) {
 
 int ssum_set_stream(ssum_ctx* h, void* stream) {
   return guarded(h, [&](Ctx& c) { c.stream = stream ? static_cast<cudaStream_t>(stream) : c.own_stream; });
+}
+
+int ssum_set_partition(ssum_ctx* h, int part, int nparts) {
+  return guarded(h, [&](Ctx& c) {
+    if (nparts < 1 || part < 0 || part >= nparts) throw Error(SSUM_INVALID, "partition out of range");
+    c.part = part;
+    c.nparts = nparts;
+  });
+}
+
+int ssum_partition_range(ssum_ctx* h, int64_t* begin, int64_t* end) {
+  return guarded(h, [&](Ctx& c) {
+    *begin = c.lists.p0;
+    *end = c.lists.p1;
+  });
+}
+
+int ssum_tree_perm(ssum_ctx* h, int* dst, int on_device) {
+  return guarded(h, [&](Ctx& c) {
+    const int64_t n = c.bins.n;
+    if (n == 0) return;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(dst, c.bins.perm.p, size_t(n) * 4,
+                                    on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
 }
 
 int ssum_tree_reset(ssum_ctx* h) {

@@ -8,10 +8,10 @@
 //   k_up_final     (compute_proxy_weights, treecode.cpp:79-91), then
 //                  w_hat = V^-T w (solve_transposed, sbb.cpp:110-115) into
 //                  the proxy entries' 4th component
-//   k_fit_tiles    Phase 3: CP/CC proxy potentials phi per fit node and the
+//   k_tiles<fit>   Phase 3: CP/CC proxy potentials phi per fit node and the
 //                  fit C = V^-1 phi (treecode.cpp:341-358, sbb.cpp:103-108)
-//   k_leaf_tiles   Phase 4 direct part: PP pairs and PC proxy pairs per leaf
-//                  tile (treecode.cpp:386-396)
+//   k_tiles<leaf>  Phase 4 direct part: PP pairs and PC proxy pairs per leaf
+//                  tile (treecode.cpp:386-396); also the direct sum
 //   k_finish       Phase 4 downward part (add_fitted_value over the path,
 //                  treecode.cpp:143-155,397-401), cross product, prefactor,
 //                  scatter back to the caller's order (:402)
@@ -162,108 +162,17 @@ __global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const i
   }
 }
 
-// Phase 3: one block per fit node, one thread per proxy target.
-template <int KER>
-__global__ void k_fit_tiles(const Tile* __restrict__ tiles, int ntiles, const SrcRange* __restrict__ ranges,
-                            const double4* __restrict__ pts, const int* __restrict__ fit_nodes,
-                            const int* __restrict__ pslot, const double* __restrict__ vinv, int P,
-                            double* __restrict__ coeff) {
-  constexpr int D = KDim<KER>::D;
-  extern __shared__ double4 smem4[];
-  double4* buf = smem4;                                        // blockDim entries
-  double* phi = reinterpret_cast<double*>(smem4 + blockDim.x);  // D * P
-  const int tix = blockIdx.x;
-  if (tix >= ntiles) return;
-  const Tile T = tiles[tix];
-  const int tid = threadIdx.x;
-  const bool active = tid < T.tgt_count;
-  const double4 x = pts[T.tgt_begin + (active ? tid : 0)];
-  Acc<KER> a;
-  a.zero();
-  for (int r = T.list_begin; r < T.list_end; ++r) {
-    const SrcRange R = ranges[r];
-    for (int base = 0; base < R.count; base += blockDim.x) {
-      const int n = min(static_cast<int>(blockDim.x), R.count - base);
-      if (tid < n) buf[tid] = pts[R.begin + base + tid];
-      __syncthreads();
-#pragma unroll 4
-      for (int k = 0; k < n; ++k) pair_far<KER>(x.x, x.y, x.z, buf[k], a);
-      __syncthreads();
-    }
-  }
-  if (active) {
-    if constexpr (KER == kBS) {
-      phi[tid] = x.y * a.s[2] - x.z * a.s[1];
-      phi[P + tid] = x.z * a.s[0] - x.x * a.s[2];
-      phi[2 * P + tid] = x.x * a.s[1] - x.y * a.s[0];
-    } else {
-      phi[tid] = -kInv4Pi * a.s[0];
-    }
-  }
-  __syncthreads();
-  const int slot = pslot[fit_nodes[tix]];
-  for (int kk = tid; kk < P; kk += blockDim.x) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      double s = 0.0;
-      for (int m = 0; m < P; ++m) s = fma(vinv[size_t(kk) * P + m], phi[d * P + m], s);
-      coeff[(size_t(slot) * D + d) * P + kk] = s;
-    }
-  }
-}
-
-// Phase 4 direct part: one warp per tile of <= 32 targets.
-template <int KER>
-__global__ void __launch_bounds__(128) k_leaf_tiles(const Tile* __restrict__ tiles, int ntiles,
-                                                    const SrcRange* __restrict__ ranges,
-                                                    const double4* __restrict__ pts, double* __restrict__ S,
-                                                    int* __restrict__ flags) {
-  constexpr int D = KDim<KER>::D;
-  __shared__ double4 buf[4][32];
-  const int wp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * 4 + wp;
-  if (t >= ntiles) return;
-  const Tile T = tiles[t];
-  const bool active = lane < T.tgt_count;
-  const int i = T.tgt_begin + (active ? lane : 0);
-  const double4 x = pts[i];
-  Acc<KER> a;
-  a.zero();
-  double4* b = buf[wp];
-  for (int r = T.list_begin; r < T.list_end; ++r) {
-    const SrcRange R = ranges[r];
-    for (int base = 0; base < R.count; base += 32) {
-      const int n = min(32, R.count - base);
-      if (lane < n) b[lane] = pts[R.begin + base + lane];
-      __syncwarp();
-      if (R.near) {
-        const int j0 = R.begin + base;
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) pair_near<KER>(x.x, x.y, x.z, b[k], i, j0 + k, a, flags);
-      } else {
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) pair_far<KER>(x.x, x.y, x.z, b[k], a);
-      }
-      __syncwarp();
-    }
-  }
-  if (active) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) S[size_t(i) * D + d] = a.s[d];
-  }
-}
-
 // Phase 4 downward part + finish.
 template <int KER, int DEG>
-__global__ void k_finish(int64_t n, const double4* __restrict__ pts, const double* __restrict__ S,
+__global__ void k_finish(int64_t p0, int64_t p1, const double4* __restrict__ pts, const double* __restrict__ S,
                          const int* __restrict__ pos_leaf, const int* __restrict__ parent,
                          const int* __restrict__ pslot, const unsigned char* __restrict__ is_fit,
                          const double* __restrict__ cramer, const double* __restrict__ coeff,
                          const int* __restrict__ perm, double* __restrict__ out) {
   constexpr int D = KDim<KER>::D;
   constexpr int P = Sbb<DEG>::P;
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
+  const int64_t k = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= p1) return;
   const double4 x = pts[k];
   double val[D];
 #pragma unroll
@@ -299,40 +208,17 @@ __global__ void k_finish(int64_t n, const double4* __restrict__ pts, const doubl
 }
 
 template <int KER>
-__global__ void k_direct_finish(int64_t n, const double4* __restrict__ pts, const double* __restrict__ S,
-                                double* __restrict__ out) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  if constexpr (KER == kBS) {
-    const double4 x = pts[k];
-    const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
-    out[3 * k] = -kInv4Pi * (x.y * s2 - x.z * s1);
-    out[3 * k + 1] = -kInv4Pi * (x.z * s0 - x.x * s2);
-    out[3 * k + 2] = -kInv4Pi * (x.x * s1 - x.y * s0);
-  } else {
-    out[k] = -kInv4Pi * S[k];
-  }
-}
-
-__global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = (n + 31) / 32;
-  if (t == 0) *range = SrcRange{0, static_cast<int>(n), 1, 0};
-  if (t >= nt) return;
-  const int64_t rem = n - t * 32;
-  tiles[t] = Tile{static_cast<int>(t * 32), static_cast<int>(rem < 32 ? rem : 32), 0, 1};
-}
-
-template <int KER>
-void launch_finish(Ctx& c, int degree, int64_t n, double* d_out) {
+void launch_finish(Ctx& c, int degree, double* d_out) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   const int bs = 128;
-#define SSUM_FINISH_CASE(DG)                                                                                  \
-  case DG:                                                                                                   \
-    k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, B.pos_leaf.p, c.nodes.parent.p, \
-                                                             L.pslot.p, L.is_fit.p, c.nodes.cramer.p,        \
-                                                             c.coeff.p, B.perm.p, d_out);                    \
+  const int64_t n = L.p1 - L.p0;
+  if (n <= 0) return;
+#define SSUM_FINISH_CASE(DG)                                                                                   \
+  case DG:                                                                                                    \
+    k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p,          \
+                                                             c.nodes.parent.p, L.pslot.p, L.is_fit.p,         \
+                                                             c.nodes.cramer.p, c.coeff.p, B.perm.p, d_out);   \
     break;
   switch (degree) {
     SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
@@ -507,29 +393,18 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   cudaEventRecord(c.ev[2], c.stream);
 
   // ---- CP/CC + fit
-  if (L.n_fit_tiles > 0) {
-    const int bt = ((P + 31) / 32) * 32;
-    const size_t sm = size_t(bt) * sizeof(double4) + size_t(D) * P * sizeof(double);
-    if (kernel == kBS)
-      k_fit_tiles<kBS><<<L.n_fit_tiles, bt, sm, c.stream>>>(L.fit_tiles.p, L.n_fit_tiles, L.fit_ranges.p, c.pts.p,
-                                                           L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
-    else
-      k_fit_tiles<kLOG><<<L.n_fit_tiles, bt, sm, c.stream>>>(L.fit_tiles.p, L.n_fit_tiles, L.fit_ranges.p, c.pts.p,
-                                                            L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
+  const int nfit = L.fit_sel_all ? L.n_fit_tiles : L.n_fit_sel;
+  if (nfit > 0) {
+    launch_fit_tiles(c, kernel, P, nfit, L.fit_sel_all ? nullptr : L.fit_sel.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
   cudaEventRecord(c.ev[3], c.stream);
 
-  // ---- PP + PC
-  if (L.n_leaf_tiles > 0) {
-    const unsigned g = grid_for(L.n_leaf_tiles, 4);
-    if (kernel == kBS)
-      k_leaf_tiles<kBS><<<g, 128, 0, c.stream>>>(L.leaf_tiles.p, L.n_leaf_tiles, L.leaf_ranges.p, c.pts.p, c.S.p,
-                                                 c.d_flags.p);
-    else
-      k_leaf_tiles<kLOG><<<g, 128, 0, c.stream>>>(L.leaf_tiles.p, L.n_leaf_tiles, L.leaf_ranges.p, c.pts.p, c.S.p,
-                                                  c.d_flags.p);
+  // ---- PP + PC (this part's contiguous tile range)
+  const int ntl = L.leaf_t1 - L.leaf_t0;
+  if (ntl > 0) {
+    launch_leaf_tiles(c, kernel, L.leaf_tiles.p + L.leaf_t0, ntl, L.leaf_ranges.p, c.S.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
@@ -537,9 +412,9 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
 
   // ---- downward + finish
   if (kernel == kBS)
-    launch_finish<kBS>(c, degree, n, d_out);
+    launch_finish<kBS>(c, degree, d_out);
   else
-    launch_finish<kLOG>(c, degree, n, d_out);
+    launch_finish<kLOG>(c, degree, d_out);
   cudaEventRecord(c.ev[5], c.stream);
   check_flags(c, "treecode_sum");
   if (st) {
@@ -555,28 +430,14 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n, double* d_out) {
   if (n == 0) return;
   const int D = kernel == kBS ? 3 : 1;
-  const int64_t nt = (n + 31) / 32;
   c.pts.ensure(size_t(n));
   c.S.ensure(size_t(n) * D);
-  c.direct_tiles.ensure(size_t(nt));
-  c.direct_range.ensure(1);
   const int bs = 256;
   SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
   k_gather<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, d_q, nullptr, n, c.pts.p);
-  k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
   SSUM_LAUNCH_CHECK();
-  const unsigned g = grid_for(nt, 4);
-  if (kernel == kBS) {
-    k_leaf_tiles<kBS><<<g, 128, 0, c.stream>>>(c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p,
-                                               c.pts.p, c.S.p, c.d_flags.p);
-    k_direct_finish<kBS><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
-  } else {
-    k_leaf_tiles<kLOG><<<g, 128, 0, c.stream>>>(c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p,
-                                                c.pts.p, c.S.p, c.d_flags.p);
-    k_direct_finish<kLOG><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
-  }
-  SSUM_LAUNCH_CHECK();
-  c.launches += 4;
+  c.launches++;
+  launch_direct(c, kernel, n, d_out);
   check_flags(c, "direct_sum");
 }
 

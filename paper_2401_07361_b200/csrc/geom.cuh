@@ -111,6 +111,31 @@ SSUM_HD double min_score_rn(d3 a, d3 b, d3 c, d3 bc, double det, d3 p) {
   return m;
 }
 
+// Divide-free screen for the containment DECISION min_score >= -1e-10.
+// The three numerators d_k are the reference's exact expressions; only the
+// divisions by det and by the sum are replaced by reciprocal multiplies. Each
+// replaced division moves a quotient by <= 2 ulp, so the screened score is
+// within ~2.5e-15 * max(|s|, 1) of the exact one; a guard band of 1e-13
+// around the threshold (and around the sum <= 1e-14 test) sends every
+// possibly-flipped case to the exact path. Returns 1 contained, 0 not,
+// -1 undecided (caller evaluates min_score_rn).
+SSUM_HD int contains_screen(d3 a, d3 b, d3 c, d3 bc, double det, double inv_det, d3 p) {
+  if (fabs(det) < 1e-14) return 0;  // exact test, same operands as min_score_rn
+  const double b1 = dot_rn(p, bc) * inv_det;
+  const double b2 = dot_rn(a, cross_rn(p, c)) * inv_det;
+  const double b3 = dot_rn(a, cross_rn(b, p)) * inv_det;
+  const double s = (b1 + b2) + b3;
+  if (fabs(s - 1e-14) <= 1e-13) return -1;
+  if (s <= 1e-14) return 0;
+  const double inv = 1.0 / s;
+  double m = b1 * inv;
+  const double m2 = b2 * inv, m3 = b3 * inv;
+  if (m2 < m) m = m2;
+  if (m3 < m) m = m3;
+  if (fabs(m + 1e-10) <= 1e-13) return -1;
+  return m >= -1e-10 ? 1 : 0;
+}
+
 // triangle_contains (geometry.cpp:85-92) via solve_vertex_basis
 // (geometry.cpp:14-25): raw_k = triple(...) / det, normalised by their sum.
 SSUM_HD bool contains_rn(d3 v1, d3 v2, d3 v3, d3 p) {

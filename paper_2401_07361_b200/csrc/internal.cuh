@@ -106,15 +106,24 @@ struct Binned {
 
 struct Ctx;
 
-// One tile = up to 32 targets against a list of source ranges.
+// One tile = up to kTileTargets targets against a list of source ranges. The
+// list starts with the ranges that may hold near pairs (1 - x.y < 2^-20, or
+// self pairs); near_total counts their sources. Beyond it every pair is
+// well separated and the kernel runs its branch-free fast loop.
+constexpr int kTileTargets = 256;
 struct Tile {
   int tgt_begin;  // index into the unified point array
-  int tgt_count;  // <= 32
+  int tgt_count;  // 1 .. kTileTargets
   int list_begin, list_end;  // into the range list
+  int near_total;            // sources in the leading near-possible ranges
+  int pad0, pad1, pad2;
 };
-// Source range in the unified point array. near != 0 marks a particle range
-// that may contain near-singular or self pairs (PP): the kernel takes the
-// reference-rounded slow path for pairs with 1 - x.y < kNearDen.
+// Arc-length margin below which a (target leaf, source node) pair may hold a
+// near pair: den = 2 sin^2(arc/2) < 2^-20 <=> arc < 1.3811e-3 rad.
+constexpr double kNearArc = 2.0e-3;
+// Source range in the unified point array. near != 0 marks a particle (PP)
+// range, which may hold near-singular or self pairs; pad is the number of
+// sources in the tile's list before this range (the flattened-list prefix).
 struct SrcRange {
   int begin;
   int count;
@@ -138,6 +147,14 @@ struct Lists {
   int64_t n_leaf_ranges = 0, n_fit_ranges = 0;
   DBuf<SrcRange> leaf_ranges, fit_ranges;
   uint64_t evals[4] = {0, 0, 0, 0};
+  // per-tile work (PP, PC) / (CP, CC) pair counts and this part's share
+  DBuf<ulonglong2> leaf_cost, fit_cost;
+  int leaf_t0 = 0, leaf_t1 = 0;  // leaf tile range of this part
+  int64_t p0 = 0, p1 = 0;        // tree-position range of this part
+  DBuf<int> fit_sel;             // selected fit tiles (when !fit_sel_all)
+  int n_fit_sel = 0;
+  bool fit_sel_all = true;
+  uint64_t local_evals[4] = {0, 0, 0, 0};
 };
 
 // Breadth-first traversal frontier entry: node pair plus depth-first order key.
@@ -165,6 +182,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   std::string last_error;
   int call_index = 0;
+  int part = 0, nparts = 1;  // target partition (multi-GPU)
   HostTree host;
   NodeTable nodes;
   Binned bins;
@@ -195,11 +213,15 @@ struct Ctx {
 void tree_init_roots(Ctx& c);
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
 void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
+void partition_targets(Ctx& c);
 void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,
               int64_t n, double* d_out, ssum_stats* st);
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
+void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel);
+void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S);
+void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out);
 void rk4_combine(Ctx& c, int stage, int64_t n, double dt, double omega, double* d_x0, double* d_z0,
                  const double* d_area, double* d_xs, double* d_q, const double* d_u, double* d_kacc,
                  double* d_kzacc);

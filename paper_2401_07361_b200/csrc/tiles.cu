@@ -1,0 +1,286 @@
+// Interaction tiles: the PP + PC (leaf) and CP + CC + fit (fit node) passes
+// and the direct sum, all on one kernel shape (k_tiles). Kept in its own
+// translation unit so tuning builds (make variants) recompile only this file.
+#include "kernels.cuh"
+
+namespace ssum {
+
+namespace {
+
+constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
+
+// Phases 3 and 4 (direct part) share one kernel shape: a block of 256
+// threads per TILE — up to 256 targets (a leaf's particles, or a fit node's
+// p proxy points) against the tile's list of source ranges.
+//
+//  * Thread -> (target t = tid % T, source group g = (tid / T) % G) with
+//    G = min(32, 256 / T): a 40-particle leaf keeps 240 of 256 lanes busy
+//    (6 groups), a p = 45 fit node 225 (5 groups).
+//  * The source ranges are streamed as ONE flattened list in chunks of 256
+//    (each thread fetches one source, locating its range by binary search on
+//    the ranges' prefix counts), double-buffered through shared memory:
+//    chunk c+1 is in flight in registers while chunk c is consumed. Every
+//    thread walks the chunk with stride G, so all warps run the same trip
+//    count (the chunk tail is zero-padded: q = 0 adds nothing).
+//  * Group partials are reduced in group order through shared memory
+//    (deterministic, no atomics).
+//  MODE kLeafMode: near-pair handling (pair_near), writes S per target.
+//  MODE kFitMode : well-separated pairs only; phi = K-sums at the proxy
+//                  points, then C = V^-1 phi (ProxyFit::solve, sbb.cpp:103-108).
+constexpr int kTileThreads = 256;
+#ifndef SSUM_CHUNK
+#define SSUM_CHUNK 512
+#endif
+constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage (multiple of kTileThreads)
+constexpr int kLeafMode = 0, kFitMode = 1;
+constexpr int kPad = 32;  // >= max G - 1: the stride-G walk reads up to G - 1 entries past n
+
+#ifndef SSUM_TILE_MINB
+#define SSUM_TILE_MINB 3
+#endif
+#ifndef SSUM_TPT
+#define SSUM_TPT 2
+#endif
+constexpr int kRangeCap = 512;
+constexpr int kTpt = SSUM_TPT;  // targets per thread (register tile)
+
+template <int KER, int MODE>
+__global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
+    k_tiles(const Tile* __restrict__ tiles, int ntiles, const int* __restrict__ sel,
+            const SrcRange* __restrict__ ranges, const double4* __restrict__ pts, double* __restrict__ S,
+            int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
+            const double* __restrict__ vinv, int P, double* __restrict__ coeff) {
+  constexpr int D = KDim<KER>::D;
+  __shared__ double4 buf[2][kChunk + kPad];
+  __shared__ int sid[2][kChunk + kPad];
+  __shared__ int2 rtab[kRangeCap];  // (begin, prefix) of the tile's ranges
+  static_assert(sizeof(double) * kTileThreads * D * kTpt <= 2 * sizeof(double4) * (kChunk + kPad), "red alias");
+  double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
+  if (static_cast<int>(blockIdx.x) >= ntiles) return;
+  const int tix = sel ? sel[blockIdx.x] : static_cast<int>(blockIdx.x);
+  const Tile T = tiles[tix];
+  const int tc = T.tgt_count;
+  const int th = (tc + kTpt - 1) / kTpt;  // thread-targets; thread slot u holds targets u, u + th, ...
+  const int G = min(32, kTileThreads / th);
+  const int tid = threadIdx.x;
+  const int u = tid % th, g = (tid / th) % G;
+  int ti[kTpt];
+  double4 x[kTpt];
+#pragma unroll
+  for (int q = 0; q < kTpt; ++q) {
+    const int tt = u + q * th;
+    ti[q] = T.tgt_begin + (tt < tc ? tt : u);  // padding slots repeat target u (discarded)
+    x[q] = pts[ti[q]];
+  }
+  const int total = (T.list_end > T.list_begin) ? ranges[T.list_end - 1].pad + ranges[T.list_end - 1].count : 0;
+  const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (tid < kPad) {  // zero tail: the stride-G walk may read up to G - 1 entries past the chunk
+    buf[0][kChunk + tid] = zero4;
+    buf[1][kChunk + tid] = zero4;
+    sid[0][kChunk + tid] = -1;
+    sid[1][kChunk + tid] = -1;
+  }
+  const int nr = T.list_end - T.list_begin;
+  const bool in_smem = nr <= kRangeCap;
+  if (in_smem)
+    for (int r = tid; r < nr; r += kTileThreads) {
+      const SrcRange R = ranges[T.list_begin + r];
+      rtab[r] = make_int2(R.begin, R.pad);
+    }
+  __syncthreads();
+  // flattened position f -> source index: binary search over range prefixes
+  auto fetch = [&](int f, double4& v, int& j) {
+    if (f < total) {
+      int lo = 0, hi = nr - 1, b, p;
+      if (in_smem) {
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (rtab[mid].y <= f)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        b = rtab[lo].x;
+        p = rtab[lo].y;
+      } else {
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ranges[T.list_begin + mid].pad <= f)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        b = ranges[T.list_begin + lo].begin;
+        p = ranges[T.list_begin + lo].pad;
+      }
+      j = b + (f - p);
+      v = pts[j];
+    } else {
+      v = zero4;
+      j = -1;
+    }
+  };
+  Acc<KER> a[kTpt];
+#pragma unroll
+  for (int q = 0; q < kTpt; ++q) a[q].zero();
+  constexpr int kPer = kChunk / kTileThreads;  // sources fetched per thread per chunk
+  const int nch = (total + kChunk - 1) / kChunk;
+  double4 v[kPer];
+  int j[kPer];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    fetch(e * kTileThreads + tid, v[e], j[e]);
+    buf[0][e * kTileThreads + tid] = v[e];
+    sid[0][e * kTileThreads + tid] = j[e];
+  }
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const bool more = c + 1 < nch;
+    if (more)
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) fetch((c + 1) * kChunk + e * kTileThreads + tid, v[e], j[e]);
+    const int n = min(kChunk, total - c * kChunk);
+    const double4* B = buf[c & 1];
+    const int* J = sid[c & 1];
+    const int iters = (n + G - 1) / G;
+    if (MODE == kLeafMode && c * kChunk < T.near_total) {
+      // chunk holds near-possible sources: per-pair warp vote + exact path
+#pragma unroll 2
+      for (int it = 0; it < iters; ++it) {
+        const int k = g + it * G;
+        source_near<KER, kTpt>(x, B[k], ti, J[k], a, flags);
+      }
+    } else {
+      // well-separated sources only: branch-free fast loop, kTpt chains per source
+#pragma unroll 4
+      for (int it = 0; it < iters; ++it) {
+        const double4 y = B[g + it * G];
+#pragma unroll
+        for (int q = 0; q < kTpt; ++q) pair_far<KER>(x[q].x, x[q].y, x[q].z, y, a[q]);
+      }
+    }
+    if (more)
+#pragma unroll
+      for (int e = 0; e < kPer; ++e) {
+        buf[(c + 1) & 1][e * kTileThreads + tid] = v[e];
+        sid[(c + 1) & 1][e * kTileThreads + tid] = j[e];
+      }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kTpt; ++q)
+#pragma unroll
+    for (int d = 0; d < D; ++d) red[(q * kTileThreads + tid) * D + d] = a[q].s[d];
+  __syncthreads();
+  // target tt = u + q th lives in slot (q, g * th + u) for every group g
+  double s[D];
+  const int tt = tid;
+  const int uq = tt % th, qq = tt / th;
+  if (tt < tc) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) s[d] = red[(qq * kTileThreads + uq) * D + d];
+    for (int gg = 1; gg < G; ++gg)
+#pragma unroll
+      for (int d = 0; d < D; ++d) s[d] += red[(qq * kTileThreads + gg * th + uq) * D + d];
+  }
+  const int i_out = T.tgt_begin + tt;
+  if constexpr (MODE == kLeafMode) {
+    if (tt < tc) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) S[size_t(i_out) * D + d] = s[d];
+    }
+  } else {
+    __syncthreads();  // red is reused for phi below
+    double* phi = red;
+    if (tt < tc) {
+      const double4 xo = pts[i_out];
+      if constexpr (KER == kBS) {
+        phi[tt] = xo.y * s[2] - xo.z * s[1];
+        phi[P + tt] = xo.z * s[0] - xo.x * s[2];
+        phi[2 * P + tt] = xo.x * s[1] - xo.y * s[0];
+      } else {
+        phi[tt] = -kInv4Pi * s[0];
+      }
+    }
+    __syncthreads();
+    const int slot = pslot[fit_nodes[tix]];
+    for (int kk = tid; kk < P; kk += kTileThreads) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        double acc = 0.0;
+        for (int m = 0; m < P; ++m) acc = fma(vinv[size_t(kk) * P + m], phi[d * P + m], acc);
+        coeff[(size_t(slot) * D + d) * P + kk] = acc;
+      }
+    }
+  }
+}
+
+template <int KER>
+__global__ void k_direct_finish(int64_t n, const double4* __restrict__ pts, const double* __restrict__ S,
+                                double* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if constexpr (KER == kBS) {
+    const double4 x = pts[k];
+    const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
+    out[3 * k] = -kInv4Pi * (x.y * s2 - x.z * s1);
+    out[3 * k + 1] = -kInv4Pi * (x.z * s0 - x.x * s2);
+    out[3 * k + 2] = -kInv4Pi * (x.x * s1 - x.y * s0);
+  } else {
+    out[k] = -kInv4Pi * S[k];
+  }
+}
+
+__global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (n + kTileThreads - 1) / kTileThreads;
+  if (t == 0) *range = SrcRange{0, static_cast<int>(n), 1, 0};
+  if (t >= nt) return;
+  const int64_t rem = n - t * kTileThreads;
+  tiles[t] = Tile{static_cast<int>(t * kTileThreads), static_cast<int>(rem < kTileThreads ? rem : kTileThreads), 0, 1,
+                  static_cast<int>(n), 0, 0, 0};
+}
+
+}  // namespace
+
+void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
+  Lists& L = c.lists;
+  if (kernel == kBS)
+    k_tiles<kBS, kFitMode><<<nfit, kTileThreads, 0, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p,
+                                                                nullptr, c.d_flags.p, L.fit_nodes.p, L.pslot.p,
+                                                                c.vinv.p, P, c.coeff.p);
+  else
+    k_tiles<kLOG, kFitMode><<<nfit, kTileThreads, 0, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p,
+                                                                 nullptr, c.d_flags.p, L.fit_nodes.p, L.pslot.p,
+                                                                 c.vinv.p, P, c.coeff.p);
+}
+
+void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S) {
+  if (kernel == kBS)
+    k_tiles<kBS, kLeafMode><<<ntl, kTileThreads, 0, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p,
+                                                                nullptr, nullptr, nullptr, 0, nullptr);
+  else
+    k_tiles<kLOG, kLeafMode><<<ntl, kTileThreads, 0, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p,
+                                                                 nullptr, nullptr, nullptr, 0, nullptr);
+}
+
+// Direct sum (treecode.cpp:246-264): every target against one range [0, n)
+// in the caller's order.
+void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out) {
+  const int64_t nt = (n + kTileThreads - 1) / kTileThreads;
+  c.direct_tiles.ensure(size_t(nt));
+  c.direct_range.ensure(1);
+  const int bs = 256;
+  k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
+  SSUM_LAUNCH_CHECK();
+  launch_leaf_tiles(c, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p);
+  SSUM_LAUNCH_CHECK();
+  if (kernel == kBS)
+    k_direct_finish<kBS><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
+  else
+    k_direct_finish<kLOG><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
+  SSUM_LAUNCH_CHECK();
+  c.launches += 3;
+}
+
+}  // namespace ssum

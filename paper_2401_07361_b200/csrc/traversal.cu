@@ -129,21 +129,27 @@ __global__ void k_root_pairs(PairEntry* F) {
 // Node flags from the emitted list (treecode.cpp:295-317).
 __global__ void k_mark(const int4* __restrict__ E, long long ne, unsigned char* is_weight, unsigned char* is_fit,
                        int* group_key, int* group_val, unsigned long long* kind_counts) {
-  __shared__ unsigned long long sc[4];
+  __shared__ unsigned int sc[4];
   if (threadIdx.x < 4) sc[threadIdx.x] = 0;
   __syncthreads();
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int kind = -1;
   if (e < ne) {
     const int4 it = E[e];
-    const int kind = it.z;
+    kind = it.z;
     if (kind == 1 || kind == 3) is_weight[it.y] = 1;
     if (kind == 2 || kind == 3) is_fit[it.x] = 1;
     group_key[e] = 2 * it.x + ((kind >= 2) ? 1 : 0);
     group_val[e] = static_cast<int>(e);
-    atomicAdd(&sc[kind], 1ull);
+  }
+  // per-kind counts: warp ballots, one shared atomic per warp and kind
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned m = __ballot_sync(0xffffffffu, kind == k);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&sc[k], static_cast<unsigned>(__popc(m)));
   }
   __syncthreads();
-  if (threadIdx.x < 4 && sc[threadIdx.x]) atomicAdd(&kind_counts[threadIdx.x], sc[threadIdx.x]);
+  if (threadIdx.x < 4 && sc[threadIdx.x]) atomicAdd(&kind_counts[threadIdx.x], static_cast<unsigned long long>(sc[threadIdx.x]));
 }
 
 __global__ void k_slot_flags(const unsigned char* is_weight, const unsigned char* is_fit, int nn, int* flag) {
@@ -187,15 +193,32 @@ __global__ void k_leaf_count(const int* __restrict__ leaves, int nl, const int* 
     r += sg.y - sg.x;
   }
   n_ranges[k] = r;
-  n_tiles[k] = (cnt[leaf] + kWarp - 1) / kWarp;
+  n_tiles[k] = (cnt[leaf] + kTileTargets - 1) / kTileTargets;
 }
 
+// May a pair (x in leaf, y in node s) have 1 - x.y < 2^-20? Only if the two
+// circumcircles come within kNearArc of each other (every binned point lies
+// in its node's circumcircle, up to the -1e-10 containment tolerance).
+__device__ __forceinline__ bool near_possible(int leaf, int s, const double* __restrict__ center,
+                                              const double* __restrict__ radius) {
+  if (leaf == s) return true;
+  const d3 a{center[3 * leaf], center[3 * leaf + 1], center[3 * leaf + 2]};
+  const d3 b{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
+  const double cx = a.y * b.z - a.z * b.y, cy = a.z * b.x - a.x * b.z, cz = a.x * b.y - a.y * b.x;
+  const double arc = atan2(sqrt(cx * cx + cy * cy + cz * cz), a.x * b.x + a.y * b.y + a.z * b.z);
+  return arc - radius[leaf] - radius[s] < kNearArc;
+}
+
+// Range list of one leaf: PP and PC entries of every node on its
+// root-to-leaf path (treecode.cpp:379-396), near-possible PP ranges first.
 __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* __restrict__ parent,
                             const int2* __restrict__ seg, const int* __restrict__ sorted_e,
                             const int4* __restrict__ E, const int* __restrict__ cnt, const int* __restrict__ off,
-                            const int* __restrict__ pslot, const int* __restrict__ range_off,
+                            const int* __restrict__ pslot, const double* __restrict__ center,
+                            const double* __restrict__ radius, const int* __restrict__ range_off,
                             const int* __restrict__ tile_off, int64_t N, int P, SrcRange* __restrict__ ranges,
-                            Tile* __restrict__ tiles, unsigned long long* __restrict__ evals) {
+                            Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
+                            unsigned long long* __restrict__ evals) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long pp = 0, pc = 0;
   if (k < nl) {
@@ -206,35 +229,45 @@ __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* _
     int w = range_off[k];
     const int w0 = w;
     unsigned long long src_pp = 0, src_pc = 0;
-    for (int q = pl - 1; q >= 0; --q) {  // root to leaf (treecode.cpp:379,392)
-      const int2 sg = seg[2 * path[q]];
-      for (int i = sg.x; i < sg.y; ++i) {
-        const int4 it = E[sorted_e[i]];
-        SrcRange r;
-        if (it.z == 0) {
-          r.begin = off[it.y];
-          r.count = cnt[it.y];
-          r.near = 1;
-          src_pp += static_cast<unsigned long long>(r.count);
-        } else {
-          r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
-          r.count = P;
-          r.near = 0;
-          src_pc += static_cast<unsigned long long>(P);
+    int near_total = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // 0: near-possible PP ranges, 1: the rest
+      for (int q = pl - 1; q >= 0; --q) {   // root to leaf (treecode.cpp:379,392)
+        const int2 sg = seg[2 * path[q]];
+        for (int i = sg.x; i < sg.y; ++i) {
+          const int4 it = E[sorted_e[i]];
+          const bool nr = it.z == 0 && near_possible(leaf, it.y, center, radius);
+          if (nr != (pass == 0)) continue;
+          SrcRange r;
+          r.pad = static_cast<int>(src_pp + src_pc);  // flattened-list prefix
+          if (it.z == 0) {
+            r.begin = off[it.y];
+            r.count = cnt[it.y];
+            r.near = nr ? 1 : 0;
+            src_pp += static_cast<unsigned long long>(r.count);
+          } else {
+            r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
+            r.count = P;
+            r.near = 0;
+            src_pc += static_cast<unsigned long long>(P);
+          }
+          ranges[w++] = r;
         }
-        r.pad = 0;
-        ranges[w++] = r;
       }
+      if (pass == 0) near_total = static_cast<int>(src_pp);
     }
     const int c = cnt[leaf];
-    const int nt = (c + kWarp - 1) / kWarp;
+    const int nt = (c + kTileTargets - 1) / kTileTargets;
     for (int j = 0; j < nt; ++j) {
       Tile t;
-      t.tgt_begin = off[leaf] + j * kWarp;
-      t.tgt_count = min(kWarp, c - j * kWarp);
+      t.tgt_begin = off[leaf] + j * kTileTargets;
+      t.tgt_count = min(kTileTargets, c - j * kTileTargets);
       t.list_begin = w0;
       t.list_end = w;
+      t.near_total = near_total;
+      t.pad0 = t.pad1 = t.pad2 = 0;
       tiles[tile_off[k] + j] = t;
+      const unsigned long long tc = static_cast<unsigned long long>(t.tgt_count);
+      tile_cost[tile_off[k] + j] = make_ulonglong2(tc * src_pp - tc, tc * src_pc);  // self pairs excluded
     }
     pp = static_cast<unsigned long long>(c) * src_pp - static_cast<unsigned long long>(c);  // self pairs excluded
     pc = static_cast<unsigned long long>(c) * src_pc;
@@ -261,7 +294,8 @@ __global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2
                            const int* __restrict__ sorted_e, const int4* __restrict__ E, const int* __restrict__ cnt,
                            const int* __restrict__ off, const int* __restrict__ pslot,
                            const int* __restrict__ range_off, int64_t N, int P, SrcRange* __restrict__ ranges,
-                           Tile* __restrict__ tiles, unsigned long long* __restrict__ evals) {
+                           Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
+                           unsigned long long* __restrict__ evals) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long cp = 0, cc = 0;
   if (k < nf) {
@@ -269,9 +303,11 @@ __global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2
     const int2 sg = seg[2 * t + 1];
     int w = range_off[k];
     const int w0 = w;
+    int pre = 0;
     for (int i = sg.x; i < sg.y; ++i) {  // emission order (treecode.cpp:347)
       const int4 it = E[sorted_e[i]];
       SrcRange r;
+      r.pad = pre;  // flattened-list prefix
       if (it.z == 2) {
         r.begin = off[it.y];
         r.count = cnt[it.y];
@@ -282,7 +318,7 @@ __global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2
         cc += static_cast<unsigned long long>(P) * static_cast<unsigned long long>(P);
       }
       r.near = 0;
-      r.pad = 0;
+      pre += r.count;
       ranges[w++] = r;
     }
     Tile tl;
@@ -290,7 +326,10 @@ __global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2
     tl.tgt_count = P;
     tl.list_begin = w0;
     tl.list_end = w;
+    tl.near_total = 0;  // CP / CC pairs are well separated
+    tl.pad0 = tl.pad1 = tl.pad2 = 0;
     tiles[k] = tl;
+    tile_cost[k] = make_ulonglong2(cp, cc);
   }
   typedef cub::BlockReduce<unsigned long long, 128> BR;
   __shared__ typename BR::TempStorage tmp;
@@ -476,9 +515,12 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
   }
   L.leaf_ranges.ensure(size_t(std::max<int64_t>(L.n_leaf_ranges, 1)));
   L.leaf_tiles.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
+  L.leaf_cost.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
   k_leaf_fill<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
-                                                        L.inter.p, B.cnt.p, B.off.p, L.pslot.p, S.nr_off.p, S.nt_off.p,
-                                                        N, P, L.leaf_ranges.p, L.leaf_tiles.p, S.counters.p + 4);
+                                                        L.inter.p, B.cnt.p, B.off.p, L.pslot.p, c.nodes.center.p,
+                                                        c.nodes.radius.p, S.nr_off.p, S.nt_off.p, N, P,
+                                                        L.leaf_ranges.p, L.leaf_tiles.p, L.leaf_cost.p,
+                                                        S.counters.p + 4);
   SSUM_LAUNCH_CHECK();
   c.launches++;
 
@@ -498,9 +540,10 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     L.n_fit_ranges = tot;
     L.fit_ranges.ensure(size_t(std::max(tot, 1)));
     L.fit_tiles.ensure(size_t(nf));
+    L.fit_cost.ensure(size_t(nf));
     k_fit_fill<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.sorted_e.p, L.inter.p, B.cnt.p,
                                                          B.off.p, L.pslot.p, S.nr_off.p, N, P, L.fit_ranges.p,
-                                                         L.fit_tiles.p, S.counters.p + 4);
+                                                         L.fit_tiles.p, L.fit_cost.p, S.counters.p + 4);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
@@ -512,6 +555,78 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     L.counts[k] = h[k];
     L.evals[k] = h[4 + k];
   }
+  partition_targets(c);
+}
+
+// Multi-GPU target partition: leaf tiles are in depth-first
+// order, so a contiguous tile range is a contiguous range [p0, p1) of tree
+// positions. Cut points balance the tiles' PP + PC pair counts; a part keeps
+// the fit nodes whose bins intersect its range (nodes straddling a cut are
+// computed by both owners, identically). Each target is computed whole by
+// one part with the same code, so the union of the parts is bitwise the
+// single-part result. The tree build and upward pass are replicated.
+void partition_targets(Ctx& c) {
+  Lists& L = c.lists;
+  const int64_t N = c.bins.n;
+  L.leaf_t0 = 0;
+  L.leaf_t1 = L.n_leaf_tiles;
+  L.p0 = 0;
+  L.p1 = N;
+  L.n_fit_sel = L.n_fit_tiles;
+  L.fit_sel_all = true;
+  L.local_evals[0] = L.evals[0];
+  L.local_evals[1] = L.evals[1];
+  L.local_evals[2] = L.evals[2];
+  L.local_evals[3] = L.evals[3];
+  if (c.nparts <= 1 || L.n_leaf_tiles == 0) return;
+  const int nt = L.n_leaf_tiles;
+  std::vector<ulonglong2> cost(static_cast<size_t>(nt));
+  std::vector<Tile> tiles(static_cast<size_t>(nt));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(cost.data(), L.leaf_cost.p, size_t(nt) * sizeof(ulonglong2), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(tiles.data(), L.leaf_tiles.p, size_t(nt) * sizeof(Tile), cudaMemcpyDeviceToHost, c.stream));
+  std::vector<ulonglong2> fcost(static_cast<size_t>(std::max(L.n_fit_tiles, 0)));
+  if (L.n_fit_tiles > 0)
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(fcost.data(), L.fit_cost.p, fcost.size() * sizeof(ulonglong2), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  std::vector<double> pre(static_cast<size_t>(nt) + 1, 0.0);
+  for (int t = 0; t < nt; ++t) pre[size_t(t) + 1] = pre[size_t(t)] + double(cost[size_t(t)].x + cost[size_t(t)].y) + 1.0;
+  const double total = pre[size_t(nt)];
+  auto cut = [&](int r) {
+    if (r <= 0) return 0;
+    if (r >= c.nparts) return nt;
+    const double goal = total * r / c.nparts;
+    return static_cast<int>(std::lower_bound(pre.begin(), pre.end(), goal) - pre.begin());
+  };
+  const int t0 = std::min(cut(c.part), nt), t1 = std::max(std::min(cut(c.part + 1), nt), t0);
+  L.leaf_t0 = t0;
+  L.leaf_t1 = t1;
+  L.local_evals[0] = L.local_evals[1] = L.local_evals[2] = L.local_evals[3] = 0;
+  if (t1 > t0) {
+    L.p0 = tiles[size_t(t0)].tgt_begin;
+    L.p1 = tiles[size_t(t1) - 1].tgt_begin + tiles[size_t(t1) - 1].tgt_count;
+  } else {
+    L.p0 = L.p1 = (t0 < nt) ? tiles[size_t(t0)].tgt_begin : N;
+  }
+  for (int t = t0; t < t1; ++t) {
+    L.local_evals[0] += cost[size_t(t)].x;
+    L.local_evals[1] += cost[size_t(t)].y;
+  }
+  std::vector<int> sel;
+  for (int k = 0; k < L.n_fit_tiles; ++k) {
+    const int id = L.h_fit_nodes[size_t(k)];
+    const int64_t o = c.host.off[size_t(id)], e = o + c.host.cnt[size_t(id)];
+    if (o < L.p1 && e > L.p0) {
+      sel.push_back(k);
+      L.local_evals[2] += fcost[size_t(k)].x;
+      L.local_evals[3] += fcost[size_t(k)].y;
+    }
+  }
+  L.n_fit_sel = static_cast<int>(sel.size());
+  L.fit_sel_all = false;
+  L.fit_sel.ensure(std::max<size_t>(sel.size(), 1));
+  if (!sel.empty())
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(L.fit_sel.p, sel.data(), sel.size() * 4, cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 // Export helper: the emitted list sorted into depth-first (reference) order.

@@ -30,10 +30,13 @@ __device__ __forceinline__ d3 load3(const double* p) { return {p[0], p[1], p[2]}
 // Root-face assignment: first of the 20 roots with triangle_contains
 // (face_tree.cpp:77-85). GeometryError when none contains the particle.
 __global__ void k_bin_roots(const double* __restrict__ xyz, int64_t n, const double* __restrict__ tri,
-                            int* __restrict__ cur, int* __restrict__ cnt, int* __restrict__ flags) {
+                            const double* __restrict__ cramer, int* __restrict__ cur, int* __restrict__ cnt,
+                            int* __restrict__ flags) {
   __shared__ double st[20 * 9];
+  __shared__ double skr[20 * 12];
   __shared__ int scount[20];
   for (int k = threadIdx.x; k < 180; k += blockDim.x) st[k] = tri[k];
+  for (int k = threadIdx.x; k < 240; k += blockDim.x) skr[k] = cramer[k];
   if (threadIdx.x < 20) scount[threadIdx.x] = 0;
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -41,7 +44,11 @@ __global__ void k_bin_roots(const double* __restrict__ xyz, int64_t n, const dou
     const d3 p = load3(xyz + 3 * i);
     int found = -1;
     for (int f = 0; f < 20; ++f) {
-      if (contains_rn(load3(st + 9 * f), load3(st + 9 * f + 3), load3(st + 9 * f + 6), p)) {
+      const d3 v1 = load3(st + 9 * f), v2 = load3(st + 9 * f + 3), v3 = load3(st + 9 * f + 6);
+      const double* k = skr + 12 * f;
+      int in = contains_screen(v1, v2, v3, d3{k[0], k[1], k[2]}, k[3], k[10], p);
+      if (in < 0) in = contains_rn(v1, v2, v3, p);
+      if (in) {
         found = f;
         break;
       }
@@ -58,7 +65,7 @@ __global__ void k_bin_roots(const double* __restrict__ xyz, int64_t n, const dou
 
 // Node geometry (TreeNode ctor, face_tree.hpp:22-25) plus the per-node
 // constants the binning and the barycentric passes reuse:
-// cramer = [v2 x v3, v1.(v2 x v3), v3 x v1, v1 x v2, 0, 0].
+// cramer = [v2 x v3, v1.(v2 x v3), v3 x v1, v1 x v2, 1 / det, 0].
 __device__ void write_node(double* tri, double* center, double* radius, double* cramer, int id, d3 a,
                            d3 b, d3 c, int* flags) {
   int bad = 0;
@@ -80,7 +87,8 @@ __device__ void write_node(double* tri, double* center, double* radius, double* 
   k[3] = dot_rn(a, bc);
   k[4] = n2.x; k[5] = n2.y; k[6] = n2.z;
   k[7] = n3.x; k[8] = n3.y; k[9] = n3.z;
-  k[10] = 0.0; k[11] = 0.0;
+  k[10] = 1.0 / k[3];  // screened containment (contains_screen)
+  k[11] = 0.0;
   if (bad) atomicOr(flags, kFlagGeometry);
 }
 
@@ -133,25 +141,33 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
   }
   const d3 p = load3(xyz + 3 * i);
   const int cb = child_base[node];
-  int best = cb;
-  double best_s = -1e300;
   int placed = -1;
-  for (int c = cb; c < cb + 4; ++c) {
+  for (int c = cb; c < cb + 4 && placed < 0; ++c) {  // first containing child wins (face_tree.cpp:56-61)
     const double* t = tri + 9 * c;
     const double* k = cramer + 12 * c;
-    const double s = min_score_rn(load3(t), load3(t + 3), load3(t + 6), d3{k[0], k[1], k[2]}, k[3], p);
-    if (s >= -1e-10) {
-      placed = c;
-      break;
-    }
-    if (s > best_s) {
-      best_s = s;
-      best = c;
+    const d3 va = load3(t), vb = load3(t + 3), vc = load3(t + 6), bc{k[0], k[1], k[2]};
+    int in = contains_screen(va, vb, vc, bc, k[3], k[10], p);
+    if (in < 0) in = min_score_rn(va, vb, vc, bc, k[3], p) >= -1e-10;
+    if (in) placed = c;
+  }
+  int best = cb;
+  if (placed < 0) {  // no child contains p: least-negative exact score (face_tree.cpp:62-69)
+    double best_s = -1e300;
+    for (int c = cb; c < cb + 4; ++c) {
+      const double* t = tri + 9 * c;
+      const double* k = cramer + 12 * c;
+      const double s = min_score_rn(load3(t), load3(t + 3), load3(t + 6), d3{k[0], k[1], k[2]}, k[3], p);
+      if (s > best_s) {
+        best_s = s;
+        best = c;
+      }
     }
   }
   if (placed < 0) placed = best;
   cur[i] = placed;
-  atomicAdd(&cnt[placed], 1);
+  // warp-aggregated bin count: one atomic per distinct child in the warp
+  const unsigned peers = __match_any_sync(__activemask(), placed);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[placed], __popc(peers));
 }
 
 __global__ void k_gather_counts(const int* __restrict__ ids, int m, const int* __restrict__ cnt, int* out) {
@@ -226,7 +242,8 @@ void tree_init_roots(Ctx& c) {
       center[3 * f + 2] = ctr.z;
       radius[f] = arc_dist(ctr, a);
       const d3 bc = cross_rn(b, cc), n2 = cross_rn(cc, a), n3 = cross_rn(a, b);
-      const double kk[12] = {bc.x, bc.y, bc.z, dot_rn(a, bc), n2.x, n2.y, n2.z, n3.x, n3.y, n3.z, 0, 0};
+      const double det = dot_rn(a, bc);
+      const double kk[12] = {bc.x, bc.y, bc.z, det, n2.x, n2.y, n2.z, n3.x, n3.y, n3.z, 1.0 / det, 0};
       std::copy(kk, kk + 12, cramer.begin() + 12 * f);
     }
   }
@@ -266,7 +283,8 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   B.cur.ensure(size_t(n));
   B.leaf_of.ensure(size_t(n));
 
-  k_bin_roots<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, c.nodes.tri.p, B.cur.p, B.cnt.p, c.d_flags.p);
+  k_bin_roots<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, c.nodes.tri.p, c.nodes.cramer.p, B.cur.p, B.cnt.p,
+                                                     c.d_flags.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   check_flags(c, "bin_particles: particle contained in no root face");
@@ -371,6 +389,9 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     }
   B.off.ensure(size_t(c.nodes.count));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.off.p, h.off.data(), size_t(c.nodes.count) * 4, cudaMemcpyHostToDevice, c.stream));
+  // leaves in depth-first (tree-position) order: leaf tiles then cover the
+  // tree-order particle array left to right, which the target partition uses
+  std::sort(B.leaves.begin(), B.leaves.end(), [&](int a, int b) { return h.off[a] < h.off[b]; });
   B.d_leaves.ensure(std::max<size_t>(B.leaves.size(), 1));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.d_leaves.p, B.leaves.data(), B.leaves.size() * 4, cudaMemcpyHostToDevice, c.stream));
 

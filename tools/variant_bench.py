@@ -1,0 +1,53 @@
+"""Time the config-4 evaluation passes for each tuning build of the library
+(make -C paper_2401_07361_b200/csrc variants). One subprocess per library.
+
+    python tools/variant_bench.py [level]
+"""
+import glob
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r"""
+import sys, json, statistics, torch
+sys.path.insert(0, '.')
+import paper_2401_07361_b200 as ss
+lvl = int(sys.argv[1])
+xyz, area = ss.make_icosa_mesh(lvl)
+q = ss.rh4_vorticity(xyz) * area
+dev = torch.device('cuda', 0)
+dx, dq = torch.from_numpy(xyz).to(dev), torch.from_numpy(q).to(dev)
+out = torch.zeros((xyz.shape[0], 3), dtype=torch.float64, device=dev)
+tree = ss.FaceTree(0)
+tree.set_stream(torch.cuda.current_stream().cuda_stream)
+cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+rows = []
+for k in range(8):
+    st = ss.TreecodeStats()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, dx.data_ptr(), dq.data_ptr(), xyz.shape[0], out.data_ptr(), stats=st)
+    e1.record(); torch.cuda.synchronize()
+    if k >= 3:
+        rows.append((e0.elapsed_time(e1), st.pp_pc_ms, st.cp_cc_fit_ms, st.upward_ms, st.finish_ms,
+                     st.bin_seconds * 1e3, st.traversal_seconds * 1e3))
+med = [statistics.median(c) for c in zip(*rows)]
+print(json.dumps(dict(zip(['step', 'pp_pc', 'fit', 'up', 'finish', 'bin', 'trav'], med))))
+"""
+
+
+def main():
+    lvl = sys.argv[1] if len(sys.argv) > 1 else "9"
+    libs = [os.path.join(ROOT, "paper_2401_07361_b200", "lib", "libspheresum_b200.so")]
+    libs += sorted(glob.glob(os.path.join(ROOT, "paper_2401_07361_b200", "lib", "variants", "*.so")))
+    for lib in libs:
+        env = dict(os.environ, SSUM_LIBRARY=lib)
+        r = subprocess.run([sys.executable, "-c", CHILD, lvl], cwd=ROOT, env=env, capture_output=True, text=True)
+        tail = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr.strip()[-300:]
+        print(os.path.basename(lib), tail, flush=True)
+
+
+if __name__ == "__main__":
+    main()
