@@ -77,7 +77,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -87,7 +87,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def window(self, t0, t1):
+        """Keep the samples taken during [t0, t1] (the timed region); if the
+        region is shorter than the sampling period keep the nearest one."""
+        inside = [r for t, r in self.rows if t0 <= t <= t1 + 0.05]
+        if not inside and self.rows:
+            inside = [min(self.rows, key=lambda tr: abs(tr[0] - t1))[1]]
+        self.rows = [(0.0, r) for r in inside]
 
     def __exit__(self, *a):
         if self.proc:
@@ -100,6 +108,7 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        self.rows = [r for _, r in self.rows] if isinstance(self.rows[0], tuple) else self.rows
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -186,6 +195,7 @@ def run_gpu(args):
         ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
                                d_out.data_ptr(), stats=st)
 
+    clocks = ClockSampler(local).__enter__()
     for _ in range(max(args.warmup, 3)):
         step(ss.TreecodeStats())
     torch.cuda.synchronize()
@@ -198,7 +208,8 @@ def run_gpu(args):
 
     times, pp_ms, launches = [], [], 0
     stats = None
-    with ClockSampler(local) as clocks:
+    t_start = time.perf_counter()
+    if True:
         for _ in range(args.steps):
             flush.zero_()
             barrier()
@@ -213,6 +224,10 @@ def run_gpu(args):
             pp_ms.append(stats.pp_pc_ms)
             launches += stats.gpu_launches
         barrier()
+    t_end = time.perf_counter()
+    time.sleep(0.12)
+    clocks.__exit__(None, None, None)
+    clocks.window(t_start, t_end)
     total_ms = sum(times)
     if ws > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -226,11 +241,22 @@ def run_gpu(args):
     h_q = torch.from_numpy(q).pin_memory()
     h_out = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
     e2e_times = []
-    ctree = tree
+    if ws > 1:
+        from paper_2401_07361_b200.dist import gather_rows
     for k in range(min(args.steps, 5) + 1):
         barrier()
         t0 = time.perf_counter()
-        ss.treecode_sum(ss.BiotSavartKernel, h_xyz.numpy(), h_q.numpy(), cfg, tree=ctree, out=h_out.numpy())
+        if ws == 1:
+            # the public host-pointer entry point: H2D, bin, traverse, evaluate, D2H
+            ss.treecode_sum(ss.BiotSavartKernel, h_xyz.numpy(), h_q.numpy(), cfg, tree=tree, out=h_out.numpy())
+        else:
+            # per rank: H2D, this rank's targets, NCCL all-gather of the rows, D2H of all N rows
+            d_xyz.copy_(h_xyz, non_blocking=True)
+            d_q.copy_(h_q, non_blocking=True)
+            step(ss.TreecodeStats())
+            gather_rows(tree, d_out)
+            h_out.copy_(d_out)
+            torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if k > 0:
             e2e_times.append(dt)
