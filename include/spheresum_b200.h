@@ -124,6 +124,16 @@ int ssum_tree_export(ssum_ctx* ctx, int* level, int* parent, int* child_base, do
 int ssum_dual_traversal(ssum_ctx* ctx, const ssum_config* cfg, int* tsk, int64_t cap,
                         int64_t* count);
 
+/* eval_pp / eval_pc / eval_cp / eval_cc (treecode.hpp:55-73,
+ * treecode.cpp:170-244): ADDS the raw kernel sums (no prefactor) of one
+ * interaction (target, source: reference node ids of the tree as last binned
+ * from these positions; kind: 0 PP, 1 PC, 2 CP, 3 CC) into field (host,
+ * N x D, caller's order). Proxy weights and fits are computed for this
+ * interaction alone, as the reference's per-interaction entry points do. */
+int ssum_eval_interaction(ssum_ctx* ctx, int kernel, const ssum_config* cfg, const double* xyz,
+                          const double* q, int64_t n, int target, int source, int kind,
+                          double* field);
+
 /* ---- multi-GPU target partition (no reference equivalent) */
 /* Subsequent treecode evaluations compute only part `part` of `nparts`
  * cost-balanced contiguous ranges of target leaves (tree order) and write only

@@ -273,6 +273,42 @@ int ref_treecode_sum_tree(void* h, int kernel, const double* xyz, const double* 
   });
 }
 
+// eval_pp / eval_pc / eval_cp / eval_cc (treecode.cpp:170-244) on a binned
+// reference tree: adds raw sums into field (N x D).
+int ref_eval_interaction(void* h, int kernel, const double* xyz, const double* q, int64_t n, double theta, int nt,
+                         int degree, int max_depth, int target, int source, int kind, double* field) {
+  return guarded([&] {
+    const FaceTree& tree = *static_cast<FaceTree*>(h);
+    const auto pts = to_points(xyz, n);
+    const std::vector<double> s(q, q + n);
+    const TraversalConfig cfg = make_cfg(theta, nt, degree, max_depth);
+    Interaction it;
+    it.target = target;
+    it.source = source;
+    it.kind = static_cast<InteractionKind>(kind);
+    auto run = [&](auto tag) {
+      using K = decltype(tag);
+      PotentialField<K::dim> f(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i)
+        for (int d = 0; d < K::dim; ++d) f[i][d] = field[i * K::dim + d];
+      if (kind == 0)
+        eval_pp<K>(tree, it, pts, s, f);
+      else if (kind == 1)
+        eval_pc<K>(tree, it, pts, s, cfg, f);
+      else if (kind == 2)
+        eval_cp<K>(tree, it, pts, s, cfg, f);
+      else
+        eval_cc<K>(tree, it, pts, s, cfg, f);
+      for (int64_t i = 0; i < n; ++i)
+        for (int d = 0; d < K::dim; ++d) field[i * K::dim + d] = f[i][d];
+    };
+    if (kernel == 0)
+      run(BiotSavartKernel{});
+    else
+      run(LogPotentialKernel{});
+  });
+}
+
 // --- SBB / geometry probes used by the KAT tests ---------------------------
 int ref_sbb_eval(int degree, double b1, double b2, double b3, double* out) {
   return guarded([&] { SBBBasis(degree).eval({b1, b2, b3}, out); });

@@ -38,7 +38,7 @@ __all__ = [
     "direct_sum", "treecode_sum", "rk4", "make_icosa_mesh", "rh4_vorticity",
     "make_random_cap", "GeometryError", "SingularKernelError", "ConditioningError",
     "ConfigError", "CudaError", "SpheresumError", "library_path", "load_library",
-    "mac_well_separated",
+    "mac_well_separated", "eval_pp", "eval_pc", "eval_cp", "eval_cc",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -108,7 +108,7 @@ EXPORTED_SYMBOLS = (
     "ssum_bin_particles", "ssum_tree_node_count", "ssum_tree_export", "ssum_dual_traversal",
     "ssum_rk4", "ssum_mesh_vertex_count", "ssum_make_icosa_mesh", "ssum_rh4_vorticity",
     "ssum_make_random_cap", "ssum_fp64_peak", "ssum_set_partition", "ssum_partition_range",
-    "ssum_tree_perm",
+    "ssum_tree_perm", "ssum_eval_interaction",
 )
 
 
@@ -149,6 +149,8 @@ def load_library():
         "ssum_set_partition": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
         "ssum_partition_range": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
         "ssum_tree_perm": (ctypes.c_int, [_P, _P, ctypes.c_int]),
+        "ssum_eval_interaction": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_Config), _P, _P, _I64, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.c_int, _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -457,6 +459,45 @@ def dual_traversal_array(tree: FaceTree, cfg: TraversalConfig) -> np.ndarray:
     tree._check(tree._lib.ssum_dual_traversal(tree._h, ctypes.byref(c), _ptr(out), count.value,
                                               ctypes.byref(count)))
     return out[: count.value]
+
+
+def _eval_interaction(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: TraversalConfig,
+                      field: np.ndarray) -> None:
+    k = _kernel_id(kernel)
+    cfg.validate()
+    p = _as_positions(positions)
+    n = p.shape[0]
+    q = _as_vector(strengths, n, "strengths")
+    d = 3 if k == 0 else 1
+    if field.dtype != np.float64 or not field.flags.c_contiguous or field.size != n * d:
+        raise ValueError(f"field must be a C-contiguous float64 array with {n * d} entries")
+    c = cfg._c()
+    tree._check(tree._lib.ssum_eval_interaction(tree._h, k, ctypes.byref(c), _ptr(p), _ptr(q), n, int(it.target),
+                                                int(it.source), int(it.kind), _ptr(field)))
+
+
+def eval_pp(kernel, tree: FaceTree, it: Interaction, positions, strengths, field: np.ndarray) -> None:
+    """eval_pp<K> (treecode.cpp:170-186): adds raw PP sums of one interaction
+    into field (N, dim), no prefactor. The tree must be binned on positions."""
+    _eval_interaction(kernel, tree, it, positions, strengths, TraversalConfig(), field)
+
+
+def eval_pc(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: TraversalConfig,
+            field: np.ndarray) -> None:
+    """eval_pc<K> (treecode.cpp:188-201)."""
+    _eval_interaction(kernel, tree, it, positions, strengths, cfg, field)
+
+
+def eval_cp(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: TraversalConfig,
+            field: np.ndarray) -> None:
+    """eval_cp<K> (treecode.cpp:203-221)."""
+    _eval_interaction(kernel, tree, it, positions, strengths, cfg, field)
+
+
+def eval_cc(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: TraversalConfig,
+            field: np.ndarray) -> None:
+    """eval_cc<K> (treecode.cpp:223-244)."""
+    _eval_interaction(kernel, tree, it, positions, strengths, cfg, field)
 
 
 _DEFAULT_TREES = {}

@@ -94,6 +94,8 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
   }
 }
 
+}  // namespace
+
 // Reference node ids: roots 0..19; each bin_particles call appends the quads
 // it creates in the order distribute() visits their parents (depth-first
 // preorder, face_tree.cpp:39-71). Returns dev -> ref.
@@ -125,6 +127,8 @@ std::vector<int> reference_ids(const HostTree& h) {
   return ref;
 }
 
+namespace {
+
 void upload(Ctx& c, DBuf<double>& buf, const double* h, size_t count, ssum_stats* st) {
   const auto t0 = clk::now();
   buf.ensure(std::max<size_t>(count, 1));
@@ -140,6 +144,17 @@ void download(Ctx& c, double* h, const double* d, size_t count, ssum_stats* st) 
   if (count) SSUM_CUDA_CHECK(cudaMemcpyAsync(h, d, count * 8, cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   if (st) st->d2h_seconds += secs(t0, clk::now());
+}
+
+__global__ void k_add_scaled(double* __restrict__ y, const double* __restrict__ x, double a, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+
+void add_scaled(Ctx& c, double* y, const double* x, double a, int64_t n) {
+  k_add_scaled<<<grid_for(n, 256), 256, 0, c.stream>>>(y, x, a, n);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
 }
 
 __global__ void k_rk4_stage(int64_t n, int stage, double cs, const double* __restrict__ x0,
@@ -417,6 +432,51 @@ int ssum_dual_traversal(ssum_ctx* h, const ssum_config* cfg, int* tsk, int64_t c
       tsk[3 * e + 1] = ref[list[size_t(e)].y];
       tsk[3 * e + 2] = list[size_t(e)].z;
     }
+  });
+}
+
+int ssum_eval_interaction(ssum_ctx* h, int kernel, const ssum_config* cfg, const double* xyz, const double* q,
+                          int64_t n, int target, int source, int kind, double* field) {
+  return guarded(h, [&](Ctx& c) {
+    validate(cfg);
+    check_kernel(kernel);
+    check_n(n);
+    if (n != c.bins.n) throw Error(SSUM_INVALID, "eval_interaction: positions do not match the binned tree");
+    if (kind < 0 || kind > 3) throw Error(SSUM_INVALID, "eval_interaction: unknown interaction kind");
+    if (n == 0) return;
+    const std::vector<int> ref = reference_ids(c.host);
+    const int nn = static_cast<int>(ref.size());
+    if (target < 0 || target >= nn || source < 0 || source >= nn)
+      throw Error(SSUM_INVALID, "eval_interaction: node id out of range");
+    std::vector<int> dev_of(static_cast<size_t>(nn));
+    for (int d = 0; d < nn; ++d) dev_of[static_cast<size_t>(ref[d])] = d;
+    const int D = kernel == SSUM_BIOT_SAVART ? 3 : 1;
+    upload(c, c.in_xyz, xyz, size_t(n) * 3, nullptr);
+    upload(c, c.in_q, q, size_t(n), nullptr);
+    c.out_buf.ensure(size_t(n) * D * 2);
+    const int4 it{dev_of[static_cast<size_t>(target)], dev_of[static_cast<size_t>(source)], kind, 0};
+    c.lists.inter.ensure(1);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.lists.inter.p, &it, sizeof(int4), cudaMemcpyHostToDevice, c.stream));
+    c.lists.n_inter = 1;
+    const int part = c.part, nparts = c.nparts;
+    c.part = 0;
+    c.nparts = 1;
+    try {
+      build_lists(c, *cfg);
+      evaluate(c, kernel, *cfg, c.in_xyz.p, c.in_q.p, n, c.out_buf.p, nullptr);
+    } catch (...) {
+      c.part = part;
+      c.nparts = nparts;
+      throw;
+    }
+    c.part = part;
+    c.nparts = nparts;
+    // field += out / prefactor (raw kernel sums, treecode.hpp:53-54)
+    double* d_field = c.out_buf.p + size_t(n) * D;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(d_field, field, size_t(n) * D * 8, cudaMemcpyHostToDevice, c.stream));
+    const double inv_pref = kernel == SSUM_BIOT_SAVART ? -4.0 * 3.14159265358979323846 : 1.0;
+    add_scaled(c, d_field, c.out_buf.p, inv_pref, int64_t(n) * D);
+    download(c, field, d_field, size_t(n) * D, nullptr);
   });
 }
 

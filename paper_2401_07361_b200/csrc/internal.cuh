@@ -214,6 +214,8 @@ void tree_init_roots(Ctx& c);
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
 void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
 void partition_targets(Ctx& c);
+void build_lists(Ctx& c, const ssum_config& cfg);
+std::vector<int> reference_ids(const HostTree& h);
 void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,
               int64_t n, double* d_out, ssum_stats* st);
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,

@@ -409,6 +409,24 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     m = next;
   }
   L.n_inter = ne;
+  build_lists(c, cfg);
+}
+
+// From the emitted interactions (L.inter[0, L.n_inter)) to the evaluation
+// layout: node flags, proxy slots, leaf tiles, fit tiles, target partition.
+void build_lists(Ctx& c, const ssum_config& cfg) {
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  TravScratch& S = scratch(c);
+  const int nn = c.nodes.count;
+  const int64_t N = B.n;
+  const int P = (cfg.degree + 1) * (cfg.degree + 2) / 2;
+  const int bs = 256;
+  const long long ne = L.n_inter;
+  for (int k = 0; k < 4; ++k) L.counts[k] = L.evals[k] = 0;
+  L.n_proxy = L.n_weight = L.n_fit = L.n_leaf_tiles = L.n_fit_tiles = 0;
+  L.n_leaf_ranges = L.n_fit_ranges = 0;
+  if (N == 0) return;
 
   // ---- node flags, kind counts, grouping by (target, class)
   L.is_weight.ensure(size_t(nn));

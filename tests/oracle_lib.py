@@ -187,6 +187,14 @@ class RefTree:
         _check(ref().ref_dual_traversal(self.h, theta, nt, degree, max_depth, _p(tsk), cnt.value, ctypes.byref(cnt)))
         return tsk[: cnt.value]
 
+    def eval_interaction(self, kernel, xyz, q, theta, nt, degree, max_depth, target, source, kind, field):
+        """eval_pp/pc/cp/cc<K> (treecode.cpp:170-244): adds into field in place."""
+        lib = ref()
+        lib.ref_eval_interaction.argtypes = [_P, ctypes.c_int, _P, _P, _I64, _D, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+        _check(lib.ref_eval_interaction(self.h, kernel, _p(xyz), _p(q), xyz.shape[0], theta, nt, degree, max_depth,
+                                        int(target), int(source), int(kind), _p(field)))
+
     def treecode(self, kernel, xyz, q, theta, nt, degree, max_depth=10, workers=1):
         n = xyz.shape[0]
         d = 3 if kernel == 0 else 1

@@ -244,6 +244,40 @@ def test_small_inputs(ss, ol):
     assert empty.shape == (0, 3)
 
 
+# ------------------------------------------------- per-interaction API
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_eval_interaction_matches_reference(ss, ol, mesh_fixture, kernel):
+    """eval_pp / eval_pc / eval_cp / eval_cc (treecode.cpp:170-244) on the
+    same binned tree, for interactions of every kind from the real list."""
+    xyz, q, a = mesh_fixture(5)
+    c = cfg(ss, nt=64, deg=4)
+    t = ss.FaceTree()
+    t.bin_particles(xyz, 64, 10)
+    r = ol.RefTree()
+    r.bin(xyz, 64, 10)
+    lst = r.traversal(0.7, 64, 4, 10)
+    rng = np.random.default_rng(1)
+    K = ss.BiotSavartKernel if kernel == 0 else ss.LogPotentialKernel
+    fns = {0: ss.eval_pp, 1: ss.eval_pc, 2: ss.eval_cp, 3: ss.eval_cc}
+    D = 3 if kernel == 0 else 1
+    for kind in range(4):
+        picks = np.flatnonzero(lst[:, 2] == kind)
+        for e in rng.choice(picks, size=min(6, picks.size), replace=False):
+            tgt, src, _ = lst[e]
+            base = rng.standard_normal((xyz.shape[0], D))
+            mine = base.copy()
+            it = ss.Interaction(int(tgt), int(src), ss.InteractionKind(kind))
+            if kind == 0:
+                fns[kind](K, t, it, xyz, q, mine)
+            else:
+                fns[kind](K, t, it, xyz, q, c, mine)
+            ref = base.copy()
+            r.eval_interaction(kernel, xyz, q, 0.7, 64, 4, 10, tgt, src, kind, ref)
+            dm, dr = mine - base, ref - base
+            assert np.abs(dr).max() > 0
+            assert ol.rel_l2(dm, dr) < REL_TOL, (kind, tgt, src)
+
+
 # ---------------------------------------------------- multi-GPU partition
 @pytest.mark.parametrize("which", ["mesh", "cap"])
 def test_partition_union_is_bitwise_single_part(ss, mesh_fixture, which):
