@@ -15,6 +15,19 @@ namespace ssum {
 
 void sorted_interactions(Ctx& c, std::vector<int4>& out);
 
+double Trace::now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+Trace& trace() {
+  static Trace t = [] {
+    Trace x;
+    const char* e = std::getenv("SSUM_TRACE");
+    x.on = e && *e && *e != '0';
+    return x;
+  }();
+  return t;
+}
+
 void check_flags(Ctx& c, const char* where) {
   int f = 0;
   SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -70,14 +83,35 @@ int guarded(ssum_ctx* h, F&& f) {
 void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q, int64_t n,
                      double* d_out, ssum_stats* st) {
   const int64_t l0 = c.launches;
+  Trace& tr = trace();
+  if (tr.on) tr.start();
   const auto t0 = clk::now();
   tree_bin(c, d_xyz, n, cfg.n_threshold, cfg.max_depth);
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  tr.mark("bin.done");
   const auto t1 = clk::now();
   traverse_and_build_lists(c, cfg, false);
+  tr.mark("lists.done");
   const auto t2 = clk::now();
   evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
+  tr.mark("eval.done");
   const auto t3 = clk::now();
+  if (tr.on) {  // per label: total ms (count)
+    double prev = tr.t0;
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+    for (const auto& m : tr.marks) {
+      const double dt = (m.second - prev) * 1e3;
+      prev = m.second;
+      auto it = std::find_if(agg.begin(), agg.end(), [&](const auto& a) { return a.first == m.first; });
+      if (it == agg.end())
+        agg.push_back({m.first, {dt, 1}});
+      else
+        it->second.first += dt, it->second.second += 1;
+    }
+    std::fprintf(stderr, "[ssum trace]");
+    for (const auto& a : agg) std::fprintf(stderr, " %s=%.3f(%d)", a.first.c_str(), a.second.first, a.second.second);
+    std::fprintf(stderr, "\n");
+  }
   if (st) {
     st->bin_seconds += secs(t0, t1);
     st->traversal_seconds += secs(t1, t2);

@@ -140,6 +140,26 @@ __global__ void __launch_bounds__(128) k_up_partial(const int4* __restrict__ chu
     wpart[size_t(blockIdx.x) * P + m] = ((red[0][m] + red[1][m]) + red[2][m]) + red[3][m];
 }
 
+constexpr int kUpChunk = 1024;  // particles per upward chunk
+
+__global__ void k_up_nchunks(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ cnt,
+                             int* __restrict__ nch) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nw) nch[w] = (cnt[weight_nodes[w]] + kUpChunk - 1) / kUpChunk;
+  if (w == nw) nch[w] = 0;
+}
+
+__global__ void k_up_fill(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ off,
+                          const int* __restrict__ cnt, const int* __restrict__ chunk_off, int4* __restrict__ chunks,
+                          int2* __restrict__ crange) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nw) return;
+  const int id = weight_nodes[w], o = off[id], cn = cnt[id];
+  int k = chunk_off[w];
+  crange[w] = make_int2(k, chunk_off[w + 1]);
+  for (int b = 0; b < cn; b += kUpChunk, ++k) chunks[k] = make_int4(id, o + b, min(kUpChunk, cn - b), 0);
+}
+
 // w = sum of the node's chunk partials (in chunk order); w_hat = V^-T w.
 __global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const int2* __restrict__ chunk_range,
                            const double* __restrict__ wpart, const double* __restrict__ vinv, int P,
@@ -364,32 +384,37 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   }
   cudaEventRecord(c.ev[1], c.stream);
 
-  // ---- upward pass: chunk table on the host (weight nodes and their bins)
+  // ---- upward pass: chunk table (weight node bins cut into <= 1024-particle
+  // chunks) built on the device
   if (L.n_weight > 0) {
-    const int kChunk = 1024;
-    std::vector<int4> chunks;
-    std::vector<int2> crange(static_cast<size_t>(L.n_weight));
-    for (int w = 0; w < L.n_weight; ++w) {
-      const int id = L.h_weight_nodes[w];
-      const int o = c.host.off[id], cn = c.host.cnt[id];
-      crange[w].x = static_cast<int>(chunks.size());
-      for (int b = 0; b < cn; b += kChunk) chunks.push_back(int4{id, o + b, std::min(kChunk, cn - b), 0});
-      crange[w].y = static_cast<int>(chunks.size());
-    }
-    const int nch = static_cast<int>(chunks.size());
-    c.wchunks.ensure(size_t(nch) + size_t(L.n_weight));
+    const int nw = L.n_weight;
+    c.wcount.ensure(size_t(nw) + 1);
+    c.wcount_off.ensure(size_t(nw) + 1);
+    k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, c.stream>>>(L.weight_nodes.p, nw, B.cnt.p, c.wcount.p);
+    SSUM_LAUNCH_CHECK();
+    size_t tb = 0;
+    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
+    c.cub_tmp.ensure(tb);
+    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
+    int nch = 0;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&nch, c.wcount_off.p + nw, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.wchunks.ensure(size_t(nch) + size_t(nw));
     c.wpart.ensure(size_t(nch) * P);
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.wchunks.p, chunks.data(), size_t(nch) * sizeof(int4), cudaMemcpyHostToDevice, c.stream));
     int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(d_crange, crange.data(), crange.size() * sizeof(int2), cudaMemcpyHostToDevice, c.stream));
+    k_up_fill<<<grid_for(nw, 256), 256, 0, c.stream>>>(L.weight_nodes.p, nw, B.off.p, B.cnt.p, c.wcount_off.p,
+                                                       c.wchunks.p, d_crange);
+    SSUM_LAUNCH_CHECK();
+    c.launches += 4;
     if (nch > 0) launch_up_partial(c, degree, nch);
     const int bt = ((P + 31) / 32) * 32;
     k_up_final<<<L.n_weight, bt, size_t(P) * 8, c.stream>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
                                                              P, L.pslot.p, n, c.pts.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));  // host vectors above are released
+    // (pageable H2D copies have consumed the host vectors when they return)
   }
+  trace().mark("eval.upward_host");
   cudaEventRecord(c.ev[2], c.stream);
 
   // ---- CP/CC + fit

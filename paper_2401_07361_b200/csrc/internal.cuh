@@ -141,7 +141,6 @@ struct Lists {
   DBuf<int> pslot;           // node -> proxy slot or -1
   DBuf<unsigned char> is_weight, is_fit;
   DBuf<int> weight_nodes, fit_nodes;  // slot-ordered node lists
-  std::vector<int> h_weight_nodes, h_fit_nodes;
   int n_leaf_tiles = 0, n_fit_tiles = 0;
   DBuf<Tile> leaf_tiles, fit_tiles;
   int64_t n_leaf_ranges = 0, n_fit_ranges = 0;
@@ -197,7 +196,8 @@ struct Ctx {
   DBuf<double> S;                    // per tree position accumulated kernel sums (D doubles)
   DBuf<double> coeff;                // per proxy slot: D x P fit coefficients
   DBuf<double> wpart;                // upward partial sums
-  DBuf<int4> wchunks;                // upward chunks (slot, begin, count, node)
+  DBuf<int4> wchunks;                // upward chunks (node, begin, count, 0) + per-node chunk ranges
+  DBuf<int> wcount, wcount_off;      // chunks per weight node, and their prefix
   DBuf<double> vinv;                 // P x P inverse Vandermonde (row-major), per degree
   int vinv_degree = -1;
   DBuf<double> in_xyz, in_q, out_buf;  // staging for host-pointer entry points
@@ -208,6 +208,23 @@ struct Ctx {
   size_t h_stage_bytes = 0;
   cudaEvent_t ev[8];
 };
+
+// Host-side phase trace (SSUM_TRACE=1): wall time between marks, printed by
+// the caller. Costs nothing when disabled.
+struct Trace {
+  bool on = false;
+  std::vector<std::pair<const char*, double>> marks;
+  double t0 = 0.0;
+  static double now();
+  void start() {
+    marks.clear();
+    t0 = now();
+  }
+  void mark(const char* what) {
+    if (on) marks.emplace_back(what, now());
+  }
+};
+Trace& trace();
 
 // ---- passes (tree.cu / traversal.cu / eval.cu) ------------------------------
 void tree_init_roots(Ctx& c);

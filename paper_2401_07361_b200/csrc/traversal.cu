@@ -409,6 +409,7 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     m = next;
   }
   L.n_inter = ne;
+  trace().mark("trav.bfs");
   build_lists(c, cfg);
 }
 
@@ -434,7 +435,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   L.pslot.ensure(size_t(nn));
   SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_weight.p, 0, size_t(nn), c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_fit.p, 0, size_t(nn), c.stream));
-  S.counters.ensure(8);
+  S.counters.ensure(16);
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), c.stream));
   const size_t nes = size_t(std::max<long long>(ne, 1));
   S.gkey.ensure(nes);
@@ -475,40 +476,34 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
                                                   S.slot_node.p);
   SSUM_LAUNCH_CHECK();
   c.launches += 2;
+  // weight / fit node lists in slot order (= node-id order): device compaction
+  L.weight_nodes.ensure(size_t(nn));
+  L.fit_nodes.ensure(size_t(nn));
   {
-    int tail[2];
+    int* nsel = reinterpret_cast<int*>(S.counters.p + 8);  // [0] weight nodes, [1] fit nodes
+    cub::CountingInputIterator<int> ids(0);
+    size_t t1 = 0, t2 = 0;
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, t1, ids, L.is_weight.p, L.weight_nodes.p,
+                                               nsel, nn, c.stream));
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, t2, ids, L.is_fit.p, L.fit_nodes.p,
+                                               nsel + 1, nn, c.stream));
+    c.cub_tmp.ensure(std::max(t1, t2));
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(c.cub_tmp.p, t1, ids, L.is_weight.p, L.weight_nodes.p,
+                                               nsel, nn, c.stream));
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(c.cub_tmp.p, t2, ids, L.is_fit.p, L.fit_nodes.p,
+                                               nsel + 1, nn, c.stream));
+    c.launches += 4;
+    int tail[4];
     SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[0], S.flag_scan.p + (nn - 1), 4, cudaMemcpyDeviceToHost, c.stream));
     SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[1], S.flag.p + (nn - 1), 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[2], nsel, 8, cudaMemcpyDeviceToHost, c.stream));
     SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     L.n_proxy = tail[0] + tail[1];
-  }
-  // weight / fit node lists in slot order (host-side compaction of the slot table)
-  {
-    std::vector<int> slot_node(static_cast<size_t>(std::max(L.n_proxy, 1)));
-    std::vector<unsigned char> w(static_cast<size_t>(nn)), f(static_cast<size_t>(nn));
-    if (L.n_proxy > 0)
-      SSUM_CUDA_CHECK(cudaMemcpyAsync(slot_node.data(), S.slot_node.p, size_t(L.n_proxy) * 4, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(w.data(), L.is_weight.p, size_t(nn), cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(f.data(), L.is_fit.p, size_t(nn), cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    std::vector<int> wn, fn;
-    for (int s = 0; s < L.n_proxy; ++s) {
-      const int id = slot_node[s];
-      if (w[id]) wn.push_back(id);
-      if (f[id]) fn.push_back(id);
-    }
-    L.h_weight_nodes = wn;
-    L.h_fit_nodes = fn;
-    L.n_weight = static_cast<int>(wn.size());
-    L.n_fit = static_cast<int>(fn.size());
-    L.weight_nodes.ensure(std::max<size_t>(wn.size(), 1));
-    L.fit_nodes.ensure(std::max<size_t>(fn.size(), 1));
-    if (!wn.empty())
-      SSUM_CUDA_CHECK(cudaMemcpyAsync(L.weight_nodes.p, wn.data(), wn.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    if (!fn.empty())
-      SSUM_CUDA_CHECK(cudaMemcpyAsync(L.fit_nodes.p, fn.data(), fn.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    L.n_weight = tail[2];
+    L.n_fit = tail[3];
   }
 
+  trace().mark("lists.group_slots");
   // ---- leaf tiles
   const int nl = static_cast<int>(B.leaves.size());
   S.nr.ensure(size_t(nl) + 1);
@@ -542,6 +537,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   SSUM_LAUNCH_CHECK();
   c.launches++;
 
+  trace().mark("lists.leaf_tiles");
   // ---- fit tiles
   const int nf = L.n_fit;
   if (nf > 0) {
@@ -573,6 +569,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     L.counts[k] = h[k];
     L.evals[k] = h[4 + k];
   }
+  trace().mark("lists.fit_tiles");
   partition_targets(c);
 }
 
@@ -629,9 +626,14 @@ void partition_targets(Ctx& c) {
     L.local_evals[0] += cost[size_t(t)].x;
     L.local_evals[1] += cost[size_t(t)].y;
   }
+  std::vector<int> fit_nodes(static_cast<size_t>(L.n_fit_tiles));
+  if (L.n_fit_tiles > 0) {
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(fit_nodes.data(), L.fit_nodes.p, fit_nodes.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  }
   std::vector<int> sel;
   for (int k = 0; k < L.n_fit_tiles; ++k) {
-    const int id = L.h_fit_nodes[size_t(k)];
+    const int id = fit_nodes[size_t(k)];
     const int64_t o = c.host.off[size_t(id)], e = o + c.host.cnt[size_t(id)];
     if (o < L.p1 && e > L.p0) {
       sel.push_back(k);

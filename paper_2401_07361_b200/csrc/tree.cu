@@ -288,6 +288,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   SSUM_LAUNCH_CHECK();
   c.launches++;
   check_flags(c, "bin_particles: particle contained in no root face");
+  trace().mark("bin.roots");
 
   std::vector<int> cand(20);
   for (int f = 0; f < 20; ++f) cand[f] = f;
@@ -304,6 +305,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     counts.resize(size_t(m));
     SSUM_CUDA_CHECK(cudaMemcpyAsync(counts.data(), B.d_cnt.p, size_t(m) * 4, cudaMemcpyDeviceToHost, c.stream));
     check_flags(c, "bin_particles: degenerate child triangle");  // synchronises
+    trace().mark("bin.lvl_counts");
 
     std::vector<int> front;
     front.reserve(size_t(m));
@@ -335,6 +337,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
       if (a == kActLeaf) B.leaves.push_back(id);
       fa.push_back(int2{id, a});
     }
+    trace().mark("bin.lvl_host");
     if (front.empty()) break;
     B.frontier.push_back(std::move(front));
 
@@ -364,6 +367,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     SSUM_LAUNCH_CHECK();
     c.launches += 2;
 
+    trace().mark("bin.lvl_launch");
     cand.clear();
     for (const int2& p : fa)
       if (p.y == kActDescend)
@@ -371,31 +375,39 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   }
   B.max_level = static_cast<int>(B.frontier.size()) - 1;
 
-  // Bin offsets in depth-first order: roots in face order, children in order.
-  int64_t run = 0;
-  for (int f = 0; f < 20; ++f) {
-    h.off[f] = static_cast<int>(run);
-    run += h.cnt[f];
-  }
-  for (const auto& front : B.frontier)
-    for (const int id : front) {
-      const int cb = h.child_base[id];
-      if (cb < 0) continue;
-      int o = h.off[id];
-      for (int q = 0; q < 4; ++q) {
-        h.off[cb + q] = o;
-        o += h.cnt[cb + q];
+  // Bin offsets in depth-first order (roots in face order, children in
+  // order) and the leaves in that order — one preorder walk over the
+  // non-empty nodes. Leaf tiles then cover the tree-order particle array
+  // left to right, which the target partition relies on.
+  {
+    std::vector<char> is_leaf(h.level.size(), 0);
+    for (const int id : B.leaves) is_leaf[size_t(id)] = 1;
+    B.leaves.clear();
+    std::vector<int> stack;
+    stack.reserve(256);
+    for (int f = 19; f >= 0; --f) stack.push_back(f);
+    int run = 0;
+    while (!stack.empty()) {
+      const int id = stack.back();
+      stack.pop_back();
+      if (h.cnt[size_t(id)] == 0) continue;
+      h.off[size_t(id)] = run;
+      if (is_leaf[size_t(id)]) {
+        B.leaves.push_back(id);
+        run += h.cnt[size_t(id)];
+      } else {
+        const int cb = h.child_base[size_t(id)];
+        for (int q = 3; q >= 0; --q) stack.push_back(cb + q);
       }
     }
+  }
   B.off.ensure(size_t(c.nodes.count));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.off.p, h.off.data(), size_t(c.nodes.count) * 4, cudaMemcpyHostToDevice, c.stream));
-  // leaves in depth-first (tree-position) order: leaf tiles then cover the
-  // tree-order particle array left to right, which the target partition uses
-  std::sort(B.leaves.begin(), B.leaves.end(), [&](int a, int b) { return h.off[a] < h.off[b]; });
   B.d_leaves.ensure(std::max<size_t>(B.leaves.size(), 1));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.d_leaves.p, B.leaves.data(), B.leaves.size() * 4, cudaMemcpyHostToDevice, c.stream));
 
   // Permutation: stable sort of particle ids by their leaf's offset.
+  trace().mark("bin.offsets");
   B.sort_keys.ensure(size_t(n));
   B.sort_keys2.ensure(size_t(n));
   B.sort_vals.ensure(size_t(n));
