@@ -158,6 +158,79 @@ __device__ __forceinline__ void pair_quad(double x0, double x1, double x2, const
   }
 }
 
+// NS sources x NT targets of well-separated pairs, written stage by stage
+// across the NS*NT independent chains (all denominators, then all
+// reciprocal seeds, then each Newton step, then the accumulations) so that
+// consecutive instructions belong to different chains and the in-order
+// issue never waits on a DFMA (8.8 cycles) or MUFU.RCP64H (~24 cycles)
+// result it just produced.
+// NEAR: the block may hold near pairs (self pairs, 1 - x.y < 2^-20): one warp
+// vote for the whole block; a block with a near lane replays its pairs
+// through the per-pair exact path (ti: target indices, J: source indices).
+template <int KER, int NT, int NS, bool NEAR = false>
+__device__ __forceinline__ void far_block(const double4* x, const double4* __restrict__ B, int k, int G, Acc<KER>* a,
+                                          const int* ti = nullptr, const int* __restrict__ J = nullptr,
+                                          int* flags = nullptr) {
+  constexpr int C = NT * NS;
+  double4 y[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) y[s] = B[k + s * G];
+  double den[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].x, y[c / NT].x, 1.0);
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].y, y[c / NT].y, den[c]);
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].z, y[c / NT].z, den[c]);
+  if constexpr (NEAR) {
+    bool nr = false;
+#pragma unroll
+    for (int c = 0; c < C; ++c) nr |= __double2hiint(den[c]) < kNearHi;
+    if (__any_sync(0xffffffffu, nr)) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double v[KDim<KER>::D];
+        const double4& yy = y[c / NT];
+        if (__double2hiint(den[c]) < kNearHi) {
+          pair_slow<KER>(x[c % NT].x, x[c % NT].y, x[c % NT].z, yy, ti[c % NT], J[k + (c / NT) * G], v, flags);
+        } else if constexpr (KER == kBS) {
+          const double r = q_over(yy.w, den[c]);
+          v[0] = r * yy.x;
+          v[1] = r * yy.y;
+          v[2] = r * yy.z;
+        } else {
+          v[0] = yy.w * log(den[c]);
+        }
+#pragma unroll
+        for (int d = 0; d < KDim<KER>::D; ++d) a[c % NT].s[d] += v[d];
+      }
+      return;
+    }
+  }
+  if constexpr (KER == kBS) {
+    double r[C], e[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = rcp_approx(den[c]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) e[c] = fma(-den[c], r[c], 1.0);
+#pragma unroll
+    for (int c = 0; c < C; ++c) e[c] = fma(e[c], e[c], e[c]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = y[c / NT].w * r[c];
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = fma(r[c], e[c], r[c]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(r[c], y[c / NT].x, a[c % NT].s[0]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[1] = fma(r[c], y[c / NT].y, a[c % NT].s[1]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[2] = fma(r[c], y[c / NT].z, a[c % NT].s[2]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(y[c / NT].w, log(den[c]), a[c % NT].s[0]);
+  }
+}
+
 // One source against NT register-tiled targets with a single warp vote: the
 // NT denominator chains are independent, so they interleave; only a source
 // with a near lane (self pair or 1 - x.y < 2^-20) takes the exact path.

@@ -33,10 +33,16 @@ constexpr int kTileThreads = 256;
 #endif
 constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage (multiple of kTileThreads)
 constexpr int kLeafMode = 0, kFitMode = 1;
-constexpr int kPad = 32;  // >= max G - 1: the stride-G walk reads up to G - 1 entries past n
+#ifndef SSUM_NS
+#define SSUM_NS 2
+#endif
+constexpr int kNs = SSUM_NS;  // sources per fast-loop step
+// zero tail past a chunk: the stride-G walk in steps of kNs sources reads up
+// to kNs*G - 1 entries beyond n
+constexpr int kPad = 32 * SSUM_NS;
 
 #ifndef SSUM_TILE_MINB
-#define SSUM_TILE_MINB 3
+#define SSUM_TILE_MINB 4
 #endif
 #ifndef SSUM_TPT
 #define SSUM_TPT 2
@@ -144,20 +150,17 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     const int* J = sid[c & 1];
     const int iters = (n + G - 1) / G;
     if (MODE == kLeafMode && c * kChunk < T.near_total) {
-      // chunk holds near-possible sources: per-pair warp vote + exact path
-#pragma unroll 2
-      for (int it = 0; it < iters; ++it) {
-        const int k = g + it * G;
-        source_near<KER, kTpt>(x, B[k], ti, J[k], a, flags);
-      }
+      // chunk holds near-possible sources: the same staged blocks, one warp
+      // vote per block, exact per-pair path only for blocks with a near lane
+      const int steps = (iters + kNs - 1) / kNs;
+#pragma unroll 1
+      for (int it = 0; it < steps; ++it) far_block<KER, kTpt, kNs, true>(x, B, g + it * kNs * G, G, a, ti, J, flags);
     } else {
-      // well-separated sources only: branch-free fast loop, kTpt chains per source
-#pragma unroll 4
-      for (int it = 0; it < iters; ++it) {
-        const double4 y = B[g + it * G];
-#pragma unroll
-        for (int q = 0; q < kTpt; ++q) pair_far<KER>(x[q].x, x[q].y, x[q].z, y, a[q]);
-      }
+      // well-separated sources only: branch-free, kNs sources x kTpt targets
+      // of independent chains per step (zero-padded tail contributes 0)
+      const int steps = (iters + kNs - 1) / kNs;
+#pragma unroll 2
+      for (int it = 0; it < steps; ++it) far_block<KER, kTpt, kNs>(x, B, g + it * kNs * G, G, a);
     }
     if (more)
 #pragma unroll
