@@ -121,7 +121,7 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
       st->kernel_evals[k] = c.lists.local_evals[k];  // this part's work (all of it when unpartitioned)
     }
     st->node_count = c.nodes.count;
-    st->leaf_count = static_cast<int64_t>(c.bins.leaves.size());
+    st->leaf_count = c.bins.n_leaves;
     st->weight_nodes = c.lists.n_weight;
     st->fit_nodes = c.lists.n_fit;
     st->gpu_launches = c.launches - l0;
@@ -295,6 +295,7 @@ void ssum_destroy(ssum_ctx* h) {
   c->out_buf.release();
   c->rk_state.release();
   for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
@@ -405,7 +406,7 @@ int ssum_tree_node_count(ssum_ctx* h, int* count) {
 int ssum_tree_export(ssum_ctx* h, int* level, int* parent, int* child_base, double* tri, double* center,
                      double* radius, int64_t* bin_offsets, int* bin_ids, int* leaf_of) {
   return guarded(h, [&](Ctx& c) {
-    const HostTree& t = c.host;
+    const HostTree& t = host_tree(c);
     const int nn = c.nodes.count;
     const std::vector<int> ref = reference_ids(t);
     std::vector<int> dev_of(static_cast<size_t>(nn));
@@ -458,7 +459,7 @@ int ssum_dual_traversal(ssum_ctx* h, const ssum_config* cfg, int* tsk, int64_t c
     traverse_and_build_lists(c, *cfg, true);
     std::vector<int4> list;
     sorted_interactions(c, list);
-    const std::vector<int> ref = reference_ids(c.host);
+    const std::vector<int> ref = reference_ids(host_tree(c));
     *count = static_cast<int64_t>(list.size());
     const int64_t m = std::min<int64_t>(cap, *count);
     for (int64_t e = 0; e < m; ++e) {
@@ -478,7 +479,7 @@ int ssum_eval_interaction(ssum_ctx* h, int kernel, const ssum_config* cfg, const
     if (n != c.bins.n) throw Error(SSUM_INVALID, "eval_interaction: positions do not match the binned tree");
     if (kind < 0 || kind > 3) throw Error(SSUM_INVALID, "eval_interaction: unknown interaction kind");
     if (n == 0) return;
-    const std::vector<int> ref = reference_ids(c.host);
+    const std::vector<int> ref = reference_ids(host_tree(c));
     const int nn = static_cast<int>(ref.size());
     if (target < 0 || target >= nn || source < 0 || source >= nn)
       throw Error(SSUM_INVALID, "eval_interaction: node id out of range");

@@ -78,9 +78,11 @@ struct NodeTable {
   DBuf<int> level, parent, child_base, created_call;
 };
 
-// Host mirror of the node structure (ids, levels, links) plus this call's bin
-// counts/offsets. Geometry lives on the device only, except the 20 roots.
+// Host snapshot of the node structure (ids, levels, links, creating call)
+// plus the last binning's counts/offsets. Downloaded on demand (exports,
+// partitioning); the binning itself runs on the device.
 struct HostTree {
+  bool valid = false;
   std::vector<int> level, parent, child_base, created_call;
   std::vector<int> cnt, off;
 };
@@ -88,20 +90,23 @@ struct HostTree {
 // Per-call binned tree (bins as contiguous ranges of the tree-order permutation).
 struct Binned {
   int64_t n = 0;
-  int max_level = 0;
+  int n_leaves = 0;
   DBuf<int> cnt;            // particles per node
   DBuf<int> off;            // first tree position of the node's bin
-  DBuf<unsigned char> act;  // per frontier node: 0 leaf, 1 descend
+  DBuf<unsigned char> act;  // per candidate node: 0 leaf, 1 descend
+  DBuf<unsigned char> is_leaf;  // node is a non-empty leaf of this call
   DBuf<int> cur;            // per particle: current node during the descent
   DBuf<int> leaf_of;        // per particle (original order)
   DBuf<int> perm;           // tree position -> original particle id
   DBuf<int> pos_leaf;       // tree position -> leaf node
   DBuf<int> sort_keys, sort_keys2, sort_vals;
-  DBuf<int> d_ids, d_cnt;
-  DBuf<int2> d_pairs;
-  std::vector<std::vector<int>> frontier;  // host copy: non-empty nodes per level (BFS)
-  std::vector<int> leaves;                 // host copy: non-empty leaves
-  DBuf<int> d_leaves;
+  // level-synchronous descent: candidates of the current level, their split
+  // flags / child counts and prefix sums, all candidates of all levels
+  DBuf<int> cand, cand_next, split, split_pos, nextc, next_pos, levels;
+  std::vector<std::pair<int, int>> level_span;  // (offset in levels, count) per level
+  DBuf<int> d_leaves;       // non-empty leaves in depth-first order
+  DBuf<int> leaf_keys;
+  int* h_small = nullptr;   // pinned host scratch
 };
 
 struct Ctx;
@@ -233,6 +238,7 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
 void partition_targets(Ctx& c);
 void build_lists(Ctx& c, const ssum_config& cfg);
 std::vector<int> reference_ids(const HostTree& h);
+const HostTree& host_tree(Ctx& c);  // downloads the node structure when stale
 void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,
               int64_t n, double* d_out, ssum_stats* st);
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,

@@ -505,7 +505,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
 
   trace().mark("lists.group_slots");
   // ---- leaf tiles
-  const int nl = static_cast<int>(B.leaves.size());
+  const int nl = B.n_leaves;
   S.nr.ensure(size_t(nl) + 1);
   S.nt.ensure(size_t(nl) + 1);
   S.nr_off.ensure(size_t(nl) + 1);
@@ -634,7 +634,8 @@ void partition_targets(Ctx& c) {
   std::vector<int> sel;
   for (int k = 0; k < L.n_fit_tiles; ++k) {
     const int id = fit_nodes[size_t(k)];
-    const int64_t o = c.host.off[size_t(id)], e = o + c.host.cnt[size_t(id)];
+    const HostTree& ht = host_tree(c);
+    const int64_t o = ht.off[size_t(id)], e = o + ht.cnt[size_t(id)];
     if (o < L.p1 && e > L.p0) {
       sel.push_back(k);
       L.local_evals[2] += fcost[size_t(k)].x;

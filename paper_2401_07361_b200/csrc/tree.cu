@@ -1,17 +1,28 @@
 // Face-tree binning on the device: FaceTree::bin_particles / distribute /
 // ensure_children (face_tree.cpp:18-88) restated level-synchronously.
 //
-// The reference descends recursively, node by node. Here every level is one
-// pass over the particles: the host decides per frontier node whether it is a
-// leaf (bin <= N_T, or level >= max_depth, and no children yet), descends into
-// existing children, or splits (face_tree.cpp:40-47); new children get their
-// geometry on the device (k_make_children: bit-exact midpoints and Cramer
-// constants); k_descend moves each particle into the first child whose
-// barycentric min-score is >= -1e-10, else the best-scoring child
-// (face_tree.cpp:50-69), and counts bins with integer atomics. Bins end up as
-// contiguous ranges of a tree-order permutation (depth-first, children in
-// order; particles ascending by id inside each leaf) from one stable radix
-// sort keyed by the leaf's offset.
+// The reference descends recursively, node by node. Here every level is a
+// handful of device passes over the level's candidate nodes and the
+// particles, with one small device->host read per level (how many nodes were
+// split and how many candidates the next level has):
+//   k_level_decide  per candidate: empty (distribute returns,
+//                   face_tree.cpp:40), leaf (bin <= N_T or level >= max_depth,
+//                   and no children yet, :42-45), descend into existing
+//                   children, or split (ensure_children, :18-37);
+//   scans           new node ids (4 per split, in candidate order) and the
+//                   next level's candidate slots;
+//   k_level_apply   child geometry (bit-exact midpoints, circumcentres,
+//                   Cramer constants) and links for the splits, next
+//                   candidates;
+//   k_descend       every particle of a descending node moves to the first
+//                   child whose barycentric min-score is >= -1e-10, else to
+//                   the best-scoring child (face_tree.cpp:50-69); bin counts
+//                   by warp-aggregated integer atomics.
+// Bins end up as contiguous ranges of a tree-order permutation (depth-first,
+// children in order, particles ascending by id inside each leaf): offsets are
+// filled top-down level by level and one stable radix sort keyed by the
+// leaf's offset orders the particles. Node ids are allocated breadth-first;
+// the reference's depth-first numbering is reconstructed on export.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -92,37 +103,74 @@ __device__ void write_node(double* tri, double* center, double* radius, double* 
   if (bad) atomicOr(flags, kFlagGeometry);
 }
 
-// ensure_children (face_tree.cpp:18-37): midpoints renormalised, children
-// {v1,m12,m31}, {m12,v2,m23}, {m31,m23,v3}, {m12,m23,m31}; links written here.
-__global__ void k_make_children(const int2* __restrict__ splits, int ns, double* tri, double* center,
-                                double* radius, double* cramer, int* level, int* parent, int* child_base,
-                                int* flags) {
+// distribute()'s per-node decision (face_tree.cpp:40-47).
+__global__ void k_level_decide(const int* __restrict__ cand, int m, const int* __restrict__ cnt,
+                               const int* __restrict__ child_base, const int* __restrict__ level, int nt,
+                               int max_depth, unsigned char* __restrict__ act, unsigned char* __restrict__ is_leaf,
+                               int* __restrict__ split, int* __restrict__ nextc) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= ns) return;
-  const int par = splits[k].x, base = splits[k].y;
-  const double* t = tri + 9 * par;
-  const d3 v1 = load3(t), v2 = load3(t + 3), v3 = load3(t + 6);
-  int bad = 0;
-  const d3 m12 = unit_rn(add3(v1, v2), &bad);
-  const d3 m23 = unit_rn(add3(v2, v3), &bad);
-  const d3 m31 = unit_rn(add3(v3, v1), &bad);
-  if (bad) atomicOr(flags, kFlagGeometry);
-  write_node(tri, center, radius, cramer, base + 0, v1, m12, m31, flags);
-  write_node(tri, center, radius, cramer, base + 1, m12, v2, m23, flags);
-  write_node(tri, center, radius, cramer, base + 2, m31, m23, v3, flags);
-  write_node(tri, center, radius, cramer, base + 3, m12, m23, m31, flags);
-  const int lv = level[par] + 1;
-  for (int q = 0; q < 4; ++q) {
-    level[base + q] = lv;
-    parent[base + q] = par;
-    child_base[base + q] = -1;
+  if (k > m) return;
+  if (k == m) {  // sentinel for the exclusive scans (totals at index m)
+    split[k] = 0;
+    nextc[k] = 0;
+    return;
   }
-  child_base[par] = base;
+  const int id = cand[k];
+  const int c = cnt[id];
+  int s = 0, nx = 0;
+  if (c > 0) {
+    if (child_base[id] >= 0) {
+      act[id] = kActDescend;
+      nx = 4;
+    } else if (c <= nt || level[id] >= max_depth) {
+      act[id] = kActLeaf;
+      is_leaf[id] = 1;
+    } else {
+      act[id] = kActDescend;
+      s = 1;
+      nx = 4;
+    }
+  }
+  split[k] = s;
+  nextc[k] = nx;
 }
 
-__global__ void k_set_actions(const int2* __restrict__ fa, int nf, unsigned char* act) {
+// ensure_children (face_tree.cpp:18-37) for the splits of this level —
+// midpoints renormalised, children {v1,m12,m31}, {m12,v2,m23},
+// {m31,m23,v3}, {m12,m23,m31} — and the next level's candidate list.
+__global__ void k_level_apply(const int* __restrict__ cand, int m, const int* __restrict__ split,
+                              const int* __restrict__ split_pos, const int* __restrict__ nextc,
+                              const int* __restrict__ next_pos, int node_base, int call_index, double* tri,
+                              double* center, double* radius, double* cramer, int* level, int* parent,
+                              int* child_base, int* created_call, int* __restrict__ cand_next, int* flags) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < nf) act[fa[k].x] = static_cast<unsigned char>(fa[k].y);
+  if (k >= m) return;
+  const int id = cand[k];
+  int cb = child_base[id];
+  if (split[k]) {
+    cb = node_base + 4 * split_pos[k];
+    const double* t = tri + 9 * id;
+    const d3 v1 = load3(t), v2 = load3(t + 3), v3 = load3(t + 6);
+    int bad = 0;
+    const d3 m12 = unit_rn(add3(v1, v2), &bad);
+    const d3 m23 = unit_rn(add3(v2, v3), &bad);
+    const d3 m31 = unit_rn(add3(v3, v1), &bad);
+    if (bad) atomicOr(flags, kFlagGeometry);
+    write_node(tri, center, radius, cramer, cb + 0, v1, m12, m31, flags);
+    write_node(tri, center, radius, cramer, cb + 1, m12, v2, m23, flags);
+    write_node(tri, center, radius, cramer, cb + 2, m31, m23, v3, flags);
+    write_node(tri, center, radius, cramer, cb + 3, m12, m23, m31, flags);
+    const int lv = level[id] + 1;
+    for (int q = 0; q < 4; ++q) {
+      level[cb + q] = lv;
+      parent[cb + q] = id;
+      child_base[cb + q] = -1;
+      created_call[cb + q] = call_index;
+    }
+    child_base[id] = cb;
+  }
+  if (nextc[k])
+    for (int q = 0; q < 4; ++q) cand_next[next_pos[k] + q] = cb + q;
 }
 
 // One level of distribute (face_tree.cpp:39-71) for every still-active particle.
@@ -170,9 +218,36 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[placed], __popc(peers));
 }
 
-__global__ void k_gather_counts(const int* __restrict__ ids, int m, const int* __restrict__ cnt, int* out) {
+// Depth-first bin offsets, top-down: roots in face order ...
+__global__ void k_root_offsets(const int* __restrict__ cnt, int* __restrict__ off) {
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int f = 0; f < 20; ++f) {
+      off[f] = run;
+      run += cnt[f];
+    }
+  }
+}
+
+// ... then each non-empty descending node hands out its range to its children.
+__global__ void k_child_offsets(const int* __restrict__ nodes, int m, const int* __restrict__ cnt,
+                                const int* __restrict__ child_base, const unsigned char* __restrict__ is_leaf,
+                                int* __restrict__ off) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < m) out[k] = cnt[ids[k]];
+  if (k >= m) return;
+  const int id = nodes[k];
+  if (cnt[id] == 0 || is_leaf[id]) return;
+  const int cb = child_base[id];
+  int o = off[id];
+  for (int q = 0; q < 4; ++q) {
+    off[cb + q] = o;
+    o += cnt[cb + q];
+  }
+}
+
+__global__ void k_leaf_keys(const int* __restrict__ leaves, int nl, const int* __restrict__ off, int* __restrict__ keys) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nl) keys[k] = off[leaves[k]];
 }
 
 __global__ void k_sort_keys(const int* __restrict__ leaf_of, int64_t n, const int* __restrict__ off,
@@ -189,8 +264,18 @@ __global__ void k_pos_leaf(const int* __restrict__ perm, int64_t n, const int* _
   if (k < n) pos_leaf[k] = leaf_of[perm[k]];
 }
 
+template <class T>
+void scan_excl(Ctx& c, const T* in, T* out, int n) {
+  size_t tmp = 0;
+  SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, c.stream));
+  c.cub_tmp.ensure(tmp);
+  SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, tmp, in, out, n, c.stream));
+  c.launches += 2;
+}
+
 }  // namespace
 
+// Node arrays (geometry persists; `need` nodes).
 static void grow_nodes(Ctx& c, int need) {
   NodeTable& t = c.nodes;
   t.tri.ensure(size_t(need) * 9, true, c.stream);
@@ -200,16 +285,18 @@ static void grow_nodes(Ctx& c, int need) {
   t.child_base.ensure(size_t(need), true, c.stream);
   t.level.ensure(size_t(need), true, c.stream);
   t.parent.ensure(size_t(need), true, c.stream);
+  t.created_call.ensure(size_t(need), true, c.stream);
   c.bins.cnt.ensure(size_t(need), true, c.stream);
   c.bins.act.ensure(size_t(need), true, c.stream);
+  c.bins.is_leaf.ensure(size_t(need), true, c.stream);
+  c.bins.off.ensure(size_t(need), true, c.stream);
 }
 
 // The 20 roots, built with the host libm so their vertices are bit-identical
 // to the reference's (IcosaMesh::base_icosahedron, icosa_mesh.cpp:10-35;
 // latlon_to_unit, geometry.cpp:41-44; FaceTree ctor, face_tree.cpp:9-16).
 void tree_init_roots(Ctx& c) {
-  HostTree& h = c.host;
-  h = HostTree{};
+  c.host = HostTree{};
   const double kPi = 3.14159265358979323846;  // M_PI
   int bad = 0;
   auto latlon = [&](double lat, double lon) {
@@ -254,31 +341,28 @@ void tree_init_roots(Ctx& c) {
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.center.p, center.data(), center.size() * 8, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.radius.p, radius.data(), radius.size() * 8, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.cramer.p, cramer.data(), cramer.size() * 8, cudaMemcpyHostToDevice, c.stream));
-  h.level.assign(20, 0);
-  h.parent.assign(20, -1);
-  h.child_base.assign(20, -1);
-  h.created_call.assign(20, 0);
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.level.p, h.level.data(), 80, cudaMemcpyHostToDevice, c.stream));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.parent.p, h.parent.data(), 80, cudaMemcpyHostToDevice, c.stream));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.child_base.p, h.child_base.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  const std::vector<int> zero(20, 0), minus(20, -1);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.level.p, zero.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.created_call.p, zero.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.parent.p, minus.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.child_base.p, minus.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  if (!c.bins.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&c.bins.h_small, 64 * sizeof(int)));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
-  HostTree& h = c.host;
   Binned& B = c.bins;
   c.call_index++;
+  c.host.valid = false;
   B.n = n;
-  B.frontier.clear();
-  B.leaves.clear();
-  B.max_level = 0;
+  B.n_leaves = 0;
+  B.level_span.clear();
   const int bs = 256;
 
-  // Fresh per-call counts; node geometry persists (face_tree.cpp:75).
-  SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p, 0, B.cnt.cap * sizeof(int), c.stream));
+  // Fresh per-call counts and leaf flags; node geometry persists (face_tree.cpp:75).
+  SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p, 0, size_t(c.nodes.count) * sizeof(int), c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(B.is_leaf.p, 0, size_t(c.nodes.count), c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, sizeof(int), c.stream));
-  h.cnt.assign(h.level.size(), 0);
-  h.off.assign(h.level.size(), 0);
   if (n == 0) return;
   B.cur.ensure(size_t(n));
   B.leaf_of.ensure(size_t(n));
@@ -290,127 +374,101 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   check_flags(c, "bin_particles: particle contained in no root face");
   trace().mark("bin.roots");
 
-  std::vector<int> cand(20);
-  for (int f = 0; f < 20; ++f) cand[f] = f;
-  std::vector<int> counts;
-  std::vector<int2> fa, splits;
-  while (!cand.empty()) {
-    const int m = static_cast<int>(cand.size());
-    B.d_ids.ensure(size_t(m));
-    B.d_cnt.ensure(size_t(m));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.d_ids.p, cand.data(), size_t(m) * 4, cudaMemcpyHostToDevice, c.stream));
-    k_gather_counts<<<grid_for(m, bs), bs, 0, c.stream>>>(B.d_ids.p, m, B.cnt.p, B.d_cnt.p);
+  // level 0 candidates: the 20 roots
+  int m = 20;
+  B.cand.ensure(1024);
+  B.levels.ensure(1024);
+  {
+    int roots[20];
+    for (int f = 0; f < 20; ++f) roots[f] = f;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.cand.p, roots, sizeof(roots), cudaMemcpyHostToDevice, c.stream));
+  }
+  int levels_used = 0;
+  while (m > 0) {
+    // node table room for every candidate splitting (4 m new nodes)
+    const int room = c.nodes.count + 4 * m;
+    if (room > static_cast<int>(c.nodes.child_base.cap)) grow_nodes(c, room);
+    SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p + c.nodes.count, 0, size_t(4) * m * sizeof(int), c.stream));
+    SSUM_CUDA_CHECK(cudaMemsetAsync(B.is_leaf.p + c.nodes.count, 0, size_t(4) * m, c.stream));
+    B.split.ensure(size_t(m) + 1);
+    B.split_pos.ensure(size_t(m) + 1);
+    B.nextc.ensure(size_t(m) + 1);
+    B.next_pos.ensure(size_t(m) + 1);
+    B.cand_next.ensure(size_t(4) * m);
+    // keep this level's candidates for the offset pass
+    B.levels.ensure(size_t(levels_used) + size_t(m), true, c.stream);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.levels.p + levels_used, B.cand.p, size_t(m) * 4, cudaMemcpyDeviceToDevice,
+                                    c.stream));
+    B.level_span.emplace_back(levels_used, m);
+    levels_used += m;
+
+    k_level_decide<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(B.cand.p, m, B.cnt.p, c.nodes.child_base.p,
+                                                              c.nodes.level.p, nt, max_depth, B.act.p, B.is_leaf.p,
+                                                              B.split.p, B.nextc.p);
     SSUM_LAUNCH_CHECK();
-    c.launches++;
-    counts.resize(size_t(m));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(counts.data(), B.d_cnt.p, size_t(m) * 4, cudaMemcpyDeviceToHost, c.stream));
-    check_flags(c, "bin_particles: degenerate child triangle");  // synchronises
-    trace().mark("bin.lvl_counts");
-
-    std::vector<int> front;
-    front.reserve(size_t(m));
-    fa.clear();
-    splits.clear();
-    for (int k = 0; k < m; ++k) {
-      const int id = cand[k];
-      h.cnt[id] = counts[k];
-      if (counts[k] == 0) continue;  // distribute returns on an empty bin (face_tree.cpp:40)
-      front.push_back(id);
-      int a = kActDescend;
-      if (h.child_base[id] < 0) {
-        if (counts[k] <= nt || h.level[id] >= max_depth) {
-          a = kActLeaf;  // face_tree.cpp:42-45
-        } else {
-          const int base = static_cast<int>(h.level.size());
-          h.child_base[id] = base;
-          for (int q = 0; q < 4; ++q) {
-            h.level.push_back(h.level[id] + 1);
-            h.parent.push_back(id);
-            h.child_base.push_back(-1);
-            h.created_call.push_back(c.call_index);
-            h.cnt.push_back(0);
-            h.off.push_back(0);
-          }
-          splits.push_back(int2{id, base});
-        }
-      }
-      if (a == kActLeaf) B.leaves.push_back(id);
-      fa.push_back(int2{id, a});
-    }
-    trace().mark("bin.lvl_host");
-    if (front.empty()) break;
-    B.frontier.push_back(std::move(front));
-
-    const int total = static_cast<int>(h.level.size());
-    if (total > c.nodes.count) {
-      const int first = c.nodes.count;
-      grow_nodes(c, total);
-      SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p + first, 0, size_t(total - first) * 4, c.stream));
-      c.nodes.count = total;
-    }
-    B.d_pairs.ensure(splits.size() + fa.size());
-    int2* d_splits = B.d_pairs.p;
-    int2* d_fa = B.d_pairs.p + splits.size();
-    if (!splits.empty()) {
-      SSUM_CUDA_CHECK(cudaMemcpyAsync(d_splits, splits.data(), splits.size() * sizeof(int2), cudaMemcpyHostToDevice, c.stream));
-      k_make_children<<<grid_for(int64_t(splits.size()), 128), 128, 0, c.stream>>>(
-          d_splits, static_cast<int>(splits.size()), c.nodes.tri.p, c.nodes.center.p, c.nodes.radius.p,
-          c.nodes.cramer.p, c.nodes.level.p, c.nodes.parent.p, c.nodes.child_base.p, c.d_flags.p);
-      SSUM_LAUNCH_CHECK();
-      c.launches++;
-    }
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(d_fa, fa.data(), fa.size() * sizeof(int2), cudaMemcpyHostToDevice, c.stream));
-    k_set_actions<<<grid_for(int64_t(fa.size()), bs), bs, 0, c.stream>>>(d_fa, static_cast<int>(fa.size()), B.act.p);
+    scan_excl(c, B.split.p, B.split_pos.p, m + 1);
+    scan_excl(c, B.nextc.p, B.next_pos.p, m + 1);
+    k_level_apply<<<grid_for(m, 128), 128, 0, c.stream>>>(
+        B.cand.p, m, B.split.p, B.split_pos.p, B.nextc.p, B.next_pos.p, c.nodes.count, c.call_index, c.nodes.tri.p,
+        c.nodes.center.p, c.nodes.radius.p, c.nodes.cramer.p, c.nodes.level.p, c.nodes.parent.p,
+        c.nodes.child_base.p, c.nodes.created_call.p, B.cand_next.p, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
     k_descend<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, B.cur.p, B.leaf_of.p, B.act.p, c.nodes.child_base.p,
                                                      c.nodes.tri.p, c.nodes.cramer.p, B.cnt.p);
     SSUM_LAUNCH_CHECK();
-    c.launches += 2;
-
-    trace().mark("bin.lvl_launch");
-    cand.clear();
-    for (const int2& p : fa)
-      if (p.y == kActDescend)
-        for (int q = 0; q < 4; ++q) cand.push_back(h.child_base[p.x] + q);
+    c.launches += 3;
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, B.split_pos.p + m, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, B.next_pos.p + m, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    trace().mark("bin.level");
+    c.nodes.count += 4 * B.h_small[0];
+    m = B.h_small[1];
+    std::swap(B.cand, B.cand_next);
   }
-  B.max_level = static_cast<int>(B.frontier.size()) - 1;
+  check_flags(c, "bin_particles: degenerate child triangle");
 
-  // Bin offsets in depth-first order (roots in face order, children in
-  // order) and the leaves in that order — one preorder walk over the
-  // non-empty nodes. Leaf tiles then cover the tree-order particle array
-  // left to right, which the target partition relies on.
+  // Depth-first bin offsets, top-down level by level.
+  k_root_offsets<<<1, 32, 0, c.stream>>>(B.cnt.p, B.off.p);
+  for (const auto& sp : B.level_span) {
+    k_child_offsets<<<grid_for(sp.second, bs), bs, 0, c.stream>>>(B.levels.p + sp.first, sp.second, B.cnt.p,
+                                                                  c.nodes.child_base.p, B.is_leaf.p, B.off.p);
+    SSUM_LAUNCH_CHECK();
+  }
+  c.launches += 1 + static_cast<int64_t>(B.level_span.size());
+
+  // Non-empty leaves in depth-first order: select, then sort by offset.
+  const int nn = c.nodes.count;
+  B.d_leaves.ensure(size_t(nn));
+  B.leaf_keys.ensure(size_t(nn) * 2);
+  B.sort_vals.ensure(std::max<size_t>(size_t(n), size_t(nn)));
   {
-    std::vector<char> is_leaf(h.level.size(), 0);
-    for (const int id : B.leaves) is_leaf[size_t(id)] = 1;
-    B.leaves.clear();
-    std::vector<int> stack;
-    stack.reserve(256);
-    for (int f = 19; f >= 0; --f) stack.push_back(f);
-    int run = 0;
-    while (!stack.empty()) {
-      const int id = stack.back();
-      stack.pop_back();
-      if (h.cnt[size_t(id)] == 0) continue;
-      h.off[size_t(id)] = run;
-      if (is_leaf[size_t(id)]) {
-        B.leaves.push_back(id);
-        run += h.cnt[size_t(id)];
-      } else {
-        const int cb = h.child_base[size_t(id)];
-        for (int q = 3; q >= 0; --q) stack.push_back(cb + q);
-      }
-    }
+    cub::CountingInputIterator<int> ids(0);
+    int* d_nsel = c.d_flags.p + 8;
+    size_t tmp = 0;
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tmp, ids, B.is_leaf.p, B.sort_vals.p, d_nsel, nn, c.stream));
+    c.cub_tmp.ensure(tmp);
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(c.cub_tmp.p, tmp, ids, B.is_leaf.p, B.sort_vals.p, d_nsel, nn,
+                                               c.stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, d_nsel, 4, cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    B.n_leaves = B.h_small[0];
+    const int nl = B.n_leaves;
+    k_leaf_keys<<<grid_for(std::max(nl, 1), bs), bs, 0, c.stream>>>(B.sort_vals.p, nl, B.off.p, B.leaf_keys.p);
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) < n) ++end_bit;
+    tmp = 0;
+    SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, B.leaf_keys.p, B.leaf_keys.p + nn, B.sort_vals.p,
+                                                    B.d_leaves.p, nl, 0, end_bit, c.stream));
+    c.cub_tmp.ensure(tmp);
+    SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, tmp, B.leaf_keys.p, B.leaf_keys.p + nn,
+                                                    B.sort_vals.p, B.d_leaves.p, nl, 0, end_bit, c.stream));
+    c.launches += 7;
   }
-  B.off.ensure(size_t(c.nodes.count));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.off.p, h.off.data(), size_t(c.nodes.count) * 4, cudaMemcpyHostToDevice, c.stream));
-  B.d_leaves.ensure(std::max<size_t>(B.leaves.size(), 1));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.d_leaves.p, B.leaves.data(), B.leaves.size() * 4, cudaMemcpyHostToDevice, c.stream));
+  trace().mark("bin.offsets_leaves");
 
   // Permutation: stable sort of particle ids by their leaf's offset.
-  trace().mark("bin.offsets");
   B.sort_keys.ensure(size_t(n));
   B.sort_keys2.ensure(size_t(n));
-  B.sort_vals.ensure(size_t(n));
   B.perm.ensure(size_t(n));
   B.pos_leaf.ensure(size_t(n));
   k_sort_keys<<<grid_for(n, bs), bs, 0, c.stream>>>(B.leaf_of.p, n, B.off.p, B.sort_keys.p, B.sort_vals.p);
@@ -428,6 +486,30 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   k_pos_leaf<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, B.leaf_of.p, B.pos_leaf.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
+}
+
+// Host snapshot of the node structure and this call's counts/offsets.
+const HostTree& host_tree(Ctx& c) {
+  HostTree& h = c.host;
+  if (h.valid) return h;
+  const size_t nn = size_t(c.nodes.count);
+  h.level.resize(nn);
+  h.parent.resize(nn);
+  h.child_base.resize(nn);
+  h.created_call.resize(nn);
+  h.cnt.resize(nn);
+  h.off.resize(nn);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.level.data(), c.nodes.level.p, nn * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.parent.data(), c.nodes.parent.p, nn * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.child_base.data(), c.nodes.child_base.p, nn * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.created_call.data(), c.nodes.created_call.p, nn * 4, cudaMemcpyDeviceToHost,
+                                  c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.cnt.data(), c.bins.cnt.p, nn * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.off.data(), c.bins.off.p, nn * 4, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (c.bins.n == 0) std::fill(h.cnt.begin(), h.cnt.end(), 0);
+  h.valid = true;
+  return h;
 }
 
 }  // namespace ssum
