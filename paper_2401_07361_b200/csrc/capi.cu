@@ -94,6 +94,7 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
   tr.mark("lists.done");
   const auto t2 = clk::now();
   evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
+  finalize_counts(c);
   tr.mark("eval.done");
   const auto t3 = clk::now();
   if (tr.on) {  // per label: total ms (count)
@@ -296,6 +297,7 @@ void ssum_destroy(ssum_ctx* h) {
   c->rk_state.release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
+  if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }

@@ -159,6 +159,7 @@ struct Lists {
   int n_fit_sel = 0;
   bool fit_sel_all = true;
   uint64_t local_evals[4] = {0, 0, 0, 0};
+  bool counts_pending = false;   // counts/evals still in flight (finalize_counts)
 };
 
 // Breadth-first traversal frontier entry: node pair plus depth-first order key.
@@ -175,8 +176,9 @@ struct TravScratch {
   DBuf<int> gkey, gkey2, gval, sorted_e;
   DBuf<int2> seg;
   DBuf<int> flag, flag_scan, slot_node;
-  DBuf<int> nr, nt, nr_off, nt_off;
+  DBuf<int> nr, nt, nr_off, nt_off, fnr, fnr_off;
   DBuf<unsigned long long> counters;  // [0..3] kinds, [4..7] kernel evals
+  unsigned long long* h_small = nullptr;  // pinned: [0..7] scratch, [8..15] counters read-back
 };
 
 struct Ctx {
@@ -237,6 +239,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
 void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
 void partition_targets(Ctx& c);
 void build_lists(Ctx& c, const ssum_config& cfg);
+void finalize_counts(Ctx& c);
 std::vector<int> reference_ids(const HostTree& h);
 const HostTree& host_tree(Ctx& c);  // downloads the node structure when stale
 void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,

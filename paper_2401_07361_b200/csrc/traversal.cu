@@ -54,7 +54,11 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
                             int thr, int max_depth, int pc_only, int* __restrict__ action,
                             unsigned long long* __restrict__ packed) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m) return;
+  if (k > m) return;
+  if (k == m) {  // sentinel: the exclusive scan's entry m is the total
+    packed[k] = 0;
+    return;
+  }
   const int t = F[k].t, s = F[k].s;
   const int ct = cnt[t], cs = cnt[s];
   int a = 0;
@@ -379,22 +383,21 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
   long long ne = 0;
   L.inter.ensure(1 << 16);
   L.key.ensure(1 << 16);
+  if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
   while (m > 0) {
-    S.action.ensure(size_t(m));
-    S.packed.ensure(size_t(m));
-    S.scan.ensure(size_t(m));
-    k_trav_eval<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
-                                                       c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
-                                                       cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
-                                                       S.packed.p);
+    S.action.ensure(size_t(m) + 1);
+    S.packed.ensure(size_t(m) + 1);
+    S.scan.ensure(size_t(m) + 1);
+    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
+                                                           c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
+                                                           cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
+                                                           S.packed.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
-    exclusive_scan(c, S.packed.p, S.scan.p, m);
-    unsigned long long tail[2];
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[0], S.scan.p + (m - 1), 8, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tail[1], S.packed.p + (m - 1), 8, cudaMemcpyDeviceToHost, c.stream));
+    exclusive_scan(c, S.packed.p, S.scan.p, m + 1);  // packed[m] = 0: totals at scan[m]
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_small, S.scan.p + m, 8, cudaMemcpyDeviceToHost, c.stream));
     SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    const unsigned long long tot = tail[0] + tail[1];
+    const unsigned long long tot = S.h_small[0];
     const int next = static_cast<int>(tot & 0xffffffffull);
     const long long emitted = static_cast<long long>(tot >> 32);
     L.inter.ensure(size_t(ne + emitted), true, c.stream);
@@ -504,27 +507,41 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   }
 
   trace().mark("lists.group_slots");
-  // ---- leaf tiles
+  // ---- range and tile counts for leaves and fit nodes, one read-back
   const int nl = B.n_leaves;
+  const int nf = L.n_fit;
   S.nr.ensure(size_t(nl) + 1);
   S.nt.ensure(size_t(nl) + 1);
   S.nr_off.ensure(size_t(nl) + 1);
   S.nt_off.ensure(size_t(nl) + 1);
+  S.fnr.ensure(size_t(nf) + 1);
+  S.fnr_off.ensure(size_t(nf) + 1);
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.nr.p + nl, 0, 4, c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.nt.p + nl, 0, 4, c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.fnr.p + nf, 0, 4, c.stream));
   k_leaf_count<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, B.cnt.p, S.nr.p,
                                                          S.nt.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   exclusive_scan(c, S.nr.p, S.nr_off.p, nl + 1);
   exclusive_scan(c, S.nt.p, S.nt_off.p, nl + 1);
+  if (nf > 0) {
+    k_fit_count<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.fnr.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    exclusive_scan(c, S.fnr.p, S.fnr_off.p, nf + 1);
+  }
+  if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
   {
-    int tot[2];
+    int* tot = reinterpret_cast<int*>(S.h_small);
     SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot[0], S.nr_off.p + nl, 4, cudaMemcpyDeviceToHost, c.stream));
     SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot[1], S.nt_off.p + nl, 4, cudaMemcpyDeviceToHost, c.stream));
+    tot[2] = 0;
+    if (nf > 0) SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot[2], S.fnr_off.p + nf, 4, cudaMemcpyDeviceToHost, c.stream));
     SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     L.n_leaf_ranges = tot[0];
     L.n_leaf_tiles = tot[1];
+    L.n_fit_ranges = tot[2];
   }
   L.leaf_ranges.ensure(size_t(std::max<int64_t>(L.n_leaf_ranges, 1)));
   L.leaf_tiles.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
@@ -537,40 +554,40 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   SSUM_LAUNCH_CHECK();
   c.launches++;
 
-  trace().mark("lists.leaf_tiles");
   // ---- fit tiles
-  const int nf = L.n_fit;
   if (nf > 0) {
-    S.nr.ensure(size_t(nf) + 1);
-    S.nr_off.ensure(size_t(nf) + 1);
-    SSUM_CUDA_CHECK(cudaMemsetAsync(S.nr.p + nf, 0, 4, c.stream));
-    k_fit_count<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.nr.p);
-    SSUM_LAUNCH_CHECK();
-    c.launches++;
-    exclusive_scan(c, S.nr.p, S.nr_off.p, nf + 1);
-    int tot = 0;
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(&tot, S.nr_off.p + nf, 4, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    L.n_fit_ranges = tot;
-    L.fit_ranges.ensure(size_t(std::max(tot, 1)));
+    L.fit_ranges.ensure(size_t(std::max<int64_t>(L.n_fit_ranges, 1)));
     L.fit_tiles.ensure(size_t(nf));
     L.fit_cost.ensure(size_t(nf));
     k_fit_fill<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.sorted_e.p, L.inter.p, B.cnt.p,
-                                                         B.off.p, L.pslot.p, S.nr_off.p, N, P, L.fit_ranges.p,
+                                                         B.off.p, L.pslot.p, S.fnr_off.p, N, P, L.fit_ranges.p,
                                                          L.fit_tiles.p, L.fit_cost.p, S.counters.p + 4);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
   L.n_fit_tiles = nf;
-  unsigned long long h[8];
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, S.counters.p, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  // interaction / evaluation counts: read back with the evaluation's final sync
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_small + 8, S.counters.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                  c.stream));
+  L.counts_pending = true;
+  trace().mark("lists.tiles");
+  partition_targets(c);
+}
+
+// L.counts / L.evals from the pinned read-back queued by build_lists (valid
+// once the stream has been synchronised).
+void finalize_counts(Ctx& c) {
+  Lists& L = c.lists;
+  if (!L.counts_pending) return;
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  const unsigned long long* h = c.trav.h_small + 8;
   for (int k = 0; k < 4; ++k) {
     L.counts[k] = h[k];
     L.evals[k] = h[4 + k];
   }
-  trace().mark("lists.fit_tiles");
-  partition_targets(c);
+  if (c.nparts <= 1)
+    for (int k = 0; k < 4; ++k) L.local_evals[k] = L.evals[k];
+  L.counts_pending = false;
 }
 
 // Multi-GPU target partition: leaf tiles are in depth-first
