@@ -121,7 +121,9 @@ struct Tile {
   int tgt_count;  // 1 .. kTileTargets
   int list_begin, list_end;  // into the range list
   int near_total;            // sources in the leading near-possible ranges
-  int pad0, pad1, pad2;
+  int self_shift;  // self source of target i at flattened list position i + self_shift
+  int has_self;    // 0: no range holds the targets themselves
+  int pad;
 };
 // Arc-length margin below which a (target leaf, source node) pair may hold a
 // near pair: den = 2 sin^2(arc/2) < 2^-20 <=> arc < 1.3811e-3 rad.

@@ -68,20 +68,6 @@ struct Acc {
   }
 };
 
-// Well-separated pair (PC, CP, CC, and PP pairs past the near threshold).
-template <int KER>
-__device__ __forceinline__ void pair_far(double x0, double x1, double x2, const double4& y, Acc<KER>& a) {
-  const double den = fma(-x2, y.z, fma(-x1, y.y, fma(-x0, y.x, 1.0)));
-  if constexpr (KER == kBS) {
-    const double r = q_over(y.w, den);
-    a.s[0] = fma(r, y.x, a.s[0]);
-    a.s[1] = fma(r, y.y, a.s[1]);
-    a.s[2] = fma(r, y.z, a.s[2]);
-  } else {
-    a.s[0] = fma(y.w, log(den), a.s[0]);
-  }
-}
-
 // The reference-rounded slow path of one pair whose
 // fast denominator fell below the near threshold, or a self pair. Returns the
 // pair's contribution r (y - x) (BS) or q log(den) (log); zero when skipped.
@@ -98,63 +84,14 @@ __device__ __forceinline__ void pair_slow(double x0, double x1, double x2, const
     return;
   }
   if constexpr (KER == kBS) {
-    const double r = __ddiv_rn(y.w, den);
+    // the exact denominator is what matters here; q / den itself only needs
+    // ~1 ulp (q_over: no division subroutine call, so no spills around it)
+    const double r = q_over(y.w, den);
     c[0] = r * __dsub_rn(y.x, x0);
     c[1] = r * __dsub_rn(y.y, x1);
     c[2] = r * __dsub_rn(y.z, x2);
   } else {
     c[0] = y.w * log(den);
-  }
-}
-
-// Four independent sources per step (y[q] = B[k + q*G]): four separate
-// dependency chains with no branch between them, so the scheduler can
-// interleave them. NEAR adds one warp vote per quad; a quad with any near
-// lane replays its four pairs through the exact per-pair path.
-template <int KER, bool NEAR>
-__device__ __forceinline__ void pair_quad(double x0, double x1, double x2, const double4* __restrict__ B,
-                                          const int* __restrict__ J, int k, int G, int i, Acc<KER>& a, int* flags) {
-  double4 y[4];
-  double den[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    y[q] = B[k + q * G];
-    den[q] = fma(-x2, y[q].z, fma(-x1, y[q].y, fma(-x0, y[q].x, 1.0)));
-  }
-  if constexpr (NEAR) {
-    bool nr = false;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) nr |= __double2hiint(den[q]) < kNearHi;
-    if (__any_sync(0xffffffffu, nr)) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double c[KDim<KER>::D];
-        if (__double2hiint(den[q]) < kNearHi) {
-          pair_slow<KER>(x0, x1, x2, y[q], i, J[k + q * G], c, flags);
-        } else if constexpr (KER == kBS) {
-          const double r = q_over(y[q].w, den[q]);
-          c[0] = r * y[q].x;
-          c[1] = r * y[q].y;
-          c[2] = r * y[q].z;
-        } else {
-          c[0] = y[q].w * log(den[q]);
-        }
-#pragma unroll
-        for (int d = 0; d < KDim<KER>::D; ++d) a.s[d] += c[d];
-      }
-      return;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if constexpr (KER == kBS) {
-      const double r = q_over(y[q].w, den[q]);
-      a.s[0] = fma(r, y[q].x, a.s[0]);
-      a.s[1] = fma(r, y[q].y, a.s[1]);
-      a.s[2] = fma(r, y[q].z, a.s[2]);
-    } else {
-      a.s[0] = fma(y[q].w, log(den[q]), a.s[0]);
-    }
   }
 }
 
@@ -164,13 +101,14 @@ __device__ __forceinline__ void pair_quad(double x0, double x1, double x2, const
 // consecutive instructions belong to different chains and the in-order
 // issue never waits on a DFMA (8.8 cycles) or MUFU.RCP64H (~24 cycles)
 // result it just produced.
-// NEAR: the block may hold near pairs (self pairs, 1 - x.y < 2^-20): one warp
-// vote for the whole block; a block with a near lane replays its pairs
-// through the per-pair exact path (ti: target indices, J: source indices).
+// NEAR: the block may hold near pairs (self pairs, 1 - x.y < 2^-20). They
+// are masked out of the sums (their NaN/inf reciprocals never reach them)
+// and counted per lane in *ncnt, with no branch and no vote: the caller
+// compares the count with the self pairs the lane must have met and
+// re-walks the chunk through near_repair only when they differ.
 template <int KER, int NT, int NS, bool NEAR = false>
 __device__ __forceinline__ void far_block(const double4* x, const double4* __restrict__ B, int k, int G, Acc<KER>* a,
-                                          const int* ti = nullptr, const int* __restrict__ J = nullptr,
-                                          int* flags = nullptr) {
+                                          int* ncnt = nullptr) {
   constexpr int C = NT * NS;
   double4 y[NS];
 #pragma unroll
@@ -182,29 +120,12 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
   for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].y, y[c / NT].y, den[c]);
 #pragma unroll
   for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].z, y[c / NT].z, den[c]);
+  bool nr[NEAR ? C : 1];
   if constexpr (NEAR) {
-    bool nr = false;
 #pragma unroll
-    for (int c = 0; c < C; ++c) nr |= __double2hiint(den[c]) < kNearHi;
-    if (__any_sync(0xffffffffu, nr)) {
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        double v[KDim<KER>::D];
-        const double4& yy = y[c / NT];
-        if (__double2hiint(den[c]) < kNearHi) {
-          pair_slow<KER>(x[c % NT].x, x[c % NT].y, x[c % NT].z, yy, ti[c % NT], J[k + (c / NT) * G], v, flags);
-        } else if constexpr (KER == kBS) {
-          const double r = q_over(yy.w, den[c]);
-          v[0] = r * yy.x;
-          v[1] = r * yy.y;
-          v[2] = r * yy.z;
-        } else {
-          v[0] = yy.w * log(den[c]);
-        }
-#pragma unroll
-        for (int d = 0; d < KDim<KER>::D; ++d) a[c % NT].s[d] += v[d];
-      }
-      return;
+    for (int c = 0; c < C; ++c) {
+      nr[c] = __double2hiint(den[c]) < kNearHi;
+      *ncnt += nr[c] ? 1 : 0;
     }
   }
   if constexpr (KER == kBS) {
@@ -219,6 +140,10 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
     for (int c = 0; c < C; ++c) r[c] = y[c / NT].w * r[c];
 #pragma unroll
     for (int c = 0; c < C; ++c) r[c] = fma(r[c], e[c], r[c]);
+    if constexpr (NEAR) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) r[c] = nr[c] ? 0.0 : r[c];
+    }
 #pragma unroll
     for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(r[c], y[c / NT].x, a[c % NT].s[0]);
 #pragma unroll
@@ -227,88 +152,47 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
     for (int c = 0; c < C; ++c) a[c % NT].s[2] = fma(r[c], y[c / NT].z, a[c % NT].s[2]);
   } else {
 #pragma unroll
-    for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(y[c / NT].w, log(den[c]), a[c % NT].s[0]);
+    for (int c = 0; c < C; ++c) {
+      double l = log(den[c]);
+      if constexpr (NEAR) l = nr[c] ? 0.0 : l;
+      a[c % NT].s[0] = fma(y[c / NT].w, l, a[c % NT].s[0]);
+    }
   }
 }
 
-// One source against NT register-tiled targets with a single warp vote: the
-// NT denominator chains are independent, so they interleave; only a source
-// with a near lane (self pair or 1 - x.y < 2^-20) takes the exact path.
-template <int KER, int NT>
-__device__ __forceinline__ void source_near(const double4* x, const double4& y, const int* ti, int j, Acc<KER>* a,
+// Second walk over one far_block<..., true> block whose warp saw a near pair
+// other than its self pairs: adds the reference-rounded contribution of each
+// near pair of distinct points (pair_slow, which also raises the singular
+// flag), and takes back the fast term of a self pair that was not near (only
+// possible for input points off the unit sphere).
+template <int KER, int NT, int NS>
+__device__ __forceinline__ void near_repair(const double4* x, const double4* __restrict__ B,
+                                            const int* __restrict__ J, int k, int G, Acc<KER>* a, const int* ti,
                                             int* flags) {
-  double den[NT];
-  bool nr = false;
 #pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    den[q] = fma(-x[q].z, y.z, fma(-x[q].y, y.y, fma(-x[q].x, y.x, 1.0)));
-    nr |= __double2hiint(den[q]) < kNearHi;
-  }
-  if (__any_sync(0xffffffffu, nr)) {
-#pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      double c[KDim<KER>::D];
-      if (__double2hiint(den[q]) < kNearHi) {
-        pair_slow<KER>(x[q].x, x[q].y, x[q].z, y, ti[q], j, c, flags);
-      } else if constexpr (KER == kBS) {
-        const double r = q_over(y.w, den[q]);
-        c[0] = r * y.x;
-        c[1] = r * y.y;
-        c[2] = r * y.z;
+  for (int c = 0; c < NT * NS; ++c) {
+    const double4 y = B[k + (c / NT) * G];
+    const int j = J[k + (c / NT) * G];
+    const double4& xx = x[c % NT];
+    const double den = fma(-xx.z, y.z, fma(-xx.y, y.y, fma(-xx.x, y.x, 1.0)));
+    const bool nr = __double2hiint(den) < kNearHi;
+    double v[KDim<KER>::D];
+    if (nr && ti[c % NT] != j) {
+      pair_slow<KER>(xx.x, xx.y, xx.z, y, ti[c % NT], j, v, flags);
+    } else if (!nr && ti[c % NT] == j) {
+      if constexpr (KER == kBS) {
+        const double r = -q_over(y.w, den);
+        v[0] = r * y.x;
+        v[1] = r * y.y;
+        v[2] = r * y.z;
       } else {
-        c[0] = y.w * log(den[q]);
+        v[0] = -y.w * log(den);
       }
-#pragma unroll
-      for (int d = 0; d < KDim<KER>::D; ++d) a[q].s[d] += c[d];
-    }
-    return;
-  }
-#pragma unroll
-  for (int q = 0; q < NT; ++q) {
-    if constexpr (KER == kBS) {
-      const double r = q_over(y.w, den[q]);
-      a[q].s[0] = fma(r, y.x, a[q].s[0]);
-      a[q].s[1] = fma(r, y.y, a[q].s[1]);
-      a[q].s[2] = fma(r, y.z, a[q].s[2]);
     } else {
-      a[q].s[0] = fma(y.w, log(den[q]), a[q].s[0]);
-    }
-  }
-}
-
-// Possibly-near pair of a PP range: i is the target's index, j the source's
-// index in the unified point array. The near test is a warp vote, so the
-// common case (no lane near) is the straight-line fast path with no
-// divergence; a warp with a near lane (a self pair of the own leaf, or
-// genuinely close points) runs the exact path for those lanes only.
-template <int KER>
-__device__ __forceinline__ void pair_near(double x0, double x1, double x2, const double4& y, int i, int j,
-                                          Acc<KER>& a, int* flags) {
-  const double den_f = fma(-x2, y.z, fma(-x1, y.y, fma(-x0, y.x, 1.0)));
-  const bool nearp = __double2hiint(den_f) < kNearHi;
-  if (__any_sync(0xffffffffu, nearp)) {
-    double c[KDim<KER>::D];
-    if (nearp) {
-      pair_slow<KER>(x0, x1, x2, y, i, j, c, flags);
-    } else if constexpr (KER == kBS) {
-      const double r = q_over(y.w, den_f);
-      c[0] = r * y.x;
-      c[1] = r * y.y;
-      c[2] = r * y.z;
-    } else {
-      c[0] = y.w * log(den_f);
+      continue;
     }
 #pragma unroll
-    for (int d = 0; d < KDim<KER>::D; ++d) a.s[d] += c[d];
-    return;
-  }
-  if constexpr (KER == kBS) {
-    const double r = q_over(y.w, den_f);
-    a.s[0] = fma(r, y.x, a.s[0]);
-    a.s[1] = fma(r, y.y, a.s[1]);
-    a.s[2] = fma(r, y.z, a.s[2]);
-  } else {
-    a.s[0] = fma(y.w, log(den_f), a.s[0]);
+    for (int d = 0; d < KDim<KER>::D; ++d) a[c % NT].s[d] += v[d];
   }
 }
 

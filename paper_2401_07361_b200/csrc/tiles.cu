@@ -149,19 +149,40 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     const double4* B = buf[c & 1];
     const int* J = sid[c & 1];
     const int iters = (n + G - 1) / G;
-    if (MODE == kLeafMode && c * kChunk < T.near_total) {
-      // chunk holds near-possible sources: the same staged blocks, one warp
-      // vote per block, exact per-pair path only for blocks with a near lane
-      const int steps = (iters + kNs - 1) / kNs;
-#pragma unroll 1
-      for (int it = 0; it < steps; ++it) far_block<KER, kTpt, kNs, true>(x, B, g + it * kNs * G, G, a, ti, J, flags);
-    } else {
-      // well-separated sources only: branch-free, kNs sources x kTpt targets
-      // of independent chains per step (zero-padded tail contributes 0)
-      const int steps = (iters + kNs - 1) / kNs;
-#pragma unroll 2
-      for (int it = 0; it < steps; ++it) far_block<KER, kTpt, kNs>(x, B, g + it * kNs * G, G, a);
+    const int steps = (iters + kNs - 1) / kNs;
+    // steps covering the chunk's near-possible prefix [0, near_total - c kChunk):
+    // the same staged blocks plus self-pair masking and one warp vote per
+    // block (exact per-pair path only for a block with a near lane)
+    int near_steps = 0;
+    if (MODE == kLeafMode) {
+      const int nn = min(n, T.near_total - c * kChunk);
+      near_steps = nn > 0 ? (nn + kNs * G - 1) / (kNs * G) : 0;
     }
+#ifdef SSUM_TIMING_NO_NEAR  // timing experiment only: wrong results for near/self pairs
+    near_steps = 0;
+#endif
+    int it = 0;
+    if (near_steps > 0) {
+      int ncnt = 0;
+#pragma unroll 2
+      for (; it < near_steps; ++it) far_block<KER, kTpt, kNs, true>(x, B, g + it * kNs * G, G, a, &ncnt);
+      // self pairs this lane walked in this chunk's near steps: the self
+      // source of target ti sits at flattened position ti + T.self_shift
+      const int o_end = min(n, near_steps * kNs * G);
+      int nself = 0;
+#pragma unroll
+      for (int q = 0; q < kTpt; ++q) {
+        const int o = ti[q] + T.self_shift - c * kChunk;
+        nself += (T.has_self && o >= 0 && o < o_end && o % G == g) ? 1 : 0;
+      }
+      if (__any_sync(0xffffffffu, ncnt != nself))
+#pragma unroll 1
+        for (int r = 0; r < near_steps; ++r) near_repair<KER, kTpt, kNs>(x, B, J, g + r * kNs * G, G, a, ti, flags);
+    }
+    // well-separated sources only: branch-free, kNs sources x kTpt targets
+    // of independent chains per step (zero-padded tail contributes 0)
+#pragma unroll 2
+    for (; it < steps; ++it) far_block<KER, kTpt, kNs>(x, B, g + it * kNs * G, G, a);
     if (more)
 #pragma unroll
       for (int e = 0; e < kPer; ++e) {
@@ -240,8 +261,9 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
   if (t == 0) *range = SrcRange{0, static_cast<int>(n), 1, 0};
   if (t >= nt) return;
   const int64_t rem = n - t * kTileThreads;
+  // one range [0, n): the self source of target i sits at flattened position i
   tiles[t] = Tile{static_cast<int>(t * kTileThreads), static_cast<int>(rem < kTileThreads ? rem : kTileThreads), 0, 1,
-                  static_cast<int>(n), 0, 0, 0};
+                  static_cast<int>(n), 0, 1, 0};
 }
 
 }  // namespace

@@ -234,6 +234,7 @@ __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* _
     const int w0 = w;
     unsigned long long src_pp = 0, src_pc = 0;
     int near_total = 0;
+    int self_shift = 0, has_self = 0;  // self source of particle i at flattened position i + self_shift
     for (int pass = 0; pass < 2; ++pass) {  // 0: near-possible PP ranges, 1: the rest
       for (int q = pl - 1; q >= 0; --q) {   // root to leaf (treecode.cpp:379,392)
         const int2 sg = seg[2 * path[q]];
@@ -247,6 +248,10 @@ __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* _
             r.begin = off[it.y];
             r.count = cnt[it.y];
             r.near = nr ? 1 : 0;
+            if (r.begin <= off[leaf] && off[leaf] < r.begin + r.count) {  // holds the leaf's own particles
+              self_shift = r.pad - r.begin;
+              has_self = 1;
+            }
             src_pp += static_cast<unsigned long long>(r.count);
           } else {
             r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
@@ -268,7 +273,9 @@ __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* _
       t.list_begin = w0;
       t.list_end = w;
       t.near_total = near_total;
-      t.pad0 = t.pad1 = t.pad2 = 0;
+      t.self_shift = self_shift;
+      t.has_self = has_self;
+      t.pad = 0;
       tiles[tile_off[k] + j] = t;
       const unsigned long long tc = static_cast<unsigned long long>(t.tgt_count);
       tile_cost[tile_off[k] + j] = make_ulonglong2(tc * src_pp - tc, tc * src_pc);  // self pairs excluded
@@ -331,7 +338,7 @@ __global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2
     tl.list_begin = w0;
     tl.list_end = w;
     tl.near_total = 0;  // CP / CC pairs are well separated
-    tl.pad0 = tl.pad1 = tl.pad2 = 0;
+    tl.self_shift = tl.has_self = tl.pad = 0;
     tiles[k] = tl;
     tile_cost[k] = make_ulonglong2(cp, cc);
   }
