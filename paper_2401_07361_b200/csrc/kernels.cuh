@@ -95,6 +95,18 @@ __device__ __forceinline__ void pair_slow(double x0, double x1, double x2, const
   }
 }
 
+// Near-segment mask of one pair's term v: when den < 2^-20 (a self pair, or a
+// near pair left to near_repair) the high word of v is cleared — what is
+// left is at most 2^-1022 in magnitude, never NaN or inf — and the lane's
+// near count is bumped; one compare, two predicated moves/adds.
+__device__ __forceinline__ double near_mask(double v, double den, int& cnt) {
+  int hi = __double2hiint(v);
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %2, %3;\n\t@p add.s32 %0, %0, 1;\n\t@p mov.b32 %1, 0;\n\t}"
+      : "+r"(cnt), "+r"(hi)
+      : "r"(__double2hiint(den)), "n"(kNearHi));
+  return __hiloint2double(hi, __double2loint(v));
+}
+
 // NS sources x NT targets of well-separated pairs, written stage by stage
 // across the NS*NT independent chains (all denominators, then all
 // reciprocal seeds, then each Newton step, then the accumulations) so that
@@ -107,12 +119,12 @@ __device__ __forceinline__ void pair_slow(double x0, double x1, double x2, const
 // compares the count with the self pairs the lane must have met and
 // re-walks the chunk through near_repair only when they differ.
 template <int KER, int NT, int NS, bool NEAR = false>
-__device__ __forceinline__ void far_block(const double4* x, const double4* __restrict__ B, int k, int G, Acc<KER>* a,
+__device__ __forceinline__ void far_block(const double4* x, const double4* __restrict__ B, int G, Acc<KER>* a,
                                           int* ncnt = nullptr) {
   constexpr int C = NT * NS;
   double4 y[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) y[s] = B[k + s * G];
+  for (int s = 0; s < NS; ++s) y[s] = B[s * G];
   double den[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].x, y[c / NT].x, 1.0);
@@ -120,14 +132,6 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
   for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].y, y[c / NT].y, den[c]);
 #pragma unroll
   for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].z, y[c / NT].z, den[c]);
-  bool nr[NEAR ? C : 1];
-  if constexpr (NEAR) {
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      nr[c] = __double2hiint(den[c]) < kNearHi;
-      *ncnt += nr[c] ? 1 : 0;
-    }
-  }
   if constexpr (KER == kBS) {
     double r[C], e[C];
 #pragma unroll
@@ -142,7 +146,7 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
     for (int c = 0; c < C; ++c) r[c] = fma(r[c], e[c], r[c]);
     if constexpr (NEAR) {
 #pragma unroll
-      for (int c = 0; c < C; ++c) r[c] = nr[c] ? 0.0 : r[c];
+      for (int c = 0; c < C; ++c) r[c] = near_mask(r[c], den[c], *ncnt);
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(r[c], y[c / NT].x, a[c % NT].s[0]);
@@ -154,7 +158,7 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       double l = log(den[c]);
-      if constexpr (NEAR) l = nr[c] ? 0.0 : l;
+      if constexpr (NEAR) l = near_mask(l, den[c], *ncnt);
       a[c % NT].s[0] = fma(y[c / NT].w, l, a[c % NT].s[0]);
     }
   }
@@ -167,12 +171,12 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
 // possible for input points off the unit sphere).
 template <int KER, int NT, int NS>
 __device__ __forceinline__ void near_repair(const double4* x, const double4* __restrict__ B,
-                                            const int* __restrict__ J, int k, int G, Acc<KER>* a, const int* ti,
+                                            const int* __restrict__ J, int G, Acc<KER>* a, const int* ti,
                                             int* flags) {
 #pragma unroll
   for (int c = 0; c < NT * NS; ++c) {
-    const double4 y = B[k + (c / NT) * G];
-    const int j = J[k + (c / NT) * G];
+    const double4 y = B[(c / NT) * G];
+    const int j = J[(c / NT) * G];
     const double4& xx = x[c % NT];
     const double den = fma(-xx.z, y.z, fma(-xx.y, y.y, fma(-xx.x, y.x, 1.0)));
     const bool nr = __double2hiint(den) < kNearHi;

@@ -57,9 +57,12 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
             const double* __restrict__ vinv, int P, double* __restrict__ coeff) {
   constexpr int D = KDim<KER>::D;
-  __shared__ double4 buf[2][kChunk + kPad];
-  __shared__ int sid[2][kChunk + kPad];
-  __shared__ int2 rtab[kRangeCap];  // (begin, prefix) of the tile's ranges
+  // dynamic shared memory (kTileSmem bytes): two source stages, their
+  // indices, and the range table
+  extern __shared__ __align__(16) unsigned char smem[];
+  auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
+  auto sid = reinterpret_cast<int(*)[kChunk + kPad]>(smem + 2 * sizeof(double4) * (kChunk + kPad));
+  int2* rtab = reinterpret_cast<int2*>(smem + 2 * (sizeof(double4) + sizeof(int)) * (kChunk + kPad));
   static_assert(sizeof(double) * kTileThreads * D * kTpt <= 2 * sizeof(double4) * (kChunk + kPad), "red alias");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
@@ -94,69 +97,81 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
       rtab[r] = make_int2(R.begin, R.pad);
     }
   __syncthreads();
-  // flattened position f -> source index: binary search over range prefixes
-  auto fetch = [&](int f, double4& v, int& j) {
-    if (f < total) {
-      int lo = 0, hi = nr - 1, b, p;
-      if (in_smem) {
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (rtab[mid].y <= f)
-            lo = mid;
-          else
-            hi = mid - 1;
-        }
-        b = rtab[lo].x;
-        p = rtab[lo].y;
-      } else {
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (ranges[T.list_begin + mid].pad <= f)
-            lo = mid;
-          else
-            hi = mid - 1;
-        }
-        b = ranges[T.list_begin + lo].begin;
-        p = ranges[T.list_begin + lo].pad;
+  // flattened position -> source index: binary search over the range
+  // prefixes. Thread tid fetches positions e * 256 + tid of each chunk
+  // (coalesced loads and shared stores; one search each — measured faster
+  // than consecutive positions with one search per thread).
+  constexpr int kPer = kChunk / kTileThreads;  // sources fetched per thread per chunk
+  auto slot = [](int e, int t) { return e * kTileThreads + t; };
+  auto rbegin = [&](int r) { return in_smem ? rtab[r].x : ranges[T.list_begin + r].begin; };
+  auto rpad = [&](int r) { return in_smem ? rtab[r].y : ranges[T.list_begin + r].pad; };
+  auto locate = [&](int f) {
+    int lo = 0, hi = nr - 1;
+    if (in_smem) {
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (rtab[mid].y <= f)
+          lo = mid;
+        else
+          hi = mid - 1;
       }
-      j = b + (f - p);
-      v = pts[j];
     } else {
-      v = zero4;
-      j = -1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ranges[T.list_begin + mid].pad <= f)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+    }
+    return lo;
+  };
+  auto fetch = [&](int c0, double4* v, int* j) {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int f = c0 + e * kTileThreads + tid;
+      if (f < total) {
+        const int lo = locate(f);
+        j[e] = rbegin(lo) + (f - rpad(lo));
+        v[e] = pts[j[e]];
+      } else {
+        v[e] = zero4;
+        j[e] = -1;
+      }
     }
   };
   Acc<KER> a[kTpt];
 #pragma unroll
   for (int q = 0; q < kTpt; ++q) a[q].zero();
-  constexpr int kPer = kChunk / kTileThreads;  // sources fetched per thread per chunk
   const int nch = (total + kChunk - 1) / kChunk;
+  // steps of kNs sources per lane per chunk: a chunk of n sources takes
+  // ceil(n / (kNs G)) steps (the zero-padded tail contributes nothing)
+  const int kStep = kNs * G;
+  const int steps_full = (kChunk + kStep - 1) / kStep;
+  const int steps_last = (total - (nch - 1) * kChunk + kStep - 1) / kStep;
   double4 v[kPer];
   int j[kPer];
+  fetch(0, v, j);
 #pragma unroll
   for (int e = 0; e < kPer; ++e) {
-    fetch(e * kTileThreads + tid, v[e], j[e]);
-    buf[0][e * kTileThreads + tid] = v[e];
-    sid[0][e * kTileThreads + tid] = j[e];
+    buf[0][slot(e, tid)] = v[e];
+    sid[0][slot(e, tid)] = j[e];
   }
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
     const bool more = c + 1 < nch;
-    if (more)
-#pragma unroll
-      for (int e = 0; e < kPer; ++e) fetch((c + 1) * kChunk + e * kTileThreads + tid, v[e], j[e]);
+    if (more) fetch((c + 1) * kChunk, v, j);
     const int n = min(kChunk, total - c * kChunk);
-    const double4* B = buf[c & 1];
-    const int* J = sid[c & 1];
-    const int iters = (n + G - 1) / G;
-    const int steps = (iters + kNs - 1) / kNs;
+    const double4* B = buf[c & 1] + g;  // this lane's sources: B[m G], m = 0, 1, ...
+    const int* J = sid[c & 1] + g;
+    const int steps = more ? steps_full : steps_last;
     // steps covering the chunk's near-possible prefix [0, near_total - c kChunk):
-    // the same staged blocks plus self-pair masking and one warp vote per
-    // block (exact per-pair path only for a block with a near lane)
+    // the same staged blocks with near pairs masked and counted, checked
+    // against the lane's self pairs once per chunk
     int near_steps = 0;
     if (MODE == kLeafMode) {
       const int nn = min(n, T.near_total - c * kChunk);
-      near_steps = nn > 0 ? (nn + kNs * G - 1) / (kNs * G) : 0;
+      near_steps = nn > 0 ? (nn + kStep - 1) / kStep : 0;
     }
 #ifdef SSUM_TIMING_NO_NEAR  // timing experiment only: wrong results for near/self pairs
     near_steps = 0;
@@ -165,10 +180,10 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     if (near_steps > 0) {
       int ncnt = 0;
 #pragma unroll 2
-      for (; it < near_steps; ++it) far_block<KER, kTpt, kNs, true>(x, B, g + it * kNs * G, G, a, &ncnt);
+      for (; it < near_steps; ++it) far_block<KER, kTpt, kNs, true>(x, B + it * kStep, G, a, &ncnt);
       // self pairs this lane walked in this chunk's near steps: the self
       // source of target ti sits at flattened position ti + T.self_shift
-      const int o_end = min(n, near_steps * kNs * G);
+      const int o_end = min(n, near_steps * kStep);
       int nself = 0;
 #pragma unroll
       for (int q = 0; q < kTpt; ++q) {
@@ -177,17 +192,18 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
       }
       if (__any_sync(0xffffffffu, ncnt != nself))
 #pragma unroll 1
-        for (int r = 0; r < near_steps; ++r) near_repair<KER, kTpt, kNs>(x, B, J, g + r * kNs * G, G, a, ti, flags);
+        for (int r = 0; r < near_steps; ++r) near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
     }
     // well-separated sources only: branch-free, kNs sources x kTpt targets
     // of independent chains per step (zero-padded tail contributes 0)
+    const double4* Bp = B + it * kStep;
 #pragma unroll 2
-    for (; it < steps; ++it) far_block<KER, kTpt, kNs>(x, B, g + it * kNs * G, G, a);
+    for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs>(x, Bp, G, a);
     if (more)
 #pragma unroll
       for (int e = 0; e < kPer; ++e) {
-        buf[(c + 1) & 1][e * kTileThreads + tid] = v[e];
-        sid[(c + 1) & 1][e * kTileThreads + tid] = j[e];
+        buf[(c + 1) & 1][slot(e, tid)] = v[e];
+        sid[(c + 1) & 1][slot(e, tid)] = j[e];
       }
     __syncthreads();
   }
@@ -266,27 +282,34 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
                   static_cast<int>(n), 0, 1, 0};
 }
 
+constexpr size_t kTileSmem = 2 * (sizeof(double4) + sizeof(int)) * (kChunk + kPad) + sizeof(int2) * kRangeCap;
+
+// k_tiles instantiation with its dynamic shared-memory limit raised once
+// (per process; every context's device is an sm_100a part)
+template <int KER, int MODE>
+auto tiles_kernel() {
+  static const bool ready = [] {
+    SSUM_CUDA_CHECK(cudaFuncSetAttribute(k_tiles<KER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTileSmem)));
+    return true;
+  }();
+  (void)ready;
+  return k_tiles<KER, MODE>;
+}
+
 }  // namespace
 
 void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
   Lists& L = c.lists;
-  if (kernel == kBS)
-    k_tiles<kBS, kFitMode><<<nfit, kTileThreads, 0, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p,
-                                                                nullptr, c.d_flags.p, L.fit_nodes.p, L.pslot.p,
-                                                                c.vinv.p, P, c.coeff.p);
-  else
-    k_tiles<kLOG, kFitMode><<<nfit, kTileThreads, 0, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p,
-                                                                 nullptr, c.d_flags.p, L.fit_nodes.p, L.pslot.p,
-                                                                 c.vinv.p, P, c.coeff.p);
+  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode>() : tiles_kernel<kLOG, kFitMode>();
+  k<<<nfit, kTileThreads, kTileSmem, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
+                                                 c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
 }
 
 void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S) {
-  if (kernel == kBS)
-    k_tiles<kBS, kLeafMode><<<ntl, kTileThreads, 0, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p,
-                                                                nullptr, nullptr, nullptr, 0, nullptr);
-  else
-    k_tiles<kLOG, kLeafMode><<<ntl, kTileThreads, 0, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p,
-                                                                 nullptr, nullptr, nullptr, 0, nullptr);
+  auto k = kernel == kBS ? tiles_kernel<kBS, kLeafMode>() : tiles_kernel<kLOG, kLeafMode>();
+  k<<<ntl, kTileThreads, kTileSmem, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
+                                                nullptr, nullptr, 0, nullptr);
 }
 
 // Direct sum (treecode.cpp:246-264): every target against one range [0, n)
