@@ -101,13 +101,27 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Partial proxy weights of one (weight node, particle chunk).
+// Partial proxy weights of one (weight node, particle chunk) per warp: each
+// lane accumulates the P basis sums over its stride of the chunk, then the
+// warp reduces them through a shared-memory transpose, 32 basis functions at
+// a time (lane j sums row j: 32 loads + adds instead of 5 shuffle rounds per
+// function).
+constexpr int kUpWarps = 4;
 template <int DEG>
-__global__ void __launch_bounds__(128) k_up_partial(const int4* __restrict__ chunks, const double4* __restrict__ pts,
-                                                    const double* __restrict__ cramer, double* __restrict__ wpart) {
+#ifndef SSUM_UP_MINB
+#define SSUM_UP_MINB 3  // measured: 3 resident blocks beat 1 (156 regs) and 4 (spills)
+#endif
+__global__ void __launch_bounds__(32 * kUpWarps, SSUM_UP_MINB) k_up_partial(const int4* __restrict__ chunks,
+                                                             const int* __restrict__ nchunks,
+                                                             const double4* __restrict__ pts,
+                                                             const double* __restrict__ cramer,
+                                                             double* __restrict__ wpart) {
   constexpr int P = Sbb<DEG>::P;
-  __shared__ double red[4][P];
-  const int4 ch = chunks[blockIdx.x];  // node, begin, count
+  __shared__ double tr[kUpWarps][32][33];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int chunk = blockIdx.x * kUpWarps + wp;
+  if (chunk >= *nchunks) return;  // warp-uniform
+  const int4 ch = chunks[chunk];  // node, begin, count
   const double* k = cramer + 12 * ch.x;
   double kc[10];
 #pragma unroll
@@ -115,8 +129,11 @@ __global__ void __launch_bounds__(128) k_up_partial(const int4* __restrict__ chu
   double w[P];
 #pragma unroll
   for (int m = 0; m < P; ++m) w[m] = 0.0;
-  for (int i = ch.y + threadIdx.x; i < ch.y + ch.z; i += blockDim.x) {
-    const double4 p = pts[i];
+  const int end = ch.y + ch.z;
+  double4 pn = ch.y + lane < end ? pts[ch.y + lane] : make_double4(0.0, 0.0, 0.0, 0.0);
+  for (int i = ch.y + lane; i < end; i += 32) {
+    const double4 p = pn;  // next particle's load in flight while this one is summed
+    if (i + 32 < end) pn = pts[i + 32];
     double b1, b2, b3;
     bary(kc, p.x, p.y, p.z, b1, b2, b3);
     double p1[DEG + 1], p2[DEG + 1], p3[DEG + 1];
@@ -129,18 +146,24 @@ __global__ void __launch_bounds__(128) k_up_partial(const int4* __restrict__ chu
       for (int jj = 0; jj <= DEG - kk; ++jj, ++m) w[m] = fma(p1[DEG - kk - jj] * p2[jj], t3, w[m]);
     }
   }
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  double (*t)[33] = tr[wp];
 #pragma unroll
-  for (int m = 0; m < P; ++m) {
-    const double v = warp_sum(w[m]);
-    if (lane == 0) red[wp][m] = v;
+  for (int g = 0; g < P; g += 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (g + j < P) t[j][lane] = w[g + j];
+    __syncwarp();
+    if (g + lane < P) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) s += t[lane][l];
+      wpart[size_t(chunk) * P + g + lane] = s;
+    }
+    __syncwarp();
   }
-  __syncthreads();
-  for (int m = threadIdx.x; m < P; m += blockDim.x)
-    wpart[size_t(blockIdx.x) * P + m] = ((red[0][m] + red[1][m]) + red[2][m]) + red[3][m];
 }
 
-constexpr int kUpChunk = 1024;  // particles per upward chunk
+constexpr int kUpChunk = 256;  // particles per upward chunk (one warp each)
 
 __global__ void k_up_nchunks(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ cnt,
                              int* __restrict__ nch) {
@@ -253,10 +276,13 @@ void launch_finish(Ctx& c, int degree, double* d_out) {
   c.launches++;
 }
 
-void launch_up_partial(Ctx& c, int degree, int nchunks) {
-#define SSUM_UP_CASE(DG)                                                                          \
-  case DG:                                                                                        \
-    k_up_partial<DG><<<nchunks, 128, 0, c.stream>>>(c.wchunks.p, c.pts.p, c.nodes.cramer.p, c.wpart.p); \
+// nchunks: host upper bound (grid size); d_nchunks: the device-side count.
+void launch_up_partial(Ctx& c, int degree, int nchunks, const int* d_nchunks) {
+  const unsigned grid = static_cast<unsigned>((nchunks + kUpWarps - 1) / kUpWarps);
+#define SSUM_UP_CASE(DG)                                                                                  \
+  case DG:                                                                                                \
+    k_up_partial<DG><<<grid, 32 * kUpWarps, 0, c.stream>>>(c.wchunks.p, d_nchunks, c.pts.p, c.nodes.cramer.p, \
+                                                           c.wpart.p);                                    \
     break;
   switch (degree) {
     SSUM_UP_CASE(1) SSUM_UP_CASE(2) SSUM_UP_CASE(3) SSUM_UP_CASE(4) SSUM_UP_CASE(5) SSUM_UP_CASE(6)
@@ -396,9 +422,11 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
     c.cub_tmp.ensure(tb);
     SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
-    int nch = 0;
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(&nch, c.wcount_off.p + nw, 4, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    // chunk count without a read-back: a particle lies in at most one node
+    // per level, so sum_w ceil(cnt_w / kUpChunk) <= nw + N (levels) / kUpChunk
+    const int64_t nch_bound =
+        int64_t(nw) + (int64_t(n) * (c.nodes.max_level + 1) + kUpChunk - 1) / kUpChunk;
+    const int nch = static_cast<int>(nch_bound);
     c.wchunks.ensure(size_t(nch) + size_t(nw));
     c.wpart.ensure(size_t(nch) * P);
     int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
@@ -406,7 +434,7 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
                                                        c.wchunks.p, d_crange);
     SSUM_LAUNCH_CHECK();
     c.launches += 4;
-    if (nch > 0) launch_up_partial(c, degree, nch);
+    if (nch > 0) launch_up_partial(c, degree, nch, c.wcount_off.p + nw);
     const int bt = ((P + 31) / 32) * 32;
     k_up_final<<<L.n_weight, bt, size_t(P) * 8, c.stream>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
                                                              P, L.pslot.p, n, c.pts.p);

@@ -76,7 +76,13 @@ struct NodeTable {
   DBuf<double> radius;      // 1
   DBuf<double> cramer;      // 12: bc = v2 x v3 (3), det (1), n2 = v3 x v1, n3 = v1 x v2 (6), spare (2)
   DBuf<int> level, parent, child_base, created_call;
+  // depth-first path key: root face << 58 | child index q << (58 - 2 level)
+  // per step; key order = depth-first order (levels <= kKeyMaxLevel)
+  DBuf<unsigned long long> key;
+  int max_level = 0;        // deepest level allocated so far
 };
+constexpr int kKeyRootShift = 58;
+constexpr int kKeyMaxLevel = 29;
 
 // Host snapshot of the node structure (ids, levels, links, creating call)
 // plus the last binning's counts/offsets. Downloaded on demand (exports,
@@ -104,6 +110,9 @@ struct Binned {
   // flags / child counts and prefix sums, all candidates of all levels
   DBuf<int> cand, cand_next, split, split_pos, nextc, next_pos, levels;
   std::vector<std::pair<int, int>> level_span;  // (offset in levels, count) per level
+  DBuf<unsigned long long> wkey, wkey2;  // reuse path: per-particle path keys, sorted
+  DBuf<unsigned char> leaf_flag;
+  DBuf<int> leaf_pos;       // reuse path: first tree position of each leaf
   DBuf<int> d_leaves;       // non-empty leaves in depth-first order
   DBuf<int> leaf_keys;
   int* h_small = nullptr;   // pinned host scratch

@@ -38,32 +38,74 @@ enum : int { kActLeaf = 0, kActDescend = 1 };
 
 __device__ __forceinline__ d3 load3(const double* p) { return {p[0], p[1], p[2]}; }
 
+// A triangle's circumcap {x : x.centre >= cos R} holds the triangle; a point
+// outside the cap by more than kCapMargin (in the cosine) is outside the
+// triangle by far more than the containment tolerance (1e-10 in barycentric
+// terms is ~1e-13 in distance), so its exact test can be skipped.
+constexpr double kCapMargin = 1e-9;
+__device__ __forceinline__ bool cap_excludes(const d3& p, const double* ctr, double cos_r_minus_margin) {
+  return fma(p.z, ctr[2], fma(p.y, ctr[1], p.x * ctr[0])) < cos_r_minus_margin;
+}
+
+// First of the 20 roots whose triangle contains p (face_tree.cpp:77-85), or
+// -1; st / skr: the roots' vertices and Cramer constants (shared memory).
+__device__ __forceinline__ int find_root(const d3& p, const double* st, const double* skr, const double* sc) {
+  for (int f = 0; f < 20; ++f) {
+    const double* k = skr + 12 * f;
+    if (cap_excludes(p, sc + 3 * f, k[11])) continue;
+    const d3 v1 = load3(st + 9 * f), v2 = load3(st + 9 * f + 3), v3 = load3(st + 9 * f + 6);
+    int in = contains_screen(v1, v2, v3, d3{k[0], k[1], k[2]}, k[3], k[10], p);
+    if (in < 0) in = contains_rn(v1, v2, v3, p);
+    if (in) return f;
+  }
+  return -1;
+}
+
+// distribute()'s child choice (face_tree.cpp:50-69): the first of the four
+// children cb .. cb+3 whose barycentric min-score is >= -1e-10, else the one
+// with the largest (least negative) exact score.
+__device__ __forceinline__ int find_child(const d3& p, int cb, const double* __restrict__ tri,
+                                          const double* __restrict__ cramer, const double* __restrict__ center) {
+  for (int c = cb; c < cb + 4; ++c) {  // first containing child wins (face_tree.cpp:56-61)
+    const double* k = cramer + 12 * c;
+    if (cap_excludes(p, center + 3 * c, k[11])) continue;
+    const double* t = tri + 9 * c;
+    const d3 va = load3(t), vb = load3(t + 3), vc = load3(t + 6), bc{k[0], k[1], k[2]};
+    int in = contains_screen(va, vb, vc, bc, k[3], k[10], p);
+    if (in < 0) in = min_score_rn(va, vb, vc, bc, k[3], p) >= -1e-10;
+    if (in) return c;
+  }
+  int best = cb;  // no child contains p: least-negative exact score (face_tree.cpp:62-69)
+  double best_s = -1e300;
+  for (int c = cb; c < cb + 4; ++c) {
+    const double* t = tri + 9 * c;
+    const double* k = cramer + 12 * c;
+    const double sc = min_score_rn(load3(t), load3(t + 3), load3(t + 6), d3{k[0], k[1], k[2]}, k[3], p);
+    if (sc > best_s) {
+      best_s = sc;
+      best = c;
+    }
+  }
+  return best;
+}
+
 // Root-face assignment: first of the 20 roots with triangle_contains
 // (face_tree.cpp:77-85). GeometryError when none contains the particle.
 __global__ void k_bin_roots(const double* __restrict__ xyz, int64_t n, const double* __restrict__ tri,
-                            const double* __restrict__ cramer, int* __restrict__ cur, int* __restrict__ cnt,
-                            int* __restrict__ flags) {
+                            const double* __restrict__ cramer, const double* __restrict__ center,
+                            int* __restrict__ cur, int* __restrict__ cnt, int* __restrict__ flags) {
   __shared__ double st[20 * 9];
   __shared__ double skr[20 * 12];
+  __shared__ double sc[20 * 3];
   __shared__ int scount[20];
   for (int k = threadIdx.x; k < 180; k += blockDim.x) st[k] = tri[k];
   for (int k = threadIdx.x; k < 240; k += blockDim.x) skr[k] = cramer[k];
+  for (int k = threadIdx.x; k < 60; k += blockDim.x) sc[k] = center[k];
   if (threadIdx.x < 20) scount[threadIdx.x] = 0;
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
-    const d3 p = load3(xyz + 3 * i);
-    int found = -1;
-    for (int f = 0; f < 20; ++f) {
-      const d3 v1 = load3(st + 9 * f), v2 = load3(st + 9 * f + 3), v3 = load3(st + 9 * f + 6);
-      const double* k = skr + 12 * f;
-      int in = contains_screen(v1, v2, v3, d3{k[0], k[1], k[2]}, k[3], k[10], p);
-      if (in < 0) in = contains_rn(v1, v2, v3, p);
-      if (in) {
-        found = f;
-        break;
-      }
-    }
+    const int found = find_root(load3(xyz + 3 * i), st, skr, sc);
     cur[i] = found;
     if (found < 0)
       atomicOr(flags, kFlagGeometry);
@@ -99,7 +141,7 @@ __device__ void write_node(double* tri, double* center, double* radius, double* 
   k[4] = n2.x; k[5] = n2.y; k[6] = n2.z;
   k[7] = n3.x; k[8] = n3.y; k[9] = n3.z;
   k[10] = 1.0 / k[3];  // screened containment (contains_screen)
-  k[11] = 0.0;
+  k[11] = cos(radius[id]) - kCapMargin;  // circumcap pre-filter (cap_excludes)
   if (bad) atomicOr(flags, kFlagGeometry);
 }
 
@@ -142,7 +184,8 @@ __global__ void k_level_apply(const int* __restrict__ cand, int m, const int* __
                               const int* __restrict__ split_pos, const int* __restrict__ nextc,
                               const int* __restrict__ next_pos, int node_base, int call_index, double* tri,
                               double* center, double* radius, double* cramer, int* level, int* parent,
-                              int* child_base, int* created_call, int* __restrict__ cand_next, int* flags) {
+                              int* child_base, int* created_call, unsigned long long* key,
+                              int* __restrict__ cand_next, int* flags) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   const int id = cand[k];
@@ -161,11 +204,13 @@ __global__ void k_level_apply(const int* __restrict__ cand, int m, const int* __
     write_node(tri, center, radius, cramer, cb + 2, m31, m23, v3, flags);
     write_node(tri, center, radius, cramer, cb + 3, m12, m23, m31, flags);
     const int lv = level[id] + 1;
+    const int ks = kKeyRootShift - 2 * min(lv, kKeyMaxLevel);  // keys past kKeyMaxLevel are unused
     for (int q = 0; q < 4; ++q) {
       level[cb + q] = lv;
       parent[cb + q] = id;
       child_base[cb + q] = -1;
       created_call[cb + q] = call_index;
+      key[cb + q] = key[id] | (static_cast<unsigned long long>(q) << ks);
     }
     child_base[id] = cb;
   }
@@ -177,7 +222,8 @@ __global__ void k_level_apply(const int* __restrict__ cand, int m, const int* __
 __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __restrict__ cur,
                           int* __restrict__ leaf_of, const unsigned char* __restrict__ act,
                           const int* __restrict__ child_base, const double* __restrict__ tri,
-                          const double* __restrict__ cramer, int* __restrict__ cnt) {
+                          const double* __restrict__ cramer, const double* __restrict__ center,
+                          int* __restrict__ cnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int node = cur[i];
@@ -187,35 +233,93 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
     cur[i] = -1;
     return;
   }
-  const d3 p = load3(xyz + 3 * i);
-  const int cb = child_base[node];
-  int placed = -1;
-  for (int c = cb; c < cb + 4 && placed < 0; ++c) {  // first containing child wins (face_tree.cpp:56-61)
-    const double* t = tri + 9 * c;
-    const double* k = cramer + 12 * c;
-    const d3 va = load3(t), vb = load3(t + 3), vc = load3(t + 6), bc{k[0], k[1], k[2]};
-    int in = contains_screen(va, vb, vc, bc, k[3], k[10], p);
-    if (in < 0) in = min_score_rn(va, vb, vc, bc, k[3], p) >= -1e-10;
-    if (in) placed = c;
-  }
-  int best = cb;
-  if (placed < 0) {  // no child contains p: least-negative exact score (face_tree.cpp:62-69)
-    double best_s = -1e300;
-    for (int c = cb; c < cb + 4; ++c) {
-      const double* t = tri + 9 * c;
-      const double* k = cramer + 12 * c;
-      const double s = min_score_rn(load3(t), load3(t + 3), load3(t + 6), d3{k[0], k[1], k[2]}, k[3], p);
-      if (s > best_s) {
-        best_s = s;
-        best = c;
-      }
-    }
-  }
-  if (placed < 0) placed = best;
+  const int placed = find_child(load3(xyz + 3 * i), child_base[node], tri, cramer, center);
   cur[i] = placed;
   // warp-aggregated bin count: one atomic per distinct child in the warp
   const unsigned peers = __match_any_sync(__activemask(), placed);
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&cnt[placed], __popc(peers));
+}
+
+// ---- reuse path: every particle's path through the existing children ------
+//
+// Once the tree exists, distribute() descends into existing children
+// whatever the bin size (face_tree.cpp:42-47), so a particle's path down to
+// the first childless node is fixed by geometry alone. One kernel walks each
+// particle down that path and emits the node's depth-first path key; one
+// radix sort of (key, id) is the tree-order permutation; per-node bin ranges
+// are two binary searches of the node's key range in the sorted keys. The
+// binning is final unless a childless node must split (bin > N_T below
+// max_depth) — then the level-synchronous build runs instead.
+__global__ void k_walk(const double* __restrict__ xyz, int64_t n, const double* __restrict__ tri,
+                       const double* __restrict__ cramer, const double* __restrict__ center,
+                       const int* __restrict__ child_base, const unsigned long long* __restrict__ nkey,
+                       unsigned long long* __restrict__ key, int* __restrict__ ids, int* __restrict__ leaf_of,
+                       int* __restrict__ flags) {
+  __shared__ double st[20 * 9];
+  __shared__ double skr[20 * 12];
+  __shared__ double sc[20 * 3];
+  for (int k = threadIdx.x; k < 180; k += blockDim.x) st[k] = tri[k];
+  for (int k = threadIdx.x; k < 240; k += blockDim.x) skr[k] = cramer[k];
+  for (int k = threadIdx.x; k < 60; k += blockDim.x) sc[k] = center[k];
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const d3 p = load3(xyz + 3 * i);
+  int node = find_root(p, st, skr, sc);
+  if (node < 0) {
+    atomicOr(flags, kFlagGeometry);
+    key[i] = ~0ull;
+    leaf_of[i] = -1;
+  } else {
+    for (int cb = child_base[node]; cb >= 0; cb = child_base[node]) node = find_child(p, cb, tri, cramer, center);
+    key[i] = nkey[node];
+    leaf_of[i] = node;
+  }
+  ids[i] = static_cast<int>(i);
+}
+
+__device__ __forceinline__ int lower_bound_u64(const unsigned long long* __restrict__ a, int n, unsigned long long v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Bin range of every node: its key range [key, key + 4^(kKeyMaxLevel - level))
+// in the sorted keys. Flags the leaves of this call (non-empty, childless)
+// and counts the childless nodes that would have to split.
+__global__ void k_node_ranges(int nn, const unsigned long long* __restrict__ nkey, const int* __restrict__ level,
+                              const int* __restrict__ child_base, const unsigned long long* __restrict__ skey,
+                              int n, int nt, int max_depth, int* __restrict__ cnt, int* __restrict__ off,
+                              unsigned char* __restrict__ is_leaf, int* __restrict__ n_split) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nn) return;
+  const unsigned long long k0 = nkey[id];
+  const unsigned long long k1 = k0 + (1ull << (kKeyRootShift - 2 * level[id]));
+  const int b = lower_bound_u64(skey, n, k0);
+  const int e = lower_bound_u64(skey, n, k1);
+  cnt[id] = e - b;
+  off[id] = b;
+  const bool leaf = e > b && child_base[id] < 0;
+  is_leaf[id] = leaf ? 1 : 0;
+  if (leaf && e - b > nt && level[id] < max_depth) atomicAdd(n_split, 1);
+}
+
+// First tree position of each leaf: where the sorted key changes.
+__global__ void k_leaf_starts(const unsigned long long* __restrict__ skey, int n, unsigned char* __restrict__ flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) flag[k] = (k == 0 || skey[k] != skey[k - 1]) ? 1 : 0;
+}
+
+__global__ void k_leaf_list(const int* __restrict__ start, const int* __restrict__ nl, const int* __restrict__ perm,
+                            const int* __restrict__ leaf_of, int* __restrict__ leaves) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < *nl) leaves[r] = leaf_of[perm[start[r]]];
 }
 
 // Depth-first bin offsets, top-down: roots in face order ...
@@ -286,6 +390,7 @@ static void grow_nodes(Ctx& c, int need) {
   t.level.ensure(size_t(need), true, c.stream);
   t.parent.ensure(size_t(need), true, c.stream);
   t.created_call.ensure(size_t(need), true, c.stream);
+  t.key.ensure(size_t(need), true, c.stream);
   c.bins.cnt.ensure(size_t(need), true, c.stream);
   c.bins.act.ensure(size_t(need), true, c.stream);
   c.bins.is_leaf.ensure(size_t(need), true, c.stream);
@@ -330,12 +435,14 @@ void tree_init_roots(Ctx& c) {
       radius[f] = arc_dist(ctr, a);
       const d3 bc = cross_rn(b, cc), n2 = cross_rn(cc, a), n3 = cross_rn(a, b);
       const double det = dot_rn(a, bc);
-      const double kk[12] = {bc.x, bc.y, bc.z, det, n2.x, n2.y, n2.z, n3.x, n3.y, n3.z, 1.0 / det, 0};
+      const double kk[12] = {bc.x, bc.y, bc.z, det, n2.x, n2.y, n2.z, n3.x, n3.y, n3.z, 1.0 / det,
+                             std::cos(radius[f]) - kCapMargin};
       std::copy(kk, kk + 12, cramer.begin() + 12 * f);
     }
   }
   if (bad) throw Error(SSUM_GEOMETRY, "degenerate base icosahedron");
   c.nodes.count = 20;
+  c.nodes.max_level = 0;
   grow_nodes(c, 1024);
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.tri.p, tri.data(), tri.size() * 8, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.center.p, center.data(), center.size() * 8, cudaMemcpyHostToDevice, c.stream));
@@ -346,8 +453,70 @@ void tree_init_roots(Ctx& c) {
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.created_call.p, zero.data(), 80, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.parent.p, minus.data(), 80, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.child_base.p, minus.data(), 80, cudaMemcpyHostToDevice, c.stream));
+  std::vector<unsigned long long> rkey(20);
+  for (int q = 0; q < 20; ++q) rkey[q] = static_cast<unsigned long long>(q) << kKeyRootShift;
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.nodes.key.p, rkey.data(), 160, cudaMemcpyHostToDevice, c.stream));
   if (!c.bins.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&c.bins.h_small, 64 * sizeof(int)));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
+// Binning through the existing tree (see k_walk). Returns false, with
+// nothing of the call's state committed, when the tree cannot be reused as
+// is: no children yet, deeper than the path keys reach, or a childless node
+// whose bin now needs a split.
+static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
+  NodeTable& T = c.nodes;
+  Binned& B = c.bins;
+  if (T.count <= 20 || T.max_level > kKeyMaxLevel || n > 0x3fffffff) return false;
+  const int nn = T.count;
+  const int ni = static_cast<int>(n);
+  const int bs = 256;
+  B.wkey.ensure(size_t(n));
+  B.wkey2.ensure(size_t(n));
+  B.sort_vals.ensure(std::max<size_t>(size_t(n), size_t(nn)));
+  B.perm.ensure(size_t(n));
+  B.pos_leaf.ensure(size_t(n));
+  B.d_leaves.ensure(size_t(nn));
+  B.leaf_pos.ensure(size_t(nn));
+  B.leaf_flag.ensure(size_t(n));
+  int* d_cnt = c.d_flags.p + 16;  // [0] splits needed, [1] leaves
+  SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(int), c.stream));
+  k_walk<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, T.tri.p, T.cramer.p, T.center.p, T.child_base.p, T.key.p,
+                                               B.wkey.p, B.sort_vals.p, B.leaf_of.p, c.d_flags.p);
+  SSUM_LAUNCH_CHECK();
+  const int begin_bit = kKeyRootShift - 2 * T.max_level;
+  size_t tmp = 0;
+  SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, B.wkey.p, B.wkey2.p, B.sort_vals.p, B.perm.p, ni,
+                                                  begin_bit, 64, c.stream));
+  c.cub_tmp.ensure(tmp);
+  SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(c.cub_tmp.p, tmp, B.wkey.p, B.wkey2.p, B.sort_vals.p, B.perm.p, ni,
+                                                  begin_bit, 64, c.stream));
+  k_node_ranges<<<grid_for(nn, bs), bs, 0, c.stream>>>(nn, T.key.p, T.level.p, T.child_base.p, B.wkey2.p, ni, nt,
+                                                       max_depth, B.cnt.p, B.off.p, B.is_leaf.p, d_cnt);
+  SSUM_LAUNCH_CHECK();
+  k_leaf_starts<<<grid_for(n, bs), bs, 0, c.stream>>>(B.wkey2.p, ni, B.leaf_flag.p);
+  SSUM_LAUNCH_CHECK();
+  {
+    cub::CountingInputIterator<int> pos(0);
+    tmp = 0;
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tmp, pos, B.leaf_flag.p, B.leaf_pos.p, d_cnt + 1, ni,
+                                               c.stream));
+    c.cub_tmp.ensure(tmp);
+    SSUM_CUDA_CHECK(cub::DeviceSelect::Flagged(c.cub_tmp.p, tmp, pos, B.leaf_flag.p, B.leaf_pos.p, d_cnt + 1, ni,
+                                               c.stream));
+  }
+  k_leaf_list<<<grid_for(n, bs), bs, 0, c.stream>>>(B.leaf_pos.p, d_cnt + 1, B.perm.p, B.leaf_of.p, B.d_leaves.p);
+  SSUM_LAUNCH_CHECK();
+  k_pos_leaf<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, B.leaf_of.p, B.pos_leaf.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches += 12;
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, d_cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (B.h_small[0] & kFlagGeometry) check_flags(c, "bin_particles: particle contained in no root face");
+  if (B.h_small[1] > 0) return false;
+  B.n_leaves = B.h_small[2];
+  return true;
 }
 
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
@@ -366,9 +535,17 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   if (n == 0) return;
   B.cur.ensure(size_t(n));
   B.leaf_of.ensure(size_t(n));
+  if (bin_reuse(c, d_xyz, n, nt, max_depth)) {
+    trace().mark("bin.reuse");
+    return;
+  }
+  // level-synchronous build from the roots (fresh counts again: the reuse
+  // attempt may have filled them)
+  SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p, 0, size_t(c.nodes.count) * sizeof(int), c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(B.is_leaf.p, 0, size_t(c.nodes.count), c.stream));
 
-  k_bin_roots<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, c.nodes.tri.p, c.nodes.cramer.p, B.cur.p, B.cnt.p,
-                                                     c.d_flags.p);
+  k_bin_roots<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, c.nodes.tri.p, c.nodes.cramer.p, c.nodes.center.p,
+                                                     B.cur.p, B.cnt.p, c.d_flags.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   check_flags(c, "bin_particles: particle contained in no root face");
@@ -411,10 +588,10 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     k_level_apply<<<grid_for(m, 128), 128, 0, c.stream>>>(
         B.cand.p, m, B.split.p, B.split_pos.p, B.nextc.p, B.next_pos.p, c.nodes.count, c.call_index, c.nodes.tri.p,
         c.nodes.center.p, c.nodes.radius.p, c.nodes.cramer.p, c.nodes.level.p, c.nodes.parent.p,
-        c.nodes.child_base.p, c.nodes.created_call.p, B.cand_next.p, c.d_flags.p);
+        c.nodes.child_base.p, c.nodes.created_call.p, c.nodes.key.p, B.cand_next.p, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
     k_descend<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, B.cur.p, B.leaf_of.p, B.act.p, c.nodes.child_base.p,
-                                                     c.nodes.tri.p, c.nodes.cramer.p, B.cnt.p);
+                                                     c.nodes.tri.p, c.nodes.cramer.p, c.nodes.center.p, B.cnt.p);
     SSUM_LAUNCH_CHECK();
     c.launches += 3;
     SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, B.split_pos.p + m, 4, cudaMemcpyDeviceToHost, c.stream));
@@ -422,6 +599,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     trace().mark("bin.level");
     c.nodes.count += 4 * B.h_small[0];
+    if (B.h_small[0] > 0) c.nodes.max_level = std::max(c.nodes.max_level, static_cast<int>(B.level_span.size()));
     m = B.h_small[1];
     std::swap(B.cand, B.cand_next);
   }

@@ -222,6 +222,31 @@ def test_reused_tree_semantics(ss, ol, mesh_fixture):
         compare_trees(t.export(), r.export())
 
 
+def test_reused_tree_moving_particles(ss, ol, mesh_fixture):
+    """Binning through an existing tree as particles move (the RK4 pattern):
+    calls that fit the existing tree take the device walk + sort path, calls
+    whose bins outgrow a leaf rebuild level by level; every call's tree and
+    bins stay bit-identical to the reference FaceTree given the same calls."""
+    xyz, _, _ = mesh_fixture(6)
+    rng = np.random.default_rng(11)
+
+    def moved(p, eps):
+        p = p + eps * rng.standard_normal(p.shape)
+        return p / np.linalg.norm(p, axis=1, keepdims=True)
+
+    def rotated(p, ang):
+        c, s = np.cos(ang), np.sin(ang)
+        return p @ np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]]).T
+
+    t = ss.FaceTree()
+    r = ol.RefTree()
+    for pts in (xyz, xyz, moved(xyz, 1e-4), rotated(xyz, 0.3), moved(xyz, 3e-3), xyz[::3].copy(), xyz):
+        pts = np.ascontiguousarray(pts)
+        t.bin_particles(pts, 32, 10)
+        r.bin(pts, 32, 10)
+        compare_trees(t.export(), r.export())
+
+
 def test_max_depth_fallback_and_big_leaves(ss, ol, mesh_fixture):
     """max_depth binds: leaves with > 32 targets (multi-tile) and PP pairs at
     internal targets (treecode.cpp:54-57)."""
