@@ -298,6 +298,7 @@ void ssum_destroy(ssum_ctx* h) {
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
+  if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }

@@ -95,12 +95,6 @@ __global__ void k_proxy(const int* __restrict__ slot_node, int nslots, int degre
   pts[N + g] = make_double4(u.x, u.y, u.z, 0.0);
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // Partial proxy weights of one (weight node, particle chunk) per warp: each
 // lane accumulates the P basis sums over its stride of the chunk, then the
 // warp reduces them through a shared-memory transpose, 32 basis functions at

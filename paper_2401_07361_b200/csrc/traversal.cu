@@ -48,14 +48,28 @@ __device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_o
 }
 
 // action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
-__global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* __restrict__ cnt,
-                            const double* __restrict__ center, const double* __restrict__ radius,
-                            const int* __restrict__ level, const int* __restrict__ child_base, double theta,
-                            int thr, int max_depth, int pc_only, int* __restrict__ action,
-                            unsigned long long* __restrict__ packed) {
+// Frontier size: *d_m when the size lives on the device (planned traversal,
+// grid sized for `bound`), else `bound` itself. A device size above the bound
+// sets *ovf and is clamped (the planned traversal is then redone).
+__device__ __forceinline__ int frontier_size(const int* d_m, int bound, int* ovf) {
+  if (!d_m) return bound;
+  const int m = *d_m;
+  if (m > bound) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(ovf, 1);
+    return bound;
+  }
+  return m;
+}
+
+__global__ void k_trav_eval(const PairEntry* __restrict__ F, const int* __restrict__ d_m, int bound,
+                            const int* __restrict__ cnt, const double* __restrict__ center,
+                            const double* __restrict__ radius, const int* __restrict__ level,
+                            const int* __restrict__ child_base, double theta, int thr, int max_depth, int pc_only,
+                            int* __restrict__ action, unsigned long long* __restrict__ packed, int* ovf) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k > m) return;
-  if (k == m) {  // sentinel: the exclusive scan's entry m is the total
+  if (k > bound) return;
+  const int m = frontier_size(d_m, bound, ovf);
+  if (k >= m) {  // sentinel and padding: the exclusive scan's entry `bound` is the total
     packed[k] = 0;
     return;
   }
@@ -85,11 +99,25 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
   packed[k] = (emit << 32) | kids;
 }
 
-__global__ void k_trav_scatter(const PairEntry* __restrict__ F, int m, const int* __restrict__ action,
-                               const unsigned long long* __restrict__ scan, const int* __restrict__ child_base,
-                               PairEntry* __restrict__ Fnext, int4* __restrict__ E,
-                               unsigned long long* __restrict__ K, long long e_base, int* flags) {
+// d_ebase: emission base of this step (planned traversal; [1] receives the
+// next step's base and d_m_next the next frontier size), else e_base_host.
+// Writes beyond cap_next / e_cap set *ovf instead.
+__global__ void k_trav_scatter(const PairEntry* __restrict__ F, const int* __restrict__ d_m, int bound,
+                               const int* __restrict__ action, const unsigned long long* __restrict__ scan,
+                               const int* __restrict__ child_base, PairEntry* __restrict__ Fnext, int cap_next,
+                               int4* __restrict__ E, unsigned long long* __restrict__ K, long long e_cap,
+                               long long e_base_host, long long* d_ebase, int* d_m_next, int* flags, int* ovf) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = frontier_size(d_m, bound, ovf);
+  const long long e_base = d_ebase ? d_ebase[0] : e_base_host;
+  if (k == 0 && d_m_next) {
+    const unsigned long long tot = scan[bound];
+    const int next = static_cast<int>(tot & 0xffffffffull);
+    const long long emitted = static_cast<long long>(tot >> 32);
+    *d_m_next = next;
+    d_ebase[1] = e_base + emitted;
+    if (next > cap_next || e_base + emitted > e_cap) atomicOr(ovf, 1);
+  }
   if (k >= m) return;
   const int a = action[k];
   if (!a) return;
@@ -97,10 +125,12 @@ __global__ void k_trav_scatter(const PairEntry* __restrict__ F, int m, const int
   const PairEntry p = F[k];
   if (a & 4) {
     const long long e = e_base + static_cast<long long>(sc >> 32);
+    if (e >= e_cap) return;
     E[e] = int4{p.t, p.s, a & 3, 0};
     K[e] = p.key;
   } else {
     const int o = static_cast<int>(sc & 0xffffffffull);
+    if (o + 4 > cap_next) return;
     const bool rt = (a & 16) != 0;
     const int cb = child_base[rt ? p.t : p.s];
     const int step = p.step + 1;
@@ -118,8 +148,13 @@ __global__ void k_trav_scatter(const PairEntry* __restrict__ F, int m, const int
   }
 }
 
-__global__ void k_root_pairs(PairEntry* F) {
+__global__ void k_root_pairs(PairEntry* F, int* d_m0, long long* d_ebase0, int* ovf) {
   const int k = threadIdx.x + blockIdx.x * blockDim.x;
+  if (k == 0 && d_m0) {
+    *d_m0 = 400;
+    *d_ebase0 = 0;
+    *ovf = 0;
+  }
   if (k >= 400) return;
   PairEntry p;
   p.t = k / 20;
@@ -366,39 +401,32 @@ void exclusive_scan(Ctx& c, const T* in, T* out, int64_t n) {
 
 static TravScratch& scratch(Ctx& c) { return c.trav; }
 
-void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys) {
-  (void)keep_order_keys;
+// Breadth-first traversal with one host read per step (the frontier size
+// sizes the next step). Records the step sizes as the plan for the next call.
+static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
   Lists& L = c.lists;
   Binned& B = c.bins;
-  TravScratch& S = scratch(c);
-  const int nn = c.nodes.count;
-  const int64_t N = B.n;
-  const int P = (cfg.degree + 1) * (cfg.degree + 2) / 2;
+  TravScratch& S = c.trav;
   const int bs = 256;
-  L.n_inter = 0;
-  for (int k = 0; k < 4; ++k) L.counts[k] = L.evals[k] = 0;
-  L.n_proxy = L.n_weight = L.n_fit = L.n_leaf_tiles = L.n_fit_tiles = 0;
-  L.n_leaf_ranges = L.n_fit_ranges = 0;
-  if (N == 0) return;
-
-  // ---- breadth-first traversal
+  int* ovf = c.d_flags.p + 24;
   S.F0.ensure(400);
-  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, nullptr, nullptr, nullptr);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   int m = 400;
   long long ne = 0;
   L.inter.ensure(1 << 16);
   L.key.ensure(1 << 16);
-  if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
+  S.plan_m.clear();
   while (m > 0) {
+    S.plan_m.push_back(m);
     S.action.ensure(size_t(m) + 1);
     S.packed.ensure(size_t(m) + 1);
     S.scan.ensure(size_t(m) + 1);
-    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
-                                                           c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
-                                                           cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
-                                                           S.packed.p);
+    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, nullptr, m, B.cnt.p, c.nodes.center.p,
+                                                           c.nodes.radius.p, c.nodes.level.p, c.nodes.child_base.p,
+                                                           cfg.theta, cfg.n_threshold, cfg.max_depth, cfg.pc_only,
+                                                           S.action.p, S.packed.p, ovf);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     exclusive_scan(c, S.packed.p, S.scan.p, m + 1);  // packed[m] = 0: totals at scan[m]
@@ -410,14 +438,94 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     L.inter.ensure(size_t(ne + emitted), true, c.stream);
     L.key.ensure(size_t(ne + emitted), true, c.stream);
     S.F1.ensure(size_t(std::max(next, 1)));
-    k_trav_scatter<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, m, S.action.p, S.scan.p, c.nodes.child_base.p,
-                                                          S.F1.p, L.inter.p, L.key.p, ne, c.d_flags.p);
+    k_trav_scatter<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, nullptr, m, S.action.p, S.scan.p,
+                                                          c.nodes.child_base.p, S.F1.p, next, L.inter.p, L.key.p,
+                                                          ne + emitted, ne, nullptr, nullptr, c.d_flags.p, ovf);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     ne += emitted;
     std::swap(S.F0, S.F1);
     m = next;
   }
+  S.plan_ne = ne;
+  S.plan_valid = true;
+  return ne;
+}
+
+// The same traversal with no host read between steps: every step's grid and
+// buffers are sized from the previous call's step sizes (plus slack), the
+// true sizes stay on the device, and one read at the end checks that no step
+// outgrew its bound (else false: the caller redoes it synchronously).
+static bool bfs_planned(Ctx& c, const ssum_config& cfg, long long& ne_out) {
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  TravScratch& S = c.trav;
+  if (!S.plan_valid || S.plan_m.empty() || S.plan_m.size() > 200) return false;
+  const int bs = 256;
+  const int steps = static_cast<int>(S.plan_m.size());
+  std::vector<int> mb(size_t(steps) + 1);
+  for (int s = 0; s < steps; ++s) mb[s] = s == 0 ? 400 : S.plan_m[s] + S.plan_m[s] / 8 + 256;
+  mb[steps] = 256;  // the frontier after the last planned step must be empty
+  const int fmax = *std::max_element(mb.begin(), mb.end());
+  const long long ecap = S.plan_ne + S.plan_ne / 8 + 4096;
+  S.F0.ensure(size_t(fmax));
+  S.F1.ensure(size_t(fmax));
+  S.action.ensure(size_t(fmax) + 1);
+  S.packed.ensure(size_t(fmax) + 1);
+  S.scan.ensure(size_t(fmax) + 1);
+  L.inter.ensure(size_t(ecap));
+  L.key.ensure(size_t(ecap));
+  S.dm.ensure(size_t(steps) + 1);
+  S.debase.ensure(size_t(steps) + 1);
+  if (!S.h_plan) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_plan, 256 * sizeof(long long)));
+  int* ovf = c.d_flags.p + 24;
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, S.dm.p, S.debase.p, ovf);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+  for (int s = 0; s < steps; ++s) {
+    k_trav_eval<<<grid_for(mb[s] + 1, bs), bs, 0, c.stream>>>(S.F0.p, S.dm.p + s, mb[s], B.cnt.p, c.nodes.center.p,
+                                                                c.nodes.radius.p, c.nodes.level.p,
+                                                                c.nodes.child_base.p, cfg.theta, cfg.n_threshold,
+                                                                cfg.max_depth, cfg.pc_only, S.action.p, S.packed.p,
+                                                                ovf);
+    SSUM_LAUNCH_CHECK();
+    exclusive_scan(c, S.packed.p, S.scan.p, mb[s] + 1);
+    k_trav_scatter<<<grid_for(std::max(mb[s], 1), bs), bs, 0, c.stream>>>(
+        S.F0.p, S.dm.p + s, mb[s], S.action.p, S.scan.p, c.nodes.child_base.p, S.F1.p, mb[s + 1], L.inter.p,
+        L.key.p, ecap, 0, S.debase.p + s, S.dm.p + s + 1, c.d_flags.p, ovf);
+    SSUM_LAUNCH_CHECK();
+    c.launches += 2;
+    std::swap(S.F0, S.F1);
+  }
+  int* h = reinterpret_cast<int*>(S.h_plan);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, ovf, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h + 1, S.dm.p, (size_t(steps) + 1) * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_plan + 128, S.debase.p + steps, sizeof(long long), cudaMemcpyDeviceToHost,
+                                  c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (h[0] != 0 || h[1 + steps] != 0) return false;
+  for (int s = 0; s < steps; ++s) S.plan_m[s] = h[1 + s];
+  S.plan_ne = S.h_plan[128];
+  ne_out = S.plan_ne;
+  return true;
+}
+
+void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys) {
+  (void)keep_order_keys;
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  TravScratch& S = scratch(c);
+  const int64_t N = B.n;
+  L.n_inter = 0;
+  for (int k = 0; k < 4; ++k) L.counts[k] = L.evals[k] = 0;
+  L.n_proxy = L.n_weight = L.n_fit = L.n_leaf_tiles = L.n_fit_tiles = 0;
+  L.n_leaf_ranges = L.n_fit_ranges = 0;
+  if (N == 0) return;
+
+  // ---- breadth-first traversal
+  long long ne = 0;
+  if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
+  if (!bfs_planned(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
   L.n_inter = ne;
   trace().mark("trav.bfs");
   build_lists(c, cfg);
