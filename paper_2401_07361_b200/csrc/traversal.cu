@@ -237,76 +237,119 @@ __global__ void k_leaf_count(const int* __restrict__ leaves, int nl, const int* 
 
 // May a pair (x in leaf, y in node s) have 1 - x.y < 2^-20? Only if the two
 // circumcircles come within kNearArc of each other (every binned point lies
-// in its node's circumcircle, up to the -1e-10 containment tolerance).
+// in its node's circumcircle, up to the -1e-10 containment tolerance). The
+// test is on the chord (<= the arc), so it errs only towards "near".
 __device__ __forceinline__ bool near_possible(int leaf, int s, const double* __restrict__ center,
                                               const double* __restrict__ radius) {
   if (leaf == s) return true;
-  const d3 a{center[3 * leaf], center[3 * leaf + 1], center[3 * leaf + 2]};
-  const d3 b{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
-  const double cx = a.y * b.z - a.z * b.y, cy = a.z * b.x - a.x * b.z, cz = a.x * b.y - a.y * b.x;
-  const double arc = atan2(sqrt(cx * cx + cy * cy + cz * cz), a.x * b.x + a.y * b.y + a.z * b.z);
-  return arc - radius[leaf] - radius[s] < kNearArc;
+  const double dx = center[3 * leaf] - center[3 * s], dy = center[3 * leaf + 1] - center[3 * s + 1],
+               dz = center[3 * leaf + 2] - center[3 * s + 2];
+  const double lim = radius[leaf] + radius[s] + kNearArc;
+  return fma(dx, dx, fma(dy, dy, dz * dz)) < lim * lim;
 }
 
-// Range list of one leaf: PP and PC entries of every node on its
-// root-to-leaf path (treecode.cpp:379-396), near-possible PP ranges first.
-__global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* __restrict__ parent,
-                            const int2* __restrict__ seg, const int* __restrict__ sorted_e,
-                            const int4* __restrict__ E, const int* __restrict__ cnt, const int* __restrict__ off,
-                            const int* __restrict__ pslot, const double* __restrict__ center,
-                            const double* __restrict__ radius, const int* __restrict__ range_off,
-                            const int* __restrict__ tile_off, int64_t N, int P, SrcRange* __restrict__ ranges,
-                            Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
-                            unsigned long long* __restrict__ evals) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// Range list of one leaf, one warp per leaf: PP and PC entries of every node
+// on its root-to-leaf path (treecode.cpp:379-396), near-possible PP ranges
+// first, each pass in path order (root to leaf, segment order within a
+// node). Lanes take 32 entries at a time; a ballot keeps the serial order and
+// a warp scan gives each range its flattened-list prefix.
+constexpr int kFillWarps = 4;
+__global__ void __launch_bounds__(32 * kFillWarps)
+    k_leaf_fill(const int* __restrict__ leaves, int nl, const int* __restrict__ parent,
+                const int2* __restrict__ seg, const int* __restrict__ sorted_e, const int4* __restrict__ E,
+                const int* __restrict__ cnt, const int* __restrict__ off, const int* __restrict__ pslot,
+                const double* __restrict__ center, const double* __restrict__ radius,
+                const int* __restrict__ range_off, const int* __restrict__ tile_off, int64_t N, int P,
+                SrcRange* __restrict__ ranges, Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
+                unsigned long long* __restrict__ evals) {
+  __shared__ int spath[kFillWarps][48];
+  __shared__ int sbeg[kFillWarps][49];  // first flattened entry of each path node (root first)
+  __shared__ int spl[kFillWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int k = blockIdx.x * kFillWarps + wid;
   unsigned long long pp = 0, pc = 0;
-  if (k < nl) {
+  if (k < nl) {  // warp-uniform
     const int leaf = leaves[k];
-    int path[48];
-    int pl = 0;
-    for (int a = leaf; a >= 0 && pl < 48; a = parent[a]) path[pl++] = a;
-    int w = range_off[k];
-    const int w0 = w;
-    unsigned long long src_pp = 0, src_pc = 0;
-    int near_total = 0;
-    int self_shift = 0, has_self = 0;  // self source of particle i at flattened position i + self_shift
-    for (int pass = 0; pass < 2; ++pass) {  // 0: near-possible PP ranges, 1: the rest
-      for (int q = pl - 1; q >= 0; --q) {   // root to leaf (treecode.cpp:379,392)
-        const int2 sg = seg[2 * path[q]];
-        for (int i = sg.x; i < sg.y; ++i) {
-          const int4 it = E[sorted_e[i]];
-          const bool nr = it.z == 0 && near_possible(leaf, it.y, center, radius);
-          if (nr != (pass == 0)) continue;
-          SrcRange r;
-          r.pad = static_cast<int>(src_pp + src_pc);  // flattened-list prefix
-          if (it.z == 0) {
-            r.begin = off[it.y];
-            r.count = cnt[it.y];
-            r.near = nr ? 1 : 0;
-            if (r.begin <= off[leaf] && off[leaf] < r.begin + r.count) {  // holds the leaf's own particles
-              self_shift = r.pad - r.begin;
-              has_self = 1;
-            }
-            src_pp += static_cast<unsigned long long>(r.count);
-          } else {
-            r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
-            r.count = P;
-            r.near = 0;
-            src_pc += static_cast<unsigned long long>(P);
-          }
-          ranges[w++] = r;
-        }
+    if (lane == 0) {
+      int tmp[48];
+      int pl = 0;
+      for (int a = leaf; a >= 0 && pl < 48; a = parent[a]) tmp[pl++] = a;
+      int run = 0;
+      for (int q = 0; q < pl; ++q) {
+        const int node = tmp[pl - 1 - q];
+        const int2 sg = seg[2 * node];
+        spath[wid][q] = node;
+        sbeg[wid][q] = run;
+        run += sg.y - sg.x;
       }
-      if (pass == 0) near_total = static_cast<int>(src_pp);
+      sbeg[wid][pl] = run;
+      spl[wid] = pl;
+    }
+    __syncwarp();
+    const int pl = spl[wid];
+    const int T = sbeg[wid][pl];
+    const int offl = off[leaf];
+    const int w0 = range_off[k];
+    int w = 0, src = 0, src_pp = 0, src_pc = 0, near_total = 0, self_shift = 0, has_self = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // 0: near-possible PP ranges, 1: the rest
+      for (int base = 0; base < T; base += 32) {
+        const int idx = base + lane;
+        bool sel = false, self = false;
+        int cpp = 0, cpc = 0;
+        SrcRange r{0, 0, 0, 0};
+        if (idx < T) {
+          int q = 0;
+          while (sbeg[wid][q + 1] <= idx) ++q;
+          const int node = spath[wid][q];
+          const int4 it = E[sorted_e[seg[2 * node].x + (idx - sbeg[wid][q])]];
+          const bool nr = it.z == 0 && near_possible(leaf, it.y, center, radius);
+          sel = nr == (pass == 0);
+          if (sel) {
+            if (it.z == 0) {
+              r.begin = off[it.y];
+              r.count = cnt[it.y];
+              r.near = nr ? 1 : 0;
+              self = r.begin <= offl && offl < r.begin + r.count;  // holds the leaf's own particles
+              cpp = r.count;
+            } else {
+              r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
+              r.count = P;
+              cpc = P;
+            }
+          }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, sel);
+        int incl = cpp + cpc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        if (sel) {
+          r.pad = src + incl - (cpp + cpc);  // flattened-list prefix
+          ranges[w0 + w + __popc(bal & ((1u << lane) - 1u))] = r;
+        }
+        const unsigned sb = __ballot_sync(0xffffffffu, self);
+        if (sb) {
+          const int sl = __ffs(sb) - 1;
+          self_shift = __shfl_sync(0xffffffffu, r.pad - r.begin, sl);
+          has_self = 1;
+        }
+        w += __popc(bal);
+        src += __shfl_sync(0xffffffffu, incl, 31);
+        src_pp += __reduce_add_sync(0xffffffffu, cpp);
+        src_pc += __reduce_add_sync(0xffffffffu, cpc);
+      }
+      if (pass == 0) near_total = src;
     }
     const int c = cnt[leaf];
     const int nt = (c + kTileTargets - 1) / kTileTargets;
-    for (int j = 0; j < nt; ++j) {
+    for (int j = lane; j < nt; j += 32) {
       Tile t;
-      t.tgt_begin = off[leaf] + j * kTileTargets;
+      t.tgt_begin = offl + j * kTileTargets;
       t.tgt_count = min(kTileTargets, c - j * kTileTargets);
       t.list_begin = w0;
-      t.list_end = w;
+      t.list_end = w0 + w;
       t.near_total = near_total;
       t.self_shift = self_shift;
       t.has_self = has_self;
@@ -315,10 +358,12 @@ __global__ void k_leaf_fill(const int* __restrict__ leaves, int nl, const int* _
       const unsigned long long tc = static_cast<unsigned long long>(t.tgt_count);
       tile_cost[tile_off[k] + j] = make_ulonglong2(tc * src_pp - tc, tc * src_pc);  // self pairs excluded
     }
-    pp = static_cast<unsigned long long>(c) * src_pp - static_cast<unsigned long long>(c);  // self pairs excluded
-    pc = static_cast<unsigned long long>(c) * src_pc;
+    if (lane == 0) {
+      pp = static_cast<unsigned long long>(c) * src_pp - static_cast<unsigned long long>(c);  // self pairs excluded
+      pc = static_cast<unsigned long long>(c) * src_pc;
+    }
   }
-  typedef cub::BlockReduce<unsigned long long, 128> BR;
+  typedef cub::BlockReduce<unsigned long long, 32 * kFillWarps> BR;
   __shared__ typename BR::TempStorage tmp;
   const unsigned long long spp = BR(tmp).Sum(pp);
   __syncthreads();
@@ -336,48 +381,68 @@ __global__ void k_fit_count(const int* __restrict__ fit_nodes, int nf, const int
   n_ranges[k] = sg.y - sg.x;
 }
 
-__global__ void k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2* __restrict__ seg,
-                           const int* __restrict__ sorted_e, const int4* __restrict__ E, const int* __restrict__ cnt,
-                           const int* __restrict__ off, const int* __restrict__ pslot,
-                           const int* __restrict__ range_off, int64_t N, int P, SrcRange* __restrict__ ranges,
-                           Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
-                           unsigned long long* __restrict__ evals) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// Range list of one fit node (its CP / CC entries in emission order,
+// treecode.cpp:341-358), one warp per node as in k_leaf_fill.
+__global__ void __launch_bounds__(32 * kFillWarps)
+    k_fit_fill(const int* __restrict__ fit_nodes, int nf, const int2* __restrict__ seg,
+               const int* __restrict__ sorted_e, const int4* __restrict__ E, const int* __restrict__ cnt,
+               const int* __restrict__ off, const int* __restrict__ pslot, const int* __restrict__ range_off,
+               int64_t N, int P, SrcRange* __restrict__ ranges, Tile* __restrict__ tiles,
+               ulonglong2* __restrict__ tile_cost, unsigned long long* __restrict__ evals) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kFillWarps + (threadIdx.x >> 5);
   unsigned long long cp = 0, cc = 0;
-  if (k < nf) {
+  if (k < nf) {  // warp-uniform
     const int t = fit_nodes[k];
     const int2 sg = seg[2 * t + 1];
-    int w = range_off[k];
-    const int w0 = w;
-    int pre = 0;
-    for (int i = sg.x; i < sg.y; ++i) {  // emission order (treecode.cpp:347)
-      const int4 it = E[sorted_e[i]];
-      SrcRange r;
-      r.pad = pre;  // flattened-list prefix
-      if (it.z == 2) {
-        r.begin = off[it.y];
-        r.count = cnt[it.y];
-        cp += static_cast<unsigned long long>(P) * static_cast<unsigned long long>(r.count);
-      } else {
-        r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
-        r.count = P;
-        cc += static_cast<unsigned long long>(P) * static_cast<unsigned long long>(P);
+    const int w0 = range_off[k];
+    int pre = 0, ncp = 0, ncc = 0;
+    for (int base = sg.x; base < sg.y; base += 32) {
+      const int i = base + lane;
+      int cv = 0, is_cp = 0, is_cc = 0;
+      SrcRange r{0, 0, 0, 0};
+      if (i < sg.y) {
+        const int4 it = E[sorted_e[i]];
+        if (it.z == 2) {
+          r.begin = off[it.y];
+          r.count = cnt[it.y];
+          is_cp = r.count;
+        } else {
+          r.begin = static_cast<int>(N + static_cast<int64_t>(pslot[it.y]) * P);
+          r.count = P;
+          is_cc = 1;
+        }
+        cv = r.count;
       }
-      r.near = 0;
-      pre += r.count;
-      ranges[w++] = r;
+      int incl = cv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (i < sg.y) {
+        r.pad = pre + incl - cv;  // flattened-list prefix
+        ranges[w0 + (i - sg.x)] = r;
+      }
+      pre += __shfl_sync(0xffffffffu, incl, 31);
+      ncp += __reduce_add_sync(0xffffffffu, is_cp);
+      ncc += __reduce_add_sync(0xffffffffu, is_cc);
     }
-    Tile tl;
-    tl.tgt_begin = static_cast<int>(N + static_cast<int64_t>(pslot[t]) * P);
-    tl.tgt_count = P;
-    tl.list_begin = w0;
-    tl.list_end = w;
-    tl.near_total = 0;  // CP / CC pairs are well separated
-    tl.self_shift = tl.has_self = tl.pad = 0;
-    tiles[k] = tl;
-    tile_cost[k] = make_ulonglong2(cp, cc);
+    if (lane == 0) {
+      Tile tl;
+      tl.tgt_begin = static_cast<int>(N + static_cast<int64_t>(pslot[t]) * P);
+      tl.tgt_count = P;
+      tl.list_begin = w0;
+      tl.list_end = w0 + (sg.y - sg.x);
+      tl.near_total = 0;  // CP / CC pairs are well separated
+      tl.self_shift = tl.has_self = tl.pad = 0;
+      tiles[k] = tl;
+      cp = static_cast<unsigned long long>(P) * static_cast<unsigned long long>(ncp);
+      cc = static_cast<unsigned long long>(P) * static_cast<unsigned long long>(P) * static_cast<unsigned long long>(ncc);
+      tile_cost[k] = make_ulonglong2(cp, cc);
+    }
   }
-  typedef cub::BlockReduce<unsigned long long, 128> BR;
+  typedef cub::BlockReduce<unsigned long long, 32 * kFillWarps> BR;
   __shared__ typename BR::TempStorage tmp;
   const unsigned long long scp = BR(tmp).Sum(cp);
   __syncthreads();
@@ -661,7 +726,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   L.leaf_ranges.ensure(size_t(std::max<int64_t>(L.n_leaf_ranges, 1)));
   L.leaf_tiles.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
   L.leaf_cost.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
-  k_leaf_fill<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
+  k_leaf_fill<<<grid_for(nl, kFillWarps), 32 * kFillWarps, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
                                                         L.inter.p, B.cnt.p, B.off.p, L.pslot.p, c.nodes.center.p,
                                                         c.nodes.radius.p, S.nr_off.p, S.nt_off.p, N, P,
                                                         L.leaf_ranges.p, L.leaf_tiles.p, L.leaf_cost.p,
@@ -674,7 +739,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     L.fit_ranges.ensure(size_t(std::max<int64_t>(L.n_fit_ranges, 1)));
     L.fit_tiles.ensure(size_t(nf));
     L.fit_cost.ensure(size_t(nf));
-    k_fit_fill<<<grid_for(nf, 128), 128, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.sorted_e.p, L.inter.p, B.cnt.p,
+    k_fit_fill<<<grid_for(nf, kFillWarps), 32 * kFillWarps, 0, c.stream>>>(L.fit_nodes.p, nf, S.seg.p, S.sorted_e.p, L.inter.p, B.cnt.p,
                                                          B.off.p, L.pslot.p, S.fnr_off.p, N, P, L.fit_ranges.p,
                                                          L.fit_tiles.p, L.fit_cost.p, S.counters.p + 4);
     SSUM_LAUNCH_CHECK();
