@@ -267,6 +267,12 @@ int ssum_create(int device, ssum_ctx** out) {
     SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     for (auto& e : c->ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
+    SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : c->io.xyz) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->io.out) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->io.q, cudaEventDisableTiming));
+    SSUM_CUDA_CHECK(cudaEventCreate(&c->io.t0));
+    SSUM_CUDA_CHECK(cudaEventCreate(&c->io.t1));
     c->d_flags.ensure(64);
     SSUM_CUDA_CHECK(cudaMemset(c->d_flags.p, 0, 64 * sizeof(int)));
     tree_init_roots(*c);
@@ -296,6 +302,12 @@ void ssum_destroy(ssum_ctx* h) {
   c->out_buf.release();
   c->rk_state.release();
   for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->io.xyz) if (e) cudaEventDestroy(e);
+  for (auto& e : c->io.out) if (e) cudaEventDestroy(e);
+  if (c->io.q) cudaEventDestroy(c->io.q);
+  if (c->io.t0) cudaEventDestroy(c->io.t0);
+  if (c->io.t1) cudaEventDestroy(c->io.t1);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);
@@ -354,6 +366,12 @@ int ssum_treecode_sum_device(ssum_ctx* h, int kernel, const ssum_config* cfg, co
   });
 }
 
+// Host buffers in and out, with the copies overlapped with the work: xyz
+// travels in kIoChunks pieces on copy_stream (the tree walk starts on each as
+// it lands), then q (waited for at the gather); the result comes back piece by
+// piece behind the downward pass (eval.cu). h2d/d2h_seconds: device time from
+// the first input byte to the last, and from the first result piece to the
+// last.
 int ssum_treecode_sum(ssum_ctx* h, int kernel, const ssum_config* cfg, const double* xyz, const double* q,
                       int64_t n, double* out, ssum_stats* st) {
   return guarded(h, [&](Ctx& c) {
@@ -361,11 +379,39 @@ int ssum_treecode_sum(ssum_ctx* h, int kernel, const ssum_config* cfg, const dou
     check_kernel(kernel);
     check_n(n);
     const int D = kernel == SSUM_BIOT_SAVART ? 3 : 1;
-    upload(c, c.in_xyz, xyz, size_t(n) * 3, st);
-    upload(c, c.in_q, q, size_t(n), st);
+    c.in_xyz.ensure(std::max<size_t>(size_t(n) * 3, 1));
+    c.in_q.ensure(std::max<size_t>(size_t(n), 1));
     c.out_buf.ensure(std::max<size_t>(size_t(n) * D, 1));
+    Ctx::HostIo& io = c.io;
+    struct Reset {  // the staged mode, and copies into the caller's buffers, never outlive this call
+      Ctx& c;
+      ~Reset() {
+        cudaStreamSynchronize(c.copy_stream);
+        c.io.active = false, c.io.h_out = nullptr;
+      }
+    } reset{c};
+    // the copy stream must not overwrite inputs still read by earlier work
+    SSUM_CUDA_CHECK(cudaEventRecord(io.t0, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, io.t0, 0));
+    for (int j = 0; j <= Ctx::kIoChunks; ++j) io.bounds[j] = n * j / Ctx::kIoChunks;
+    for (int j = 0; j < Ctx::kIoChunks; ++j) {
+      const int64_t a = io.bounds[j], b = io.bounds[j + 1];
+      if (b > a)
+        SSUM_CUDA_CHECK(cudaMemcpyAsync(c.in_xyz.p + 3 * a, xyz + 3 * a, size_t(b - a) * 24, cudaMemcpyHostToDevice,
+                                        c.copy_stream));
+      SSUM_CUDA_CHECK(cudaEventRecord(io.xyz[j], c.copy_stream));
+    }
+    if (n) SSUM_CUDA_CHECK(cudaMemcpyAsync(c.in_q.p, q, size_t(n) * 8, cudaMemcpyHostToDevice, c.copy_stream));
+    SSUM_CUDA_CHECK(cudaEventRecord(io.q, c.copy_stream));
+    io.active = true;
+    io.h_out = out;
+    io.dim = D;
     treecode_device(c, kernel, *cfg, c.in_xyz.p, c.in_q.p, n, c.out_buf.p, st);
-    download(c, out, c.out_buf.p, size_t(n) * D, st);
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));
+    if (st) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, io.t0, io.t1) == cudaSuccess) st->d2h_seconds += ms * 1e-3;
+    }
   });
 }
 

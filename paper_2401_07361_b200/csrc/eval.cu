@@ -205,11 +205,24 @@ __global__ void k_finish(int64_t p0, int64_t p1, const double4* __restrict__ pts
                          const int* __restrict__ pos_leaf, const int* __restrict__ parent,
                          const int* __restrict__ pslot, const unsigned char* __restrict__ is_fit,
                          const double* __restrict__ cramer, const double* __restrict__ coeff,
-                         const int* __restrict__ perm, double* __restrict__ out) {
+                         const int* __restrict__ perm, double* __restrict__ out, const int* __restrict__ inv,
+                         int64_t i0, int64_t i1) {
   constexpr int D = KDim<KER>::D;
   constexpr int P = Sbb<DEG>::P;
-  const int64_t k = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= p1) return;
+  // thread -> tree position k (and original id o): in tree order over
+  // [p0, p1), or, with inv, in original order over [i0, i1) (one piece of
+  // the host result), skipping positions outside this part
+  int64_t k, o;
+  if (inv) {
+    o = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (o >= i1) return;
+    k = inv[o];
+    if (k < p0 || k >= p1) return;
+  } else {
+    k = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= p1) return;
+    o = perm[k];
+  }
   const double4 x = pts[k];
   double val[D];
 #pragma unroll
@@ -232,7 +245,6 @@ __global__ void k_finish(int64_t p0, int64_t p1, const double4* __restrict__ pts
       }
     }
   }
-  const int o = perm[k];
   if constexpr (KER == kBS) {
     const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
     const double pref = -kInv4Pi;  // BiotSavartKernel::prefactor (kernels.hpp:54)
@@ -244,18 +256,24 @@ __global__ void k_finish(int64_t p0, int64_t p1, const double4* __restrict__ pts
   }
 }
 
+__global__ void k_inv_perm(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) inv[perm[k]] = static_cast<int>(k);
+}
+
 template <int KER>
-void launch_finish(Ctx& c, int degree, double* d_out) {
+void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, int64_t i0 = 0, int64_t i1 = 0) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   const int bs = 128;
-  const int64_t n = L.p1 - L.p0;
+  const int64_t n = inv ? i1 - i0 : L.p1 - L.p0;
   if (n <= 0) return;
 #define SSUM_FINISH_CASE(DG)                                                                                   \
   case DG:                                                                                                    \
     k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p,          \
                                                              c.nodes.parent.p, L.pslot.p, L.is_fit.p,         \
-                                                             c.nodes.cramer.p, c.coeff.p, B.perm.p, d_out);   \
+                                                             c.nodes.cramer.p, c.coeff.p, B.perm.p, d_out,    \
+                                                             inv, i0, i1);                                    \
     break;
   switch (degree) {
     SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
@@ -392,6 +410,7 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   c.coeff.ensure(std::max<size_t>(size_t(L.n_proxy) * D * P, 1));
   const int bs = 256;
 
+  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.q, 0));  // q of a host-pointer call
   cudaEventRecord(c.ev[0], c.stream);
   k_gather<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
   SSUM_LAUNCH_CHECK();
@@ -458,10 +477,32 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   cudaEventRecord(c.ev[4], c.stream);
 
   // ---- downward + finish
-  if (kernel == kBS)
+  if (c.io.active && c.io.h_out) {
+    // host result: finish in original order, piece by piece, each piece's
+    // copy to the host overlapping the next piece's finish
+    c.inv_perm.ensure(size_t(n));
+    k_inv_perm<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, c.inv_perm.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    for (int j = 0; j < Ctx::kIoChunks; ++j) {
+      const int64_t a = c.io.bounds[j], b = c.io.bounds[j + 1];
+      if (kernel == kBS)
+        launch_finish<kBS>(c, degree, d_out, c.inv_perm.p, a, b);
+      else
+        launch_finish<kLOG>(c, degree, d_out, c.inv_perm.p, a, b);
+      SSUM_CUDA_CHECK(cudaEventRecord(c.io.out[j], c.stream));
+      SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, c.io.out[j], 0));
+      if (j == 0) SSUM_CUDA_CHECK(cudaEventRecord(c.io.t0, c.copy_stream));
+      if (b > a)
+        SSUM_CUDA_CHECK(cudaMemcpyAsync(c.io.h_out + a * D, d_out + a * D, size_t(b - a) * D * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c.copy_stream));
+    }
+    SSUM_CUDA_CHECK(cudaEventRecord(c.io.t1, c.copy_stream));
+  } else if (kernel == kBS) {
     launch_finish<kBS>(c, degree, d_out);
-  else
+  } else {
     launch_finish<kLOG>(c, degree, d_out);
+  }
   cudaEventRecord(c.ev[5], c.stream);
   check_flags(c, "treecode_sum");
   if (st) {

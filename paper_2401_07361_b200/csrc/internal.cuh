@@ -233,6 +233,20 @@ struct Ctx {
   double* h_stage = nullptr;         // pinned staging
   size_t h_stage_bytes = 0;
   cudaEvent_t ev[8];
+  // Host-pointer entry (ssum_treecode_sum): the inputs travel on copy_stream
+  // in kIoChunks pieces (the tree walk starts on each piece as it lands, q is
+  // waited for only at the gather) and the result leaves in pieces as the
+  // downward pass finishes them (eval.cu).
+  static constexpr int kIoChunks = 4;
+  cudaStream_t copy_stream = nullptr;
+  struct HostIo {
+    bool active = false;
+    int64_t bounds[kIoChunks + 1] = {};  // particle ranges of the pieces
+    cudaEvent_t xyz[kIoChunks] = {}, q = nullptr, out[kIoChunks] = {}, t0 = nullptr, t1 = nullptr;
+    double* h_out = nullptr;           // result destination (original order), nullptr: none
+    int dim = 0;
+  } io;
+  DBuf<int> inv_perm;                // original particle id -> tree position
 };
 
 // Host-side phase trace (SSUM_TRACE=1): wall time between marks, printed by

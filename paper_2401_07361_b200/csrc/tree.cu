@@ -250,7 +250,7 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
 // are two binary searches of the node's key range in the sorted keys. The
 // binning is final unless a childless node must split (bin > N_T below
 // max_depth) — then the level-synchronous build runs instead.
-__global__ void k_walk(const double* __restrict__ xyz, int64_t n, const double* __restrict__ tri,
+__global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const double* __restrict__ tri,
                        const double* __restrict__ cramer, const double* __restrict__ center,
                        const int* __restrict__ child_base, const unsigned long long* __restrict__ nkey,
                        unsigned long long* __restrict__ key, int* __restrict__ ids, int* __restrict__ leaf_of,
@@ -262,8 +262,8 @@ __global__ void k_walk(const double* __restrict__ xyz, int64_t n, const double* 
   for (int k = threadIdx.x; k < 240; k += blockDim.x) skr[k] = cramer[k];
   for (int k = threadIdx.x; k < 60; k += blockDim.x) sc[k] = center[k];
   __syncthreads();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   const d3 p = load3(xyz + 3 * i);
   int node = find_root(p, st, skr, sc);
   if (node < 0) {
@@ -481,9 +481,16 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   B.leaf_flag.ensure(size_t(n));
   int* d_cnt = c.d_flags.p + 16;  // [0] splits needed, [1] leaves
   SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(int), c.stream));
-  k_walk<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, n, T.tri.p, T.cramer.p, T.center.p, T.child_base.p, T.key.p,
-                                               B.wkey.p, B.sort_vals.p, B.leaf_of.p, c.d_flags.p);
-  SSUM_LAUNCH_CHECK();
+  // host-pointer calls: walk each input piece as soon as it has landed
+  const int pieces = c.io.active ? Ctx::kIoChunks : 1;
+  for (int j = 0; j < pieces; ++j) {
+    const int64_t a = c.io.active ? c.io.bounds[j] : 0, b = c.io.active ? c.io.bounds[j + 1] : n;
+    if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[j], 0));
+    if (b <= a) continue;
+    k_walk<<<grid_for(b - a, bs), bs, 0, c.stream>>>(d_xyz, a, b, T.tri.p, T.cramer.p, T.center.p, T.child_base.p,
+                                                     T.key.p, B.wkey.p, B.sort_vals.p, B.leaf_of.p, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+  }
   const int begin_bit = kKeyRootShift - 2 * T.max_level;
   size_t tmp = 0;
   SSUM_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, B.wkey.p, B.wkey2.p, B.sort_vals.p, B.perm.p, ni,
@@ -540,7 +547,8 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
     return;
   }
   // level-synchronous build from the roots (fresh counts again: the reuse
-  // attempt may have filled them)
+  // attempt may have filled them); needs the whole input
+  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[Ctx::kIoChunks - 1], 0));
   SSUM_CUDA_CHECK(cudaMemsetAsync(B.cnt.p, 0, size_t(c.nodes.count) * sizeof(int), c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(B.is_leaf.p, 0, size_t(c.nodes.count), c.stream));
 
