@@ -190,14 +190,15 @@ struct TravScratch {
   DBuf<int> nr, nt, nr_off, nt_off, fnr, fnr_off;
   DBuf<unsigned long long> counters;  // [0..3] kinds, [4..7] kernel evals
   unsigned long long* h_small = nullptr;  // pinned: [0..7] scratch, [8..15] counters read-back
-  // planned traversal (traversal.cu bfs_planned): the last call's frontier
-  // size per step and emission count size the next call's steps
+  // single-launch traversal (traversal.cu bfs_persistent): the last call's
+  // frontier sizes and emission count size the next call's buffers
   std::vector<int> plan_m;
   long long plan_ne = 0;
   bool plan_valid = false;
-  DBuf<int> dm;              // device-side frontier size per step
-  DBuf<long long> debase;    // device-side emission base per step
-  long long* h_plan = nullptr;  // pinned read-back of the step sizes
+  int bfs_blocks = 0;        // cooperative grid size (0: not queried, -1: unavailable)
+  DBuf<int> dm;              // k_bfs results: steps, overflow, largest frontier
+  DBuf<long long> debase;    // k_bfs result: emission count
+  long long* h_plan = nullptr;  // pinned read-back
 };
 
 struct Ctx {

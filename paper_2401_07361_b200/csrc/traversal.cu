@@ -20,6 +20,7 @@
 //     (particles) and CC ranges (proxy points) — treecode.cpp:341-358;
 //   * proxy slots for every node that needs proxy points (PC/CC sources carry
 //     weights, CP/CC targets carry fit coefficients) — treecode.cpp:289-324.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -48,6 +49,59 @@ __device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_o
 }
 
 // action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
+__device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__ cnt,
+                                           const double* __restrict__ center, const double* __restrict__ radius,
+                                           const int* __restrict__ level, const int* __restrict__ child_base,
+                                           double theta, int thr, int max_depth, int pc_only) {
+  const int ct = cnt[t], cs = cnt[s];
+  int a = 0;
+  if (ct > 0 && cs > 0) {
+    const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
+    const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
+    const double R = arc_dist(a3, b3);
+    if (R > 0.0 && div_rn(add_rn(radius[t], radius[s]), R) < theta) {
+      a = 4 | classify_kind(ct, cs, thr, pc_only);
+    } else if (ct <= thr && cs <= thr) {
+      a = 4;  // PP
+    } else {
+      const bool rt = ct > cs;
+      const int r = rt ? t : s;
+      if (child_base[r] < 0 || level[r] >= max_depth)
+        a = 4;  // PP fallback
+      else
+        a = 8 | (rt ? 16 : 0);
+    }
+  }
+  return a;
+}
+
+// Emission / refinement of frontier entry p with action a at exclusive
+// prefix pos = (emissions before << 32) | (children slots before).
+__device__ __forceinline__ void pair_scatter(const PairEntry& p, int a, unsigned long long pos, long long e_base,
+                                             const int* __restrict__ child_base, PairEntry* __restrict__ Fnext,
+                                             int4* __restrict__ E, unsigned long long* __restrict__ K, int* flags) {
+  if (a & 4) {
+    const long long e = e_base + static_cast<long long>(pos >> 32);
+    E[e] = int4{p.t, p.s, a & 3, 0};
+    K[e] = p.key;
+  } else {
+    const int o = static_cast<int>(pos & 0xffffffffull);
+    const bool rt = (a & 16) != 0;
+    const int cb = child_base[rt ? p.t : p.s];
+    const int step = p.step + 1;
+    if (step > kKeyMaxSteps) atomicOr(flags, 4);  // order keys saturated (export only)
+    const int shift = 54 - kKeyStepBits * min(step, kKeyMaxSteps);
+    for (int q = 0; q < 4; ++q) {
+      PairEntry c;
+      c.t = rt ? cb + q : p.t;
+      c.s = rt ? p.s : cb + q;
+      c.key = p.key | (static_cast<unsigned long long>(q) << shift);
+      c.step = step;
+      c.pad = 0;
+      Fnext[o + q] = c;
+    }
+  }
+}
 // Frontier size: *d_m when the size lives on the device (planned traversal,
 // grid sized for `bound`), else `bound` itself. A device size above the bound
 // sets *ovf and is clamped (the planned traversal is then redone).
@@ -73,26 +127,7 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, const int* __restri
     packed[k] = 0;
     return;
   }
-  const int t = F[k].t, s = F[k].s;
-  const int ct = cnt[t], cs = cnt[s];
-  int a = 0;
-  if (ct > 0 && cs > 0) {
-    const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
-    const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
-    const double R = arc_dist(a3, b3);
-    if (R > 0.0 && div_rn(add_rn(radius[t], radius[s]), R) < theta) {
-      a = 4 | classify_kind(ct, cs, thr, pc_only);
-    } else if (ct <= thr && cs <= thr) {
-      a = 4;  // PP
-    } else {
-      const bool rt = ct > cs;
-      const int r = rt ? t : s;
-      if (child_base[r] < 0 || level[r] >= max_depth)
-        a = 4;  // PP fallback
-      else
-        a = 8 | (rt ? 16 : 0);
-    }
-  }
+  const int a = pair_action(F[k].t, F[k].s, cnt, center, radius, level, child_base, theta, thr, max_depth, pc_only);
   action[k] = a;
   const unsigned long long emit = (a & 4) ? 1ull : 0ull;
   const unsigned long long kids = (a & 8) ? 4ull : 0ull;
@@ -163,6 +198,104 @@ __global__ void k_root_pairs(PairEntry* F, int* d_m0, long long* d_ebase0, int* 
   p.step = 0;
   p.pad = 0;
   F[k] = p;
+}
+
+// The whole breadth-first traversal in one cooperative launch (all blocks
+// resident): per step, each block takes a contiguous slice of the frontier,
+// decides every pair (pair_action) and scans its slice; after a grid barrier
+// every block reads all block totals (its base = the totals of the blocks
+// before it, so emissions and children keep frontier order exactly as the
+// step-by-step version) and scatters; a second barrier hands the next
+// frontier over. Capacities come from the previous call; a step that would
+// exceed them stops the walk with out[1] = 1 (the caller then redoes the
+// traversal step by step). out: [0] steps, [1] overflow, [2] largest frontier.
+constexpr int kBfsThreads = 256;
+#ifndef SSUM_BFS_MINB
+#define SSUM_BFS_MINB 1
+#endif
+__global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
+    k_bfs(const int* __restrict__ cnt, const double* __restrict__ center, const double* __restrict__ radius,
+          const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr, int max_depth,
+          int pc_only, PairEntry* F0, PairEntry* F1, int fcap, int4* __restrict__ E,
+          unsigned long long* __restrict__ K, long long ecap, int* __restrict__ action,
+          unsigned long long* __restrict__ loc, unsigned long long* btot, int* out, long long* ne_out,
+          int* flags) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  typedef cub::BlockScan<unsigned long long, kBfsThreads> BS;
+  typedef cub::BlockReduce<unsigned long long, kBfsThreads> BR;
+  __shared__ union {
+    typename BS::TempStorage scan;
+    typename BR::TempStorage red;
+  } tmp;
+  const int nb = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  PairEntry* Fc = F0;
+  PairEntry* Fn = F1;
+  int m = 400, fmax = 400;
+  long long e_base = 0;
+  for (int step = 0;; ++step) {
+    const int per = (m + nb - 1) / nb;
+    const int lo = min(m, b * per), hi = min(m, lo + per);
+    unsigned long long run = 0;  // (emissions << 32) | child slots, this block so far
+    for (int base = lo; base < hi; base += kBfsThreads) {
+      const int k = base + tid;
+      unsigned long long v = 0;
+      if (k < hi) {
+        const int a = pair_action(Fc[k].t, Fc[k].s, cnt, center, radius, level, child_base, theta, thr,
+                                  max_depth, pc_only);
+        action[k] = a;
+        v = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
+      }
+      unsigned long long ex, agg;
+      BS(tmp.scan).ExclusiveSum(v, ex, agg);
+      __syncthreads();
+      if (k < hi) loc[k] = run + ex;
+      run += agg;
+    }
+    if (tid == 0) btot[b] = run;
+    grid.sync();
+    unsigned long long below = 0, all = 0;
+    for (int i = tid; i < nb; i += kBfsThreads) {
+      const unsigned long long t = btot[i];
+      all += t;
+      if (i < b) below += t;
+    }
+    below = BR(tmp.red).Sum(below);
+    __syncthreads();
+    all = BR(tmp.red).Sum(all);
+    __shared__ unsigned long long s_below, s_all;
+    if (tid == 0) {
+      s_below = below;
+      s_all = all;
+    }
+    __syncthreads();
+    below = s_below;
+    all = s_all;
+    const int next = static_cast<int>(all & 0xffffffffull);
+    const long long emitted = static_cast<long long>(all >> 32);
+    const bool ovf = next > fcap || e_base + emitted > ecap;
+    if (!ovf)
+      for (int k = lo + tid; k < hi; k += kBfsThreads) {
+        const int a = action[k];
+        if (a) pair_scatter(Fc[k], a, below + loc[k], e_base, child_base, Fn, E, K, flags);
+      }
+    e_base += emitted;
+    if (ovf || next == 0) {
+      if (b == 0 && tid == 0) {
+        out[0] = step + 1;
+        out[1] = ovf ? 1 : 0;
+        out[2] = fmax;
+        *ne_out = e_base;
+      }
+      break;
+    }
+    fmax = max(fmax, next);
+    grid.sync();  // the next frontier is complete, and btot is free again
+    PairEntry* t = Fc;
+    Fc = Fn;
+    Fn = t;
+    m = next;
+  }
 }
 
 // Node flags from the emitted list (treecode.cpp:295-317).
@@ -517,59 +650,71 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
   return ne;
 }
 
-// The same traversal with no host read between steps: every step's grid and
-// buffers are sized from the previous call's step sizes (plus slack), the
-// true sizes stay on the device, and one read at the end checks that no step
-// outgrew its bound (else false: the caller redoes it synchronously).
-static bool bfs_planned(Ctx& c, const ssum_config& cfg, long long& ne_out) {
+// The traversal as one cooperative kernel (k_bfs), sized from the previous
+// call's largest frontier and emission count (plus slack); one read-back at
+// the end. False (nothing committed) when there is no previous call, the
+// launch is refused, or a step outgrew the capacities: the caller then runs
+// the step-by-step traversal, which also refreshes the sizes.
+static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   TravScratch& S = c.trav;
-  if (!S.plan_valid || S.plan_m.empty() || S.plan_m.size() > 200) return false;
-  const int bs = 256;
-  const int steps = static_cast<int>(S.plan_m.size());
-  std::vector<int> mb(size_t(steps) + 1);
-  for (int s = 0; s < steps; ++s) mb[s] = s == 0 ? 400 : S.plan_m[s] + S.plan_m[s] / 8 + 256;
-  mb[steps] = 256;  // the frontier after the last planned step must be empty
-  const int fmax = *std::max_element(mb.begin(), mb.end());
-  const long long ecap = S.plan_ne + S.plan_ne / 8 + 4096;
-  S.F0.ensure(size_t(fmax));
-  S.F1.ensure(size_t(fmax));
-  S.action.ensure(size_t(fmax) + 1);
-  S.packed.ensure(size_t(fmax) + 1);
-  S.scan.ensure(size_t(fmax) + 1);
+  if (!S.plan_valid || S.plan_m.empty()) return false;
+  if (S.bfs_blocks == 0) {
+    int per_sm = 0, sms = 0;
+    SSUM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, kBfsThreads, 0));
+    SSUM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+#ifndef SSUM_BFS_PER_SM
+#define SSUM_BFS_PER_SM 4
+#endif
+    S.bfs_blocks = sms * std::min(per_sm, SSUM_BFS_PER_SM);
+    if (S.bfs_blocks <= 0) S.bfs_blocks = -1;
+  }
+  if (S.bfs_blocks < 0) return false;
+  const int nb = S.bfs_blocks;
+  const int fplan = *std::max_element(S.plan_m.begin(), S.plan_m.end());
+  int fcap = fplan + fplan / 8 + 1024;
+  long long ecap = S.plan_ne + S.plan_ne / 8 + 4096;
+  S.F0.ensure(size_t(fcap));
+  S.F1.ensure(size_t(fcap));
+  S.action.ensure(size_t(fcap));
+  S.packed.ensure(size_t(fcap));
+  S.scan.ensure(size_t(nb));
+  S.dm.ensure(4);
+  S.debase.ensure(1);
   L.inter.ensure(size_t(ecap));
   L.key.ensure(size_t(ecap));
-  S.dm.ensure(size_t(steps) + 1);
-  S.debase.ensure(size_t(steps) + 1);
   if (!S.h_plan) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_plan, 256 * sizeof(long long)));
-  int* ovf = c.d_flags.p + 24;
-  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, S.dm.p, S.debase.p, ovf);
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, nullptr, nullptr, nullptr);
   SSUM_LAUNCH_CHECK();
-  c.launches++;
-  for (int s = 0; s < steps; ++s) {
-    k_trav_eval<<<grid_for(mb[s] + 1, bs), bs, 0, c.stream>>>(S.F0.p, S.dm.p + s, mb[s], B.cnt.p, c.nodes.center.p,
-                                                                c.nodes.radius.p, c.nodes.level.p,
-                                                                c.nodes.child_base.p, cfg.theta, cfg.n_threshold,
-                                                                cfg.max_depth, cfg.pc_only, S.action.p, S.packed.p,
-                                                                ovf);
-    SSUM_LAUNCH_CHECK();
-    exclusive_scan(c, S.packed.p, S.scan.p, mb[s] + 1);
-    k_trav_scatter<<<grid_for(std::max(mb[s], 1), bs), bs, 0, c.stream>>>(
-        S.F0.p, S.dm.p + s, mb[s], S.action.p, S.scan.p, c.nodes.child_base.p, S.F1.p, mb[s + 1], L.inter.p,
-        L.key.p, ecap, 0, S.debase.p + s, S.dm.p + s + 1, c.d_flags.p, ovf);
-    SSUM_LAUNCH_CHECK();
-    c.launches += 2;
-    std::swap(S.F0, S.F1);
+  const int* cnt = B.cnt.p;
+  const double *center = c.nodes.center.p, *radius = c.nodes.radius.p;
+  const int *level = c.nodes.level.p, *child_base = c.nodes.child_base.p;
+  double theta = cfg.theta;
+  int thr = cfg.n_threshold, max_depth = cfg.max_depth, pc_only = cfg.pc_only;
+  PairEntry *f0 = S.F0.p, *f1 = S.F1.p;
+  int4* e = L.inter.p;
+  unsigned long long* k = L.key.p;
+  int* action = S.action.p;
+  unsigned long long *loc = S.packed.p, *btot = S.scan.p;
+  int* out = S.dm.p;
+  long long* ne = S.debase.p;
+  int* flags = c.d_flags.p;
+  void* args[] = {&cnt, &center, &radius, &level, &child_base, &theta, &thr, &max_depth, &pc_only, &f0, &f1,
+                  &fcap, &e, &k, &ecap, &action, &loc, &btot, &out, &ne, &flags};
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs), dim3(nb), dim3(kBfsThreads), args, 0, c.stream) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    S.bfs_blocks = -1;  // no cooperative launch here: step by step from now on
+    return false;
   }
+  c.launches += 2;
   int* h = reinterpret_cast<int*>(S.h_plan);
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, ovf, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(h + 1, S.dm.p, (size_t(steps) + 1) * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_plan + 128, S.debase.p + steps, sizeof(long long), cudaMemcpyDeviceToHost,
-                                  c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, S.dm.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_plan + 128, S.debase.p, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-  if (h[0] != 0 || h[1 + steps] != 0) return false;
-  for (int s = 0; s < steps; ++s) S.plan_m[s] = h[1 + s];
+  if (h[1] != 0) return false;
+  S.plan_m.assign(1, h[2]);
   S.plan_ne = S.h_plan[128];
   ne_out = S.plan_ne;
   return true;
@@ -590,7 +735,7 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
   // ---- breadth-first traversal
   long long ne = 0;
   if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
-  if (!bfs_planned(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+  if (!bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
   L.n_inter = ne;
   trace().mark("trav.bfs");
   build_lists(c, cfg);

@@ -54,6 +54,10 @@ def test_interaction_list_bit_identical(ss, ol, mesh_fixture, level, nt, theta):
     mine = ss.dual_traversal_array(t, cfg(ss, theta=theta, nt=nt, deg=4))
     ref = r.traversal(theta, nt, 4, 10)
     assert np.array_equal(mine, ref)
+    # a second traversal on the same context runs as one cooperative kernel
+    # sized from the first: same list, same order
+    again = ss.dual_traversal_array(t, cfg(ss, theta=theta, nt=nt, deg=4))
+    assert np.array_equal(again, ref)
 
 
 def test_interaction_objects(ss, ol, mesh_fixture):
