@@ -154,6 +154,20 @@ int ssum_tree_perm(ssum_ctx* ctx, int* dst, int on_device);
 int ssum_rk4(ssum_ctx* ctx, const ssum_config* cfg, double* xyz, double* zeta,
              const double* area, int64_t n, double dt, int steps, double omega, int direct,
              ssum_stats* stats);
+/* The pieces of one ssum_rk4 step on device arrays, for drivers that
+ * evaluate the stage velocities themselves (multi-GPU: partitioned
+ * evaluation, then one all-gather of the rows per stage). Same kernels as
+ * ssum_rk4, so such a driver reproduces it bit for bit. Per step:
+ *   for stage in 0..3: stage_begin (xs, q from x0, z0, area and the previous
+ *   stage's k, kz) -> evaluate u at (xs, q) -> stage_end (k, kz, acc, accz);
+ *   then step_end (x0, z0 advanced, renormalised). */
+int ssum_rk4_stage_begin(ssum_ctx* ctx, int stage, double dt, int64_t n, const double* d_x0,
+                         const double* d_z0, const double* d_area, const double* d_k,
+                         const double* d_kz, double* d_xs, double* d_q);
+int ssum_rk4_stage_end(ssum_ctx* ctx, int stage, double omega, int64_t n, const double* d_u,
+                       double* d_k, double* d_kz, double* d_acc, double* d_accz);
+int ssum_rk4_step_end(ssum_ctx* ctx, double dt, int64_t n, double* d_x0, double* d_z0,
+                      const double* d_acc, const double* d_accz);
 
 /* ---- measurement --------------------------------------------------------- */
 /* FP64 roofline denominator: DFMA-chain throughput of this device in TFLOP/s

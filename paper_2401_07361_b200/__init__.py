@@ -108,7 +108,8 @@ EXPORTED_SYMBOLS = (
     "ssum_bin_particles", "ssum_tree_node_count", "ssum_tree_export", "ssum_dual_traversal",
     "ssum_rk4", "ssum_mesh_vertex_count", "ssum_make_icosa_mesh", "ssum_rh4_vorticity",
     "ssum_make_random_cap", "ssum_fp64_peak", "ssum_set_partition", "ssum_partition_range",
-    "ssum_tree_perm", "ssum_eval_interaction",
+    "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
+    "ssum_rk4_step_end",
 )
 
 
@@ -151,6 +152,9 @@ def load_library():
         "ssum_tree_perm": (ctypes.c_int, [_P, _P, ctypes.c_int]),
         "ssum_eval_interaction": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(_Config), _P, _P, _I64, ctypes.c_int,
                                                  ctypes.c_int, ctypes.c_int, _P]),
+        "ssum_rk4_stage_begin": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64] + [_P] * 7),
+        "ssum_rk4_stage_end": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64] + [_P] * 5),
+        "ssum_rk4_step_end": (ctypes.c_int, [_P, ctypes.c_double, _I64] + [_P] * 4),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -366,6 +370,27 @@ class FaceTree:
         if out.size:
             self._check(self._lib.ssum_tree_perm(self._h, _ptr(out), 0))
         return out
+
+    # ---- RK4 step pieces on device arrays (ssum_rk4_stage_begin & co.) ----
+    def rk4_stage_begin(self, stage: int, dt: float, n: int, x0: int, z0: int, area: int, k: int, kz: int,
+                        xs: int, q: int) -> None:
+        """Stage positions xs (renormalised) and strengths q = zeta_s A from
+        x0, z0 and the previous stage's k, kz (device pointers)."""
+        v = ctypes.c_void_p
+        self._check(self._lib.ssum_rk4_stage_begin(self._h, int(stage), float(dt), int(n), v(x0), v(z0), v(area),
+                                                   v(k), v(kz), v(xs), v(q)))
+
+    def rk4_stage_end(self, stage: int, omega: float, n: int, u: int, k: int, kz: int, acc: int,
+                      accz: int) -> None:
+        """k = u, kz = -2 omega u_z, accumulated into acc/accz with RK4 weights."""
+        v = ctypes.c_void_p
+        self._check(self._lib.ssum_rk4_stage_end(self._h, int(stage), float(omega), int(n), v(u), v(k), v(kz),
+                                                 v(acc), v(accz)))
+
+    def rk4_step_end(self, dt: float, n: int, x0: int, z0: int, acc: int, accz: int) -> None:
+        """x0, z0 advanced by dt/6 (acc, accz); positions renormalised."""
+        v = ctypes.c_void_p
+        self._check(self._lib.ssum_rk4_step_end(self._h, float(dt), int(n), v(x0), v(z0), v(acc), v(accz)))
 
     def set_stream(self, stream_ptr: int) -> None:
         self._check(self._lib.ssum_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))

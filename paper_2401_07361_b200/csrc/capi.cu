@@ -612,4 +612,46 @@ int ssum_rk4(ssum_ctx* h, const ssum_config* cfg, double* xyz, double* zeta, con
   });
 }
 
+// The three pieces of ssum_rk4's step, for drivers that evaluate the stage
+// velocities themselves (the multi-GPU driver: partitioned evaluation + one
+// all-gather per stage). Same kernels, so a driver built from them matches
+// ssum_rk4 bit for bit. Device pointers, the context's stream.
+int ssum_rk4_stage_begin(ssum_ctx* h, int stage, double dt, int64_t n, const double* d_x0, const double* d_z0,
+                         const double* d_area, const double* d_k, const double* d_kz, double* d_xs, double* d_q) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (stage < 0 || stage > 3) throw Error(SSUM_INVALID, "RK4 stage must be 0..3");
+    if (n == 0) return;
+    const double cs[4] = {0.0, 0.5 * dt, 0.5 * dt, dt};
+    k_rk4_stage<<<grid_for(n, 256), 256, 0, c.stream>>>(n, stage, cs[stage], d_x0, d_z0, d_area, d_k, d_kz, d_xs,
+                                                        d_q, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  });
+}
+
+int ssum_rk4_stage_end(ssum_ctx* h, int stage, double omega, int64_t n, const double* d_u, double* d_k, double* d_kz,
+                       double* d_acc, double* d_accz) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (stage < 0 || stage > 3) throw Error(SSUM_INVALID, "RK4 stage must be 0..3");
+    if (n == 0) return;
+    k_rk4_accum<<<grid_for(n, 256), 256, 0, c.stream>>>(n, stage, omega, d_u, d_k, d_kz, d_acc, d_accz);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  });
+}
+
+int ssum_rk4_step_end(ssum_ctx* h, double dt, int64_t n, double* d_x0, double* d_z0, const double* d_acc,
+                      const double* d_accz) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (n == 0) return;
+    k_rk4_final<<<grid_for(n, 256), 256, 0, c.stream>>>(n, dt / 6.0, d_x0, d_z0, d_acc, d_accz, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    check_flags(c, "rk4");
+  });
+}
+
 }  // extern "C"

@@ -21,7 +21,7 @@ def gather_partitioned_rows(out: torch.Tensor, perm: torch.Tensor, p0: int, p1: 
     """out: (N, D) with valid rows perm[p0:p1] on this rank; returns `out`
     with every rank's rows filled in. Works for NCCL (CUDA tensors) and gloo
     (CPU tensors)."""
-    ws = dist.get_world_size(group)
+    ws = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     if ws == 1:
         return out
     dev = out.device
@@ -49,3 +49,57 @@ def gather_rows(tree, out: torch.Tensor, group: Optional[dist.ProcessGroup] = No
     perm = torch.empty(n, dtype=torch.int32, device=out.device)
     tree.perm(perm.data_ptr())
     return gather_partitioned_rows(out, perm, p0, p1, group)
+
+
+# ------------------------------------------------------------------ RK4
+class TreecodeRK4Ops:
+    """Stage operations of the multi-GPU RK4 on one FaceTree (this rank's
+    GPU): the RK4 arithmetic runs through ssum_rk4_stage_* (the kernels of
+    ssum_rk4), the stage velocity is this rank's partitioned tree-code
+    evaluation followed by the row all-gather (one exchange
+    per stage)."""
+
+    def __init__(self, tree, cfg, group: Optional[dist.ProcessGroup] = None):
+        from . import BiotSavartKernel, treecode_sum_device
+
+        self.tree, self.cfg, self.group = tree, cfg, group
+        self._k, self._eval = BiotSavartKernel, treecode_sum_device
+
+    def stage_begin(self, s: int, dt: float, st: dict) -> None:
+        n = st["n"]
+        self.tree.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
+                                  st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
+
+    def velocity(self, st: dict) -> None:
+        n = st["n"]
+        st["u"].zero_()
+        self._eval(self.tree, self._k, self.cfg, st["xs"].data_ptr(), st["q"].data_ptr(), n, st["u"].data_ptr())
+        gather_rows(self.tree, st["u"], self.group)
+
+    def stage_end(self, s: int, omega: float, st: dict) -> None:
+        self.tree.rk4_stage_end(s, omega, st["n"], st["u"].data_ptr(), st["k"].data_ptr(), st["kz"].data_ptr(),
+                                st["acc"].data_ptr(), st["accz"].data_ptr())
+
+    def step_end(self, dt: float, st: dict) -> None:
+        self.tree.rk4_step_end(dt, st["n"], st["x0"].data_ptr(), st["z0"].data_ptr(), st["acc"].data_ptr(),
+                               st["accz"].data_ptr())
+
+
+def rk4_distributed(x: torch.Tensor, zeta: torch.Tensor, area: torch.Tensor, dt: float, steps: int, ops,
+                    omega: float = 2.0 * 3.141592653589793):
+    """Lagrangian RK4 of the BVE with the stage velocities
+    from `ops.velocity` (every rank ends each stage holding all N rows). x
+    (N, 3), zeta (N), area (N) are replicated on every rank and advanced in
+    place; returns (x, zeta). With TreecodeRK4Ops on one rank this is
+    ssum_rk4 bit for bit."""
+    n = x.shape[0]
+    st = {"n": n, "x0": x, "z0": zeta, "area": area, "xs": torch.empty_like(x), "q": torch.empty_like(zeta),
+          "u": torch.zeros_like(x), "k": torch.zeros_like(x), "kz": torch.zeros_like(zeta),
+          "acc": torch.zeros_like(x), "accz": torch.zeros_like(zeta)}
+    for _ in range(steps):
+        for s in range(4):
+            ops.stage_begin(s, dt, st)
+            ops.velocity(st)
+            ops.stage_end(s, omega, st)
+        ops.step_end(dt, st)
+    return x, zeta
