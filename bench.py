@@ -277,6 +277,33 @@ def run_gpu(args):
         except (OSError, ValueError):
             traffic = None
     all_evals = sum(stats.kernel_evals)
+    # upward / downward passes: algorithmic flops per
+    # (particle, node) visit plus the p x p transforms per node; bytes as
+    # stated there. Timed by the same events as phase_ms (upward includes
+    # the particle gather and proxy points).
+    hbm = None
+    try:
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        hbm = 7700.0  # B200_PROFILING.md fallback
+    deg = CFG["degree"]
+    p_pts = (deg + 1) * (deg + 2) // 2
+    base = 21 + 3 * (deg - 1)
+    up_flop = stats.up_visits * (base + 4 * p_pts) + stats.weight_nodes * 2 * p_pts * p_pts
+    up_bytes = 32 * stats.up_visits
+    down_flop = stats.down_visits * (base + 8 * p_pts) + stats.fit_nodes * 6 * p_pts * p_pts
+    down_bytes = (32 + 24) * n
+
+    def _pass(flop, byts, ms):
+        s = max(ms, 1e-9) * 1e-3
+        return {"ms": ms, "TFLOP/s": flop / s / 1e12, "fp64_frac": flop / s / 1e12 / peak, "GB/s": byts / s / 1e9,
+                "hbm_frac": byts / s / 1e9 / hbm, "flop": flop, "bytes": byts}
+
+    passes = {"visits": {"upward": stats.up_visits, "downward": stats.down_visits},
+              "upward": _pass(up_flop, up_bytes, stats.upward_ms),
+              "downward": _pass(down_flop, down_bytes, stats.finish_ms),
+              "flop_per_visit": {"upward": base + 4 * p_pts, "downward": base + 8 * p_pts},
+              "hbm_peak_gbs": hbm}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -297,14 +324,17 @@ def run_gpu(args):
                      "pp_pc": stats.pp_pc_ms, "downward_finish": stats.finish_ms},
         "kernel_evals": {"pp": stats.kernel_evals[0], "pc": stats.kernel_evals[1], "cp": stats.kernel_evals[2],
                          "cc": stats.kernel_evals[3]},
+        "passes": passes,
         "clocks": clocks.summary(),
     }
+    ref_u = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle_lib as ol
 
         if ol.ref_available():
             cores = os.cpu_count() or 1
             dt, ref_out, _ = reference_step(ol, xyz, q, cores)
+            ref_u = ref_out
             mine = h_out.numpy()
             line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "reference",
                                     "sample": "one full config-4 treecode_sum (unmodified reference, "
@@ -312,10 +342,46 @@ def run_gpu(args):
             line["parity_rel_l2_vs_reference"] = ol.rel_l2(mine, ref_out)
         else:
             line["cpu_baseline"] = None
+    if rank == 0 and ws == 1 and not args.no_error:
+        try:
+            line["error_vs_direct"] = sampled_direct_error(xyz, q, h_out.numpy(), dev, ref_u)
+        except Exception as exc:  # a failed extra must not cost the bench line
+            line["error_vs_direct"] = {"error": repr(exc)}
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def sampled_direct_error(xyz, q, u_tree, dev, u_ref=None, m=2048, seed=2024):
+    """Relative L2 error of the tree code against direct summation on m
+    seeded random targets (all N sources; fp64 torch matmuls, outside the
+    timed region). The reference measured E = 2.38e-6 at config 4 (SURVEY.md
+    §8(d)); the bar is E(mine) <= E(reference)."""
+    import torch
+
+    n = xyz.shape[0]
+    idx = np.random.default_rng(seed).choice(n, size=min(m, n), replace=False)
+    X = torch.from_numpy(xyz).to(dev)
+    Q = torch.from_numpy(q).to(dev)
+    tid = torch.from_numpy(idx).to(dev)
+    T = X[tid]
+    S = torch.zeros_like(T)
+    chunk = 1 << 18
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        den = 1.0 - T @ X[c0:c1].T
+        own = (tid >= c0) & (tid < c1)  # self pairs excluded
+        den[own.nonzero().squeeze(1), (tid[own] - c0)] = float("inf")
+        S += (Q[c0:c1] / den) @ X[c0:c1]
+    u_dir = (-1.0 / (4.0 * np.pi)) * torch.cross(T, S, dim=1)
+    def rel(u):
+        ut = torch.from_numpy(np.ascontiguousarray(u[idx])).to(dev)
+        return float(torch.linalg.norm(ut - u_dir) / torch.linalg.norm(u_dir))
+
+    return {"value": rel(u_tree), "reference_same_targets": rel(u_ref) if u_ref is not None else None,
+            "targets": int(len(idx)), "seed": seed, "survey_reference_E_config4": 2.38e-6,
+            "definition": "||u_tree - u_direct||_2 / ||u_direct||_2 over the sampled targets"}
 
 
 def main():
@@ -325,6 +391,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-error", action="store_true", help="skip the sampled error vs direct summation")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -76,6 +76,7 @@ typedef struct {
   int64_t node_count, leaf_count, weight_nodes, fit_nodes;
   int64_t gpu_launches;           /* kernels launched by the last call            */
   double pp_pc_ms, cp_cc_fit_ms, upward_ms, finish_ms; /* device time per pass     */
+  uint64_t up_visits, down_visits; /* (particle, weight node) / (particle, fit node) pairs */
 } ssum_stats;
 
 /* ---- context ------------------------------------------------------------ */

@@ -94,7 +94,8 @@ class _Stats(ctypes.Structure):
                 ("leaf_count", ctypes.c_int64), ("weight_nodes", ctypes.c_int64),
                 ("fit_nodes", ctypes.c_int64), ("gpu_launches", ctypes.c_int64),
                 ("pp_pc_ms", ctypes.c_double), ("cp_cc_fit_ms", ctypes.c_double),
-                ("upward_ms", ctypes.c_double), ("finish_ms", ctypes.c_double)]
+                ("upward_ms", ctypes.c_double), ("finish_ms", ctypes.c_double),
+                ("up_visits", ctypes.c_uint64), ("down_visits", ctypes.c_uint64)]
 
 
 _LIB = None
@@ -249,6 +250,8 @@ class TreecodeStats:
     cp_cc_fit_ms: float = 0.0
     upward_ms: float = 0.0
     finish_ms: float = 0.0
+    up_visits: int = 0      # (particle, weight node) pairs of the upward pass
+    down_visits: int = 0    # (particle, fit node) pairs of the downward pass
 
     def _to_c(self) -> _Stats:
         s = _Stats()

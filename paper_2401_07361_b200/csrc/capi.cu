@@ -125,6 +125,8 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
     st->leaf_count = c.bins.n_leaves;
     st->weight_nodes = c.lists.n_weight;
     st->fit_nodes = c.lists.n_fit;
+    st->up_visits = c.lists.visits[0];
+    st->down_visits = c.lists.visits[1];
     st->gpu_launches = c.launches - l0;
   }
 }

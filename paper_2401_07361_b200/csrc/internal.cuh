@@ -162,6 +162,7 @@ struct Lists {
   int64_t n_leaf_ranges = 0, n_fit_ranges = 0;
   DBuf<SrcRange> leaf_ranges, fit_ranges;
   uint64_t evals[4] = {0, 0, 0, 0};
+  uint64_t visits[2] = {0, 0};   // upward (particle, weight node), downward (particle, fit node)
   // per-tile work (PP, PC) / (CP, CC) pair counts and this part's share
   DBuf<ulonglong2> leaf_cost, fit_cost;
   int leaf_t0 = 0, leaf_t1 = 0;  // leaf tile range of this part

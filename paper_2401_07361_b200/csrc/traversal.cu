@@ -298,6 +298,25 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
   }
 }
 
+// Upward / downward pass visits: bin sizes of the weight nodes and of the
+// fit nodes (counters[0], counters[1]).
+__global__ void k_visits(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ fit_nodes, int nf,
+                         const int* __restrict__ cnt, unsigned long long* counters) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long up = 0, down = 0;
+  if (k < nw) up = static_cast<unsigned long long>(cnt[weight_nodes[k]]);
+  else if (k < nw + nf) down = static_cast<unsigned long long>(cnt[fit_nodes[k - nw]]);
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  up = BR(tmp).Sum(up);
+  __syncthreads();
+  down = BR(tmp).Sum(down);
+  if (threadIdx.x == 0) {
+    if (up) atomicAdd(&counters[0], up);
+    if (down) atomicAdd(&counters[1], down);
+  }
+}
+
 // Node flags from the emitted list (treecode.cpp:295-317).
 __global__ void k_mark(const int4* __restrict__ E, long long ne, unsigned char* is_weight, unsigned char* is_fit,
                        int* group_key, int* group_val, unsigned long long* kind_counts) {
@@ -764,7 +783,8 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_weight.p, 0, size_t(nn), c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_fit.p, 0, size_t(nn), c.stream));
   S.counters.ensure(16);
-  SSUM_CUDA_CHECK(cudaMemsetAsync(S.counters.p, 0, 8 * sizeof(unsigned long long), c.stream));
+  // [0..3] kinds, [4..7] kernel evals, [8] node-list selection counts, [10..11] pass visits
+  SSUM_CUDA_CHECK(cudaMemsetAsync(S.counters.p, 0, 12 * sizeof(unsigned long long), c.stream));
   const size_t nes = size_t(std::max<long long>(ne, 1));
   S.gkey.ensure(nes);
   S.gkey2.ensure(nes);
@@ -891,8 +911,16 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     c.launches++;
   }
   L.n_fit_tiles = nf;
-  // interaction / evaluation counts: read back with the evaluation's final sync
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_small + 8, S.counters.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  // (particle, weight node) and (particle, fit node) visits of the upward /
+  // downward passes
+  if (L.n_weight + nf > 0) {
+    k_visits<<<grid_for(L.n_weight + nf, 256), 256, 0, c.stream>>>(L.weight_nodes.p, L.n_weight, L.fit_nodes.p, nf,
+                                                                  B.cnt.p, S.counters.p + 10);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  // interaction / evaluation / visit counts: read back with the evaluation's final sync
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_small + 8, S.counters.p, 12 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                   c.stream));
   L.counts_pending = true;
   trace().mark("lists.tiles");
@@ -910,6 +938,8 @@ void finalize_counts(Ctx& c) {
     L.counts[k] = h[k];
     L.evals[k] = h[4 + k];
   }
+  L.visits[0] = h[10];
+  L.visits[1] = h[11];
   if (c.nparts <= 1)
     for (int k = 0; k < 4; ++k) L.local_evals[k] = L.evals[k];
   L.counts_pending = false;
