@@ -1,9 +1,8 @@
 """Summaries for profiles/README.md from ncu output.
 
     python tools/summarize_profiles.py launches <launches.csv>
-        launch table of the last treecode call (launches after the
-        second-to-last k_finish) in a `ncu --metrics gpu__time_duration.sum`
-        launch list.
+        launch table of the last treecode call on device-resident inputs in a
+        `ncu --metrics gpu__time_duration.sum` launch list.
     python tools/summarize_profiles.py full <report.ncu-rep> [out.json]
         key metrics of every kernel in an `ncu --set full` capture.
 """
@@ -29,15 +28,20 @@ def launches(path):
         ms = v * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}.get(u, 1e-6)
         name = d[ik].split("(")[0].replace("void ", "").replace("ssum::<unnamed>::", "").replace("<unnamed>::", "")
         seq.append((name, ms))
-    # one step = one treecode call, which ends with k_finish: take the last one
-    ends = [i for i, (n, _) in enumerate(seq) if n.startswith("k_finish")]
-    step = seq[ends[-2] + 1 : ends[-1] + 1] if len(ends) > 1 else seq[: ends[-1] + 1]
+    # one step = one treecode call, which starts with the binning (k_walk on
+    # a reused tree, k_bin_roots on a new one); report the last call on
+    # device-resident inputs (one k_finish: host-pointer calls finish in pieces)
+    starts = [i for i, (n, _) in enumerate(seq) if n in ("k_walk", "k_bin_roots")] + [len(seq)]
+    calls = [seq[a:b] for a, b in zip(starts[:-1], starts[1:])]
+    device_calls = [c for c in calls if sum(1 for n, _ in c if n.startswith("k_finish")) == 1]
+    step = (device_calls or calls)[-1]
+    ends = calls
     agg = OrderedDict()
     for name, ms in step:
         c, t = agg.get(name, (0, 0.0))
         agg[name] = (c + 1, t + ms)
     tot = sum(t for c, t in agg.values())
-    print(f"{len(ends)} treecode calls in the capture; the last one: {len(step)} launches, "
+    print(f"{len(ends)} treecode calls in the capture; the last on device-resident inputs: {len(step)} launches, "
           f"{tot:.3f} ms serialised cold-cache device time\n")
     print("| kernel | ms | launches | share |\n|---|---|---|---|")
     for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
