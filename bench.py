@@ -39,13 +39,39 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-METRIC = "BVE tree-code velocity evals/s (N=2.6M, fp64)"
 UNIT = "velocity_evals/s"
-LEVEL = 9
-CFG = dict(theta=0.7, n_threshold=64, degree=8, max_depth=10)
-WORKLOAD = ("config4: L9 icosahedral mesh N=2,621,442, BASELINE RH4 vorticity, Voronoi areas, "
-            "Biot-Savart, d=8, theta=0.7, N_T=64, max_depth=10; one full treecode_sum per step")
 FLOP_PER_PAIR = 13  # F_BS
+# BASELINE.json workloads. The bench line is config 4 (the metric's own
+# config); --config c2 / c3 / c5 print the same line for the other
+# single-evaluation configs (parity-test sizes, reported for information).
+CONFIGS = {
+    "c4": dict(metric="BVE tree-code velocity evals/s (N=2.6M, fp64)", mesh=9,
+               cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
+               workload="config4: L9 icosahedral mesh N=2,621,442, BASELINE RH4 vorticity, Voronoi areas, "
+                        "Biot-Savart, d=8, theta=0.7, N_T=64, max_depth=10; one full treecode_sum per step"),
+    "c2": dict(metric="BVE tree-code velocity evals/s (N=655k, fp64)", mesh=8,
+               cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
+               workload="config2: L8 icosahedral mesh N=655,362, RH4, Voronoi areas, Biot-Savart, d=8, "
+                        "theta=0.7, cluster-cluster; one full treecode_sum per step"),
+    "c3": dict(metric="BVE tree-code velocity evals/s (N=4.2M random cap, fp64)", cap=1 << 22,
+               cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
+               workload="config3: 2^22 seeded points (half uniform, half in a 10 deg cap at lat 40), Gaussian "
+                        "vortex minus its mean, A=4pi/N, Biot-Savart, d=8, theta=0.7, N_T=64, max_depth=10"),
+    "c5": dict(metric="BVE tree-code velocity evals/s (N=10.5M, fp64)", mesh=10,
+               cfg=dict(theta=0.8, n_threshold=64, degree=8, max_depth=10),
+               workload="config5: L10 icosahedral mesh N=10,485,762, RH4, Voronoi areas, Biot-Savart, d=8, "
+                        "theta=0.8, cluster-cluster; one full treecode_sum per step"),
+}
+CONFIG = "c4"
+METRIC = CONFIGS[CONFIG]["metric"]
+CFG = CONFIGS[CONFIG]["cfg"]
+WORKLOAD = CONFIGS[CONFIG]["workload"]
+
+
+def use_config(name):
+    global CONFIG, METRIC, CFG, WORKLOAD
+    CONFIG = name
+    METRIC, CFG, WORKLOAD = CONFIGS[name]["metric"], CONFIGS[name]["cfg"], CONFIGS[name]["workload"]
 
 
 def dist_env():
@@ -58,7 +84,11 @@ def dist_env():
 def fixture():
     import paper_2401_07361_b200 as ss
 
-    xyz, area = ss.make_icosa_mesh(LEVEL)
+    c = CONFIGS[CONFIG]
+    if "cap" in c:
+        xyz, zeta, area = ss.make_random_cap(c["cap"], 5)
+        return xyz, zeta * area, area
+    xyz, area = ss.make_icosa_mesh(c["mesh"])
     q = ss.rh4_vorticity(xyz) * area
     return xyz, q, area
 
@@ -160,7 +190,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, **CFG, "n": n},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"full config-4 treecode_sum per step ({len(times)} timed of {args.steps} "
+                         "sample": f"full {CONFIG} treecode_sum per step ({len(times)} timed of {args.steps} "
                                    f"requested, 240 s budget); warm-up steps on a level-5 mesh"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -337,7 +367,7 @@ def run_gpu(args):
             ref_u = ref_out
             mine = h_out.numpy()
             line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "reference",
-                                    "sample": "one full config-4 treecode_sum (unmodified reference, "
+                                    "sample": f"one full {CONFIG} treecode_sum (unmodified reference, "
                                               f"workers={cores}), {dt:.1f} s"}
             line["parity_rel_l2_vs_reference"] = ol.rel_l2(mine, ref_out)
         else:
@@ -392,7 +422,9 @@ def main():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-error", action="store_true", help="skip the sampled error vs direct summation")
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS), help="BASELINE workload (default c4)")
     args = ap.parse_args()
+    use_config(args.config)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -178,9 +178,16 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
 #endif
     int it = 0;
     if (near_steps > 0) {
+      // bit `it` of hit: step `it` met a masked pair (self or near); steps
+      // past 32 are all re-walked when a repair is needed
       int ncnt = 0;
+      unsigned hit = 0;
 #pragma unroll 2
-      for (; it < near_steps; ++it) far_block<KER, kTpt, kNs, true>(x, B + it * kStep, G, a, &ncnt);
+      for (; it < near_steps; ++it) {
+        const int before = ncnt;
+        far_block<KER, kTpt, kNs, true>(x, B + it * kStep, G, a, &ncnt);
+        hit |= static_cast<unsigned>(ncnt != before) << (it & 31);
+      }
       // self pairs this lane walked in this chunk's near steps: the self
       // source of target ti sits at flattened position ti + T.self_shift
       const int o_end = min(n, near_steps * kStep);
@@ -190,9 +197,21 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
         const int o = ti[q] + T.self_shift - c * kChunk;
         nself += (T.has_self && o >= 0 && o < o_end && o % G == g) ? 1 : 0;
       }
-      if (__any_sync(0xffffffffu, ncnt != nself))
+      if (__any_sync(0xffffffffu, ncnt != nself)) {
+        // only the steps that met a masked pair (dense inputs: a handful of
+        // the chunk's near steps)
+        if (near_steps <= 32) {
 #pragma unroll 1
-        for (int r = 0; r < near_steps; ++r) near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
+          for (unsigned m = hit; m; m &= m - 1) {
+            const int r = __ffs(m) - 1;
+            near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
+          }
+        } else {
+#pragma unroll 1
+          for (int r = 0; r < near_steps; ++r)
+            near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
+        }
+      }
     }
     // well-separated sources only: branch-free, kNs sources x kTpt targets
     // of independent chains per step (zero-padded tail contributes 0)
