@@ -104,6 +104,8 @@ struct Binned {
   DBuf<int> cur;            // per particle: current node during the descent
   DBuf<int> leaf_of;        // per particle (original order)
   DBuf<int> perm;           // tree position -> original particle id
+  int64_t perm_n = -1;      // particle count perm is complete for (-1: none)
+  bool input_coherent = true;  // last reuse binning: most consecutive inputs in one leaf
   DBuf<int> pos_leaf;       // tree position -> leaf node
   DBuf<int> sort_keys, sort_keys2, sort_vals;
   // level-synchronous descent: candidates of the current level, their split

@@ -250,7 +250,8 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
 // are two binary searches of the node's key range in the sorted keys. The
 // binning is final unless a childless node must split (bin > N_T below
 // max_depth) — then the level-synchronous build runs instead.
-__global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const double* __restrict__ tri,
+__global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const int* __restrict__ order,
+                       const double* __restrict__ tri,
                        const double* __restrict__ cramer, const double* __restrict__ center,
                        const int* __restrict__ child_base, const unsigned long long* __restrict__ nkey,
                        unsigned long long* __restrict__ key, int* __restrict__ ids, int* __restrict__ leaf_of,
@@ -262,8 +263,11 @@ __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, c
   for (int k = threadIdx.x; k < 240; k += blockDim.x) skr[k] = cramer[k];
   for (int k = threadIdx.x; k < 60; k += blockDim.x) sc[k] = center[k];
   __syncthreads();
-  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= i1) return;
+  const int64_t k = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= i1) return;
+  // order: the previous call's tree order, so that a warp's particles are
+  // neighbours and share their descent (results still land at index i)
+  const int64_t i = order ? order[k] : k;
   const d3 p = load3(xyz + 3 * i);
   int node = find_root(p, st, skr, sc);
   if (node < 0) {
@@ -276,6 +280,19 @@ __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, c
     leaf_of[i] = node;
   }
   ids[i] = static_cast<int>(i);
+}
+
+// How many consecutive input particles share a leaf (input-order coherence).
+__global__ void k_coherence(const int* __restrict__ leaf_of, int64_t n, int* count) {
+  __shared__ int block_sum;
+  if (threadIdx.x == 0) block_sum = 0;
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool same = i + 1 < n && leaf_of[i] == leaf_of[i + 1];
+  const unsigned m = __ballot_sync(0xffffffffu, same);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(&block_sum, __popc(m));
+  __syncthreads();
+  if (threadIdx.x == 0 && block_sum) atomicAdd(count, block_sum);
 }
 
 __device__ __forceinline__ int lower_bound_u64(const unsigned long long* __restrict__ a, int n, unsigned long long v) {
@@ -464,7 +481,7 @@ void tree_init_roots(Ctx& c) {
 // nothing of the call's state committed, when the tree cannot be reused as
 // is: no children yet, deeper than the path keys reach, or a childless node
 // whose bin now needs a split.
-static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
+static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth, int64_t prev_perm_n) {
   NodeTable& T = c.nodes;
   Binned& B = c.bins;
   if (T.count <= 20 || T.max_level > kKeyMaxLevel || n > 0x3fffffff) return false;
@@ -479,16 +496,24 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   B.d_leaves.ensure(size_t(nn));
   B.leaf_pos.ensure(size_t(nn));
   B.leaf_flag.ensure(size_t(n));
-  int* d_cnt = c.d_flags.p + 16;  // [0] splits needed, [1] leaves
-  SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 2 * sizeof(int), c.stream));
-  // host-pointer calls: walk each input piece as soon as it has landed
-  const int pieces = c.io.active ? Ctx::kIoChunks : 1;
+  int* d_cnt = c.d_flags.p + 16;  // [0] splits needed, [1] leaves, [2] input-order coherence
+  SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 3 * sizeof(int), c.stream));
+  // Walk order: input order when the input is spatially coherent (the last
+  // call found most consecutive particles in one leaf) — a host-pointer call
+  // then walks each input piece as soon as it has landed — else the previous
+  // call's tree order, so that a warp's particles are neighbours and share
+  // their descent.
+  const bool by_tree = prev_perm_n == n && !B.input_coherent;
+  const int pieces = (c.io.active && !by_tree) ? Ctx::kIoChunks : 1;
+  const int* order = by_tree ? B.perm.p : nullptr;
+  if (c.io.active && pieces == 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[Ctx::kIoChunks - 1], 0));
   for (int j = 0; j < pieces; ++j) {
-    const int64_t a = c.io.active ? c.io.bounds[j] : 0, b = c.io.active ? c.io.bounds[j + 1] : n;
-    if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[j], 0));
+    const int64_t a = pieces > 1 ? c.io.bounds[j] : 0, b = pieces > 1 ? c.io.bounds[j + 1] : n;
+    if (pieces > 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[j], 0));
     if (b <= a) continue;
-    k_walk<<<grid_for(b - a, bs), bs, 0, c.stream>>>(d_xyz, a, b, T.tri.p, T.cramer.p, T.center.p, T.child_base.p,
-                                                     T.key.p, B.wkey.p, B.sort_vals.p, B.leaf_of.p, c.d_flags.p);
+    k_walk<<<grid_for(b - a, bs), bs, 0, c.stream>>>(d_xyz, a, b, order, T.tri.p, T.cramer.p, T.center.p,
+                                                     T.child_base.p, T.key.p, B.wkey.p, B.sort_vals.p, B.leaf_of.p,
+                                                     c.d_flags.p);
     SSUM_LAUNCH_CHECK();
   }
   const int begin_bit = kKeyRootShift - 2 * T.max_level;
@@ -518,16 +543,24 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   SSUM_LAUNCH_CHECK();
   c.launches += 12;
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, d_cnt, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  k_coherence<<<grid_for(n, 1024), 1024, 0, c.stream>>>(B.leaf_of.p, n, d_cnt + 2);
+  SSUM_LAUNCH_CHECK();
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, d_cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   if (B.h_small[0] & kFlagGeometry) check_flags(c, "bin_particles: particle contained in no root face");
   if (B.h_small[1] > 0) return false;
   B.n_leaves = B.h_small[2];
+  B.input_coherent = 2 * int64_t(B.h_small[3]) > n;
+  B.perm_n = n;
   return true;
 }
 
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   Binned& B = c.bins;
+  // the previous permutation (a walk-order hint) is only trusted if that
+  // binning completed; it is invalid until this one does
+  const int64_t prev_perm_n = B.perm_n;
+  B.perm_n = -1;
   c.call_index++;
   c.host.valid = false;
   B.n = n;
@@ -542,7 +575,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   if (n == 0) return;
   B.cur.ensure(size_t(n));
   B.leaf_of.ensure(size_t(n));
-  if (bin_reuse(c, d_xyz, n, nt, max_depth)) {
+  if (bin_reuse(c, d_xyz, n, nt, max_depth, prev_perm_n)) {
     trace().mark("bin.reuse");
     return;
   }
@@ -672,6 +705,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   k_pos_leaf<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, B.leaf_of.p, B.pos_leaf.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
+  B.perm_n = n;
 }
 
 // Host snapshot of the node structure and this call's counts/offsets.
