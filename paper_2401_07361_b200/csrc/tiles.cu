@@ -13,18 +13,21 @@ constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
 // threads per TILE — up to 256 targets (a leaf's particles, or a fit node's
 // p proxy points) against the tile's list of source ranges.
 //
-//  * Thread -> (target t = tid % T, source group g = (tid / T) % G) with
-//    G = min(32, 256 / T): a 40-particle leaf keeps 240 of 256 lanes busy
-//    (6 groups), a p = 45 fit node 225 (5 groups).
-//  * The source ranges are streamed as ONE flattened list in chunks of 256
-//    (each thread fetches one source, locating its range by binary search on
-//    the ranges' prefix counts), double-buffered through shared memory:
+//  * Thread -> (targets u, u + th with th = ceil(T / 2), source group g)
+//    with G = min(32, 256 / th) groups: a 40-particle leaf keeps 240 of 256
+//    lanes busy (th 20, 12 groups), a p = 45 fit node 253 (th 23, 11 groups).
+//  * The source ranges are streamed as ONE flattened list in chunks of 512
+//    (each thread fetches two sources, locating their ranges by binary search
+//    on the ranges' prefix counts), double-buffered through shared memory:
 //    chunk c+1 is in flight in registers while chunk c is consumed. Every
-//    thread walks the chunk with stride G, so all warps run the same trip
-//    count (the chunk tail is zero-padded: q = 0 adds nothing).
+//    thread walks the chunk with stride G, 2 sources x 2 targets per step
+//    (far_block), so all warps run the same trip count (the chunk tail is
+//    zero-padded: q = 0 adds nothing).
 //  * Group partials are reduced in group order through shared memory
 //    (deterministic, no atomics).
-//  MODE kLeafMode: near-pair handling (pair_near), writes S per target.
+//  MODE kLeafMode: the near-possible prefix of the list runs with near pairs
+//                  masked, counted and repaired (kernels.cuh); writes S per
+//                  target.
 //  MODE kFitMode : well-separated pairs only; phi = K-sums at the proxy
 //                  points, then C = V^-1 phi (ProxyFit::solve, sbb.cpp:103-108).
 constexpr int kTileThreads = 256;

@@ -12,7 +12,7 @@
 // refinement) so the reference's emission order can be reproduced on export.
 //
 // The emitted list is then compacted into the evaluation layout:
-//   * leaf tiles  (<= 32 target particles each) with a list of source ranges
+//   * leaf tiles  (<= 256 target particles each) with a list of source ranges
 //     gathered over the leaf's root-to-leaf path: PP ranges (particles of the
 //     source bin, contiguous in tree order) and PC ranges (the source node's
 //     proxy points) — treecode.cpp:366-396;
@@ -102,94 +102,38 @@ __device__ __forceinline__ void pair_scatter(const PairEntry& p, int a, unsigned
     }
   }
 }
-// Frontier size: *d_m when the size lives on the device (planned traversal,
-// grid sized for `bound`), else `bound` itself. A device size above the bound
-// sets *ovf and is clamped (the planned traversal is then redone).
-__device__ __forceinline__ int frontier_size(const int* d_m, int bound, int* ovf) {
-  if (!d_m) return bound;
-  const int m = *d_m;
-  if (m > bound) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(ovf, 1);
-    return bound;
-  }
-  return m;
-}
-
-__global__ void k_trav_eval(const PairEntry* __restrict__ F, const int* __restrict__ d_m, int bound,
-                            const int* __restrict__ cnt, const double* __restrict__ center,
-                            const double* __restrict__ radius, const int* __restrict__ level,
-                            const int* __restrict__ child_base, double theta, int thr, int max_depth, int pc_only,
-                            int* __restrict__ action, unsigned long long* __restrict__ packed, int* ovf) {
+// One step of the breadth-first traversal, host-sized (bfs_synchronous):
+// decide every frontier pair; packed[k] = (emits << 32) | child slots, and
+// packed[m] = 0 so that the exclusive scan's entry m is the total.
+__global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* __restrict__ cnt,
+                            const double* __restrict__ center, const double* __restrict__ radius,
+                            const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr,
+                            int max_depth, int pc_only, int* __restrict__ action,
+                            unsigned long long* __restrict__ packed) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k > bound) return;
-  const int m = frontier_size(d_m, bound, ovf);
-  if (k >= m) {  // sentinel and padding: the exclusive scan's entry `bound` is the total
+  if (k > m) return;
+  if (k == m) {
     packed[k] = 0;
     return;
   }
   const int a = pair_action(F[k].t, F[k].s, cnt, center, radius, level, child_base, theta, thr, max_depth, pc_only);
   action[k] = a;
-  const unsigned long long emit = (a & 4) ? 1ull : 0ull;
-  const unsigned long long kids = (a & 8) ? 4ull : 0ull;
-  packed[k] = (emit << 32) | kids;
+  packed[k] = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
 }
 
-// d_ebase: emission base of this step (planned traversal; [1] receives the
-// next step's base and d_m_next the next frontier size), else e_base_host.
-// Writes beyond cap_next / e_cap set *ovf instead.
-__global__ void k_trav_scatter(const PairEntry* __restrict__ F, const int* __restrict__ d_m, int bound,
-                               const int* __restrict__ action, const unsigned long long* __restrict__ scan,
-                               const int* __restrict__ child_base, PairEntry* __restrict__ Fnext, int cap_next,
-                               int4* __restrict__ E, unsigned long long* __restrict__ K, long long e_cap,
-                               long long e_base_host, long long* d_ebase, int* d_m_next, int* flags, int* ovf) {
+// ... and emit / refine at the scanned positions.
+__global__ void k_trav_scatter(const PairEntry* __restrict__ F, int m, const int* __restrict__ action,
+                               const unsigned long long* __restrict__ scan, const int* __restrict__ child_base,
+                               PairEntry* __restrict__ Fnext, int4* __restrict__ E, unsigned long long* __restrict__ K,
+                               long long e_base, int* flags) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int m = frontier_size(d_m, bound, ovf);
-  const long long e_base = d_ebase ? d_ebase[0] : e_base_host;
-  if (k == 0 && d_m_next) {
-    const unsigned long long tot = scan[bound];
-    const int next = static_cast<int>(tot & 0xffffffffull);
-    const long long emitted = static_cast<long long>(tot >> 32);
-    *d_m_next = next;
-    d_ebase[1] = e_base + emitted;
-    if (next > cap_next || e_base + emitted > e_cap) atomicOr(ovf, 1);
-  }
   if (k >= m) return;
   const int a = action[k];
-  if (!a) return;
-  const unsigned long long sc = scan[k];
-  const PairEntry p = F[k];
-  if (a & 4) {
-    const long long e = e_base + static_cast<long long>(sc >> 32);
-    if (e >= e_cap) return;
-    E[e] = int4{p.t, p.s, a & 3, 0};
-    K[e] = p.key;
-  } else {
-    const int o = static_cast<int>(sc & 0xffffffffull);
-    if (o + 4 > cap_next) return;
-    const bool rt = (a & 16) != 0;
-    const int cb = child_base[rt ? p.t : p.s];
-    const int step = p.step + 1;
-    if (step > kKeyMaxSteps) atomicOr(flags, 4);  // order keys saturated (export only)
-    const int shift = 54 - kKeyStepBits * min(step, kKeyMaxSteps);
-    for (int q = 0; q < 4; ++q) {
-      PairEntry c;
-      c.t = rt ? cb + q : p.t;
-      c.s = rt ? p.s : cb + q;
-      c.key = p.key | (static_cast<unsigned long long>(q) << shift);
-      c.step = step;
-      c.pad = 0;
-      Fnext[o + q] = c;
-    }
-  }
+  if (a) pair_scatter(F[k], a, scan[k], e_base, child_base, Fnext, E, K, flags);
 }
 
-__global__ void k_root_pairs(PairEntry* F, int* d_m0, long long* d_ebase0, int* ovf) {
+__global__ void k_root_pairs(PairEntry* F) {
   const int k = threadIdx.x + blockIdx.x * blockDim.x;
-  if (k == 0 && d_m0) {
-    *d_m0 = 400;
-    *d_ebase0 = 0;
-    *ovf = 0;
-  }
   if (k >= 400) return;
   PairEntry p;
   p.t = k / 20;
@@ -625,9 +569,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
   Binned& B = c.bins;
   TravScratch& S = c.trav;
   const int bs = 256;
-  int* ovf = c.d_flags.p + 24;
   S.F0.ensure(400);
-  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, nullptr, nullptr, nullptr);
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   int m = 400;
@@ -640,10 +583,10 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
     S.action.ensure(size_t(m) + 1);
     S.packed.ensure(size_t(m) + 1);
     S.scan.ensure(size_t(m) + 1);
-    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, nullptr, m, B.cnt.p, c.nodes.center.p,
-                                                           c.nodes.radius.p, c.nodes.level.p, c.nodes.child_base.p,
-                                                           cfg.theta, cfg.n_threshold, cfg.max_depth, cfg.pc_only,
-                                                           S.action.p, S.packed.p, ovf);
+    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
+                                                           c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
+                                                           cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
+                                                           S.packed.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     exclusive_scan(c, S.packed.p, S.scan.p, m + 1);  // packed[m] = 0: totals at scan[m]
@@ -655,9 +598,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
     L.inter.ensure(size_t(ne + emitted), true, c.stream);
     L.key.ensure(size_t(ne + emitted), true, c.stream);
     S.F1.ensure(size_t(std::max(next, 1)));
-    k_trav_scatter<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, nullptr, m, S.action.p, S.scan.p,
-                                                          c.nodes.child_base.p, S.F1.p, next, L.inter.p, L.key.p,
-                                                          ne + emitted, ne, nullptr, nullptr, c.d_flags.p, ovf);
+    k_trav_scatter<<<grid_for(m, bs), bs, 0, c.stream>>>(S.F0.p, m, S.action.p, S.scan.p, c.nodes.child_base.p,
+                                                          S.F1.p, L.inter.p, L.key.p, ne, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     ne += emitted;
@@ -704,7 +646,7 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   L.inter.ensure(size_t(ecap));
   L.key.ensure(size_t(ecap));
   if (!S.h_plan) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_plan, 256 * sizeof(long long)));
-  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p, nullptr, nullptr, nullptr);
+  k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
   SSUM_LAUNCH_CHECK();
   const int* cnt = B.cnt.p;
   const double *center = c.nodes.center.p, *radius = c.nodes.radius.p;
