@@ -251,6 +251,61 @@ def test_reused_tree_moving_particles(ss, ol, mesh_fixture):
         compare_trees(t.export(), r.export())
 
 
+def _device_eval(ss, tree, xyz, q, c):
+    import torch
+
+    dev = torch.device("cuda", 0)
+    tree.set_stream(torch.cuda.current_stream().cuda_stream)
+    dx = torch.from_numpy(np.ascontiguousarray(xyz)).to(dev)
+    dq = torch.from_numpy(np.ascontiguousarray(q)).to(dev)
+    out = torch.zeros((xyz.shape[0], 3), dtype=torch.float64, device=dev)
+    ss.treecode_sum_device(tree, ss.BiotSavartKernel, c, dx.data_ptr(), dq.data_ptr(), xyz.shape[0], out.data_ptr())
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("which", ["mesh", "cap"])
+def test_host_and_device_entry_points_identical(ss, mesh_fixture, which):
+    """The host-pointer entry (input in pieces walked as they land, result
+    finished in original order and copied back piece by piece) and the
+    device-pointer entry give bit-identical velocities, on a spatially
+    coherent input (mesh) and an incoherent one (random cap: the binning walk
+    switches to the previous tree order)."""
+    if which == "mesh":
+        xyz, q, _ = mesh_fixture(6)
+    else:
+        xyz, z, a = ss.make_random_cap(1 << 16, 3)
+        q = z * a
+    c = cfg(ss, deg=6)
+    t = ss.FaceTree()
+    first = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t)  # builds the tree
+    host = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t)  # reuse path, host pointers
+    dev = _device_eval(ss, t, xyz, q, c)                               # reuse path, device pointers
+    dev2 = _device_eval(ss, t, xyz, q, c)
+    assert np.array_equal(first, host)
+    assert np.array_equal(host, dev)
+    assert np.array_equal(dev, dev2)
+
+
+def test_walk_order_switch_matches_reference(ss, ol):
+    """Incoherent input (shuffled random cap) on a reused tree: later calls walk
+    the particles in the previous tree order; bins and velocities stay those
+    of the reference's reused FaceTree."""
+    xyz, z, a = ss.make_random_cap(1 << 15, 9)
+    perm = np.random.default_rng(4).permutation(xyz.shape[0])
+    xyz, z, a = xyz[perm].copy(), z[perm].copy(), a[perm].copy()
+    q = z * a
+    t = ss.FaceTree()
+    r = ol.RefTree()
+    for _ in range(3):
+        mine = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, deg=4), tree=t)
+        ref, _ = r.treecode(0, xyz, q, 0.7, 64, 4, 10, NCPU)
+        assert ol.rel_l2(mine, ref) < REL_TOL
+        compare_trees(t.export(), r.export())
+    dev = _device_eval(ss, t, xyz, q, cfg(ss, deg=4))
+    assert np.array_equal(dev, mine)
+
+
 def test_max_depth_fallback_and_big_leaves(ss, ol, mesh_fixture):
     """max_depth binds: leaves with > 32 targets (multi-tile) and PP pairs at
     internal targets (treecode.cpp:54-57)."""
