@@ -149,6 +149,17 @@ class ClockSampler:
                                    default=None)}
 
 
+def cpu_model():
+    """Host CPU model name (the reference arm's hardware)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def reference_step(ol, xyz, q, workers):
     t0 = time.perf_counter()
     out, st = ol.ref_treecode(0, xyz, q, CFG["theta"], CFG["n_threshold"], CFG["degree"], CFG["max_depth"],
@@ -189,7 +200,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, **CFG, "n": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "cpu": cpu_model(),
                          "sample": f"full {CONFIG} treecode_sum per step ({len(times)} timed of {args.steps} "
                                    f"requested, 240 s budget); warm-up steps on a level-5 mesh"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -367,6 +378,7 @@ def run_gpu(args):
             ref_u = ref_out
             mine = h_out.numpy()
             line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+                                    "cpu": cpu_model(),
                                     "sample": f"one full {CONFIG} treecode_sum (unmodified reference, "
                                               f"workers={cores}), {dt:.1f} s"}
             line["parity_rel_l2_vs_reference"] = ol.rel_l2(mine, ref_out)
