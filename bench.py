@@ -317,7 +317,12 @@ def run_gpu(args):
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
-    all_evals = sum(stats.kernel_evals)
+    all_evals = sum(stats.kernel_evals)  # this rank's part of the work
+    job_evals = all_evals
+    if ws > 1:  # whole-job interactions/s: every rank's part
+        t = torch.tensor([float(all_evals)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+        job_evals = float(t.item())
     # upward / downward passes: algorithmic flops per
     # (particle, node) visit plus the p x p transforms per node; bytes as
     # stated there. Timed by the same events as phase_ms (upward includes
@@ -358,7 +363,7 @@ def run_gpu(args):
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xyz.nbytes + q.nbytes),
                 "d2h_bytes_per_step": int(n * 3 * 8), "ms_per_step": e2e_s * 1e3},
         "gpu_launches": launches,
-        "interactions_per_s": all_evals / (ms_per_step * 1e-3),
+        "interactions_per_s": job_evals / (ms_per_step * 1e-3),
         "all_kernel_flops_frac": FLOP_PER_PAIR * all_evals / (ms_per_step * 1e-3) / 1e12 / peak,
         "phase_ms": {"bin": stats.bin_seconds * 1e3, "traversal": stats.traversal_seconds * 1e3,
                      "eval": stats.eval_seconds * 1e3, "upward": stats.upward_ms, "cp_cc_fit": stats.cp_cc_fit_ms,
