@@ -344,6 +344,66 @@ __device__ __forceinline__ bool near_possible(int leaf, int s, const double* __r
   return fma(dx, dx, fma(dy, dy, dz * dz)) < lim * lim;
 }
 
+// Warp-cooperative append of one round of ranges (lane order = list order)
+// to a tile's range list. A range that continues the previous one in memory
+// with the same near flag is merged into it: the flattened source sequence
+// is unchanged, the list (and the kernels' binary searches) shorter —
+// sibling leaves' bins and sibling nodes' proxy blocks are contiguous.
+// Returns this lane's flattened-list prefix (valid for selected lanes).
+struct ListCursor {
+  int w = 0;          // ranges written
+  int src = 0;        // flattened sources so far
+  int last_end = -1;  // end (begin + count) and near flag of the last range
+  int last_near = -1;
+};
+__device__ __forceinline__ int append_ranges(bool sel, const SrcRange& r, SrcRange* __restrict__ out,
+                                             ListCursor& cur, int lane) {
+  const unsigned full = 0xffffffffu;
+  const unsigned bal = __ballot_sync(full, sel);
+  const int cnt = sel ? r.count : 0;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(full, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int excl = incl - cnt;
+  const int total = __shfl_sync(full, incl, 31);
+  const int end = r.begin + r.count;
+  const unsigned below = bal & ((1u << lane) - 1u);
+  const int pl = below ? 31 - __clz(below) : -1;  // previous selected lane
+  const int pend = __shfl_sync(full, end, pl < 0 ? 0 : pl);
+  const int pnear = __shfl_sync(full, r.near, pl < 0 ? 0 : pl);
+  const int prev_end = pl < 0 ? cur.last_end : pend, prev_near = pl < 0 ? cur.last_near : pnear;
+  const bool cont = sel && (pl >= 0 || cur.w > 0) && prev_end == r.begin && prev_near == r.near;
+  const bool head = sel && !cont;
+  const unsigned hb = __ballot_sync(full, head);
+  const unsigned after = hb & ~((2u << lane) - 1u);  // heads after this lane (none for lane 31)
+  const int nh = after ? __ffs(after) - 1 : -1;
+  const int nh_excl = __shfl_sync(full, excl, nh < 0 ? 0 : nh);
+  if (head) {
+    SrcRange h = r;
+    h.count = (nh < 0 ? total : nh_excl) - excl;  // this range and its continuations
+    h.pad = cur.src + excl;
+    out[cur.w + __popc(hb & ((1u << lane) - 1u))] = h;
+  }
+  // continuations before this round's first head extend the last range
+  const int fh = hb ? __ffs(hb) - 1 : -1;
+  const int lead = fh < 0 ? total : __shfl_sync(full, excl, fh);
+  __syncwarp();
+  if (lane == 0 && lead > 0) out[cur.w - 1].count += lead;
+  __syncwarp();
+  const int ls = bal ? 31 - __clz(bal) : -1;  // last selected lane
+  if (ls >= 0) {
+    cur.last_end = __shfl_sync(full, end, ls);
+    cur.last_near = __shfl_sync(full, r.near, ls);
+  }
+  const int pad = cur.src + excl;
+  cur.w += __popc(hb);
+  cur.src += total;
+  return pad;
+}
+
 // Range list of one leaf, one warp per leaf: PP and PC entries of every node
 // on its root-to-leaf path (treecode.cpp:379-396), near-possible PP ranges
 // first, each pass in path order (root to leaf, segment order within a
@@ -386,7 +446,8 @@ __global__ void __launch_bounds__(32 * kFillWarps)
     const int T = sbeg[wid][pl];
     const int offl = off[leaf];
     const int w0 = range_off[k];
-    int w = 0, src = 0, src_pp = 0, src_pc = 0, near_total = 0, self_shift = 0, has_self = 0;
+    ListCursor cur;
+    int src_pp = 0, src_pc = 0, near_total = 0, self_shift = 0, has_self = 0;
     for (int pass = 0; pass < 2; ++pass) {  // 0: near-possible PP ranges, 1: the rest
       for (int base = 0; base < T; base += 32) {
         const int idx = base + lane;
@@ -414,30 +475,19 @@ __global__ void __launch_bounds__(32 * kFillWarps)
             }
           }
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, sel);
-        int incl = cpp + cpc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        if (sel) {
-          r.pad = src + incl - (cpp + cpc);  // flattened-list prefix
-          ranges[w0 + w + __popc(bal & ((1u << lane) - 1u))] = r;
-        }
+        r.pad = append_ranges(sel, r, ranges + w0, cur, lane);  // flattened-list prefix
         const unsigned sb = __ballot_sync(0xffffffffu, self);
         if (sb) {
           const int sl = __ffs(sb) - 1;
           self_shift = __shfl_sync(0xffffffffu, r.pad - r.begin, sl);
           has_self = 1;
         }
-        w += __popc(bal);
-        src += __shfl_sync(0xffffffffu, incl, 31);
         src_pp += __reduce_add_sync(0xffffffffu, cpp);
         src_pc += __reduce_add_sync(0xffffffffu, cpc);
       }
-      if (pass == 0) near_total = src;
+      if (pass == 0) near_total = cur.src;
     }
+    const int w = cur.w;
     const int c = cnt[leaf];
     const int nt = (c + kTileTargets - 1) / kTileTargets;
     for (int j = lane; j < nt; j += 32) {
@@ -492,10 +542,11 @@ __global__ void __launch_bounds__(32 * kFillWarps)
     const int t = fit_nodes[k];
     const int2 sg = seg[2 * t + 1];
     const int w0 = range_off[k];
-    int pre = 0, ncp = 0, ncc = 0;
+    ListCursor cur;
+    int ncp = 0, ncc = 0;
     for (int base = sg.x; base < sg.y; base += 32) {
       const int i = base + lane;
-      int cv = 0, is_cp = 0, is_cc = 0;
+      int is_cp = 0, is_cc = 0;
       SrcRange r{0, 0, 0, 0};
       if (i < sg.y) {
         const int4 it = E[sorted_e[i]];
@@ -508,19 +559,8 @@ __global__ void __launch_bounds__(32 * kFillWarps)
           r.count = P;
           is_cc = 1;
         }
-        cv = r.count;
       }
-      int incl = cv;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      if (i < sg.y) {
-        r.pad = pre + incl - cv;  // flattened-list prefix
-        ranges[w0 + (i - sg.x)] = r;
-      }
-      pre += __shfl_sync(0xffffffffu, incl, 31);
+      append_ranges(i < sg.y, r, ranges + w0, cur, lane);
       ncp += __reduce_add_sync(0xffffffffu, is_cp);
       ncc += __reduce_add_sync(0xffffffffu, is_cc);
     }
@@ -529,7 +569,7 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       tl.tgt_begin = static_cast<int>(N + static_cast<int64_t>(pslot[t]) * P);
       tl.tgt_count = P;
       tl.list_begin = w0;
-      tl.list_end = w0 + (sg.y - sg.x);
+      tl.list_end = w0 + cur.w;
       tl.near_total = 0;  // CP / CC pairs are well separated
       tl.self_shift = tl.has_self = tl.pad = 0;
       tiles[k] = tl;
