@@ -90,6 +90,11 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   tr.mark("bin.done");
   const auto t1 = clk::now();
+  struct Unrestrict {  // the restriction is this evaluation's only (exports list everything)
+    Ctx& c;
+    ~Unrestrict() { c.restrict_on = false; }
+  } unrestrict{c};
+  plan_restriction(c);
   traverse_and_build_lists(c, cfg, false);
   tr.mark("lists.done");
   const auto t2 = clk::now();

@@ -174,6 +174,7 @@ struct Lists {
   bool fit_sel_all = true;
   uint64_t local_evals[4] = {0, 0, 0, 0};
   bool counts_pending = false;   // counts/evals still in flight (finalize_counts)
+  bool local_is_all = true;      // this part's work = all listed work (one part, or restricted lists)
 };
 
 // Breadth-first traversal frontier entry: node pair plus depth-first order key.
@@ -212,6 +213,18 @@ struct Ctx {
   std::string last_error;
   int call_index = 0;
   int part = 0, nparts = 1;  // target partition (multi-GPU)
+  // Restricted multi-part evaluation (traversal.cu plan_restriction): the
+  // cost-balanced cut positions of the last full multi-part call, and — once
+  // they exist — this call's tree-position range and leaf-index range; the
+  // traversal then only follows pairs whose target bin meets the range.
+  struct Cuts {
+    int64_t n = -1;
+    int nparts = 0;
+    std::vector<int64_t> pos;  // nparts + 1 tree positions
+  } cuts;
+  bool restrict_on = false;
+  int64_t rp0 = 0, rp1 = 0;
+  int rl0 = 0, rl1 = 0;
   HostTree host;
   NodeTable nodes;
   Binned bins;
@@ -275,6 +288,7 @@ void tree_init_roots(Ctx& c);
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
 void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
 void partition_targets(Ctx& c);
+bool plan_restriction(Ctx& c);  // multi-part: restrict this call's lists to the part's targets
 void build_lists(Ctx& c, const ssum_config& cfg);
 void finalize_counts(Ctx& c);
 std::vector<int> reference_ids(const HostTree& h);

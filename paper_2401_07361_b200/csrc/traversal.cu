@@ -49,13 +49,17 @@ __device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_o
 }
 
 // action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
-__device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__ cnt,
-                                           const double* __restrict__ center, const double* __restrict__ radius,
-                                           const int* __restrict__ level, const int* __restrict__ child_base,
-                                           double theta, int thr, int max_depth, int pc_only) {
+// [rlo, rhi): the tree-position range whose targets this call evaluates
+// (restricted multi-part call; [0, INT_MAX) otherwise): a pair whose target
+// bin misses it only feeds other parts' targets and is dropped.
+__device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__ cnt, const int* __restrict__ off,
+                                           int rlo, int rhi, const double* __restrict__ center,
+                                           const double* __restrict__ radius, const int* __restrict__ level,
+                                           const int* __restrict__ child_base, double theta, int thr, int max_depth,
+                                           int pc_only) {
   const int ct = cnt[t], cs = cnt[s];
   int a = 0;
-  if (ct > 0 && cs > 0) {
+  if (ct > 0 && cs > 0 && off[t] < rhi && off[t] + ct > rlo) {
     const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
     const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
     const double R = arc_dist(a3, b3);
@@ -106,7 +110,8 @@ __device__ __forceinline__ void pair_scatter(const PairEntry& p, int a, unsigned
 // decide every frontier pair; packed[k] = (emits << 32) | child slots, and
 // packed[m] = 0 so that the exclusive scan's entry m is the total.
 __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* __restrict__ cnt,
-                            const double* __restrict__ center, const double* __restrict__ radius,
+                            const int* __restrict__ off, int rlo, int rhi, const double* __restrict__ center,
+                            const double* __restrict__ radius,
                             const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr,
                             int max_depth, int pc_only, int* __restrict__ action,
                             unsigned long long* __restrict__ packed) {
@@ -116,7 +121,8 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
     packed[k] = 0;
     return;
   }
-  const int a = pair_action(F[k].t, F[k].s, cnt, center, radius, level, child_base, theta, thr, max_depth, pc_only);
+  const int a = pair_action(F[k].t, F[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
+                            max_depth, pc_only);
   action[k] = a;
   packed[k] = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
 }
@@ -158,7 +164,8 @@ constexpr int kBfsThreads = 256;
 #define SSUM_BFS_MINB 1
 #endif
 __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
-    k_bfs(const int* __restrict__ cnt, const double* __restrict__ center, const double* __restrict__ radius,
+    k_bfs(const int* __restrict__ cnt, const int* __restrict__ off, int rlo, int rhi,
+          const double* __restrict__ center, const double* __restrict__ radius,
           const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr, int max_depth,
           int pc_only, PairEntry* F0, PairEntry* F1, int fcap, int4* __restrict__ E,
           unsigned long long* __restrict__ K, long long ecap, int* __restrict__ action,
@@ -185,8 +192,8 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
       const int k = base + tid;
       unsigned long long v = 0;
       if (k < hi) {
-        const int a = pair_action(Fc[k].t, Fc[k].s, cnt, center, radius, level, child_base, theta, thr,
-                                  max_depth, pc_only);
+        const int a = pair_action(Fc[k].t, Fc[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta,
+                                  thr, max_depth, pc_only);
         action[k] = a;
         v = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
       }
@@ -613,6 +620,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
   k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
+  const int rlo = c.restrict_on ? static_cast<int>(c.rp0) : 0;
+  const int rhi = c.restrict_on ? static_cast<int>(c.rp1) : 0x7fffffff;
   int m = 400;
   long long ne = 0;
   L.inter.ensure(1 << 16);
@@ -623,7 +632,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
     S.action.ensure(size_t(m) + 1);
     S.packed.ensure(size_t(m) + 1);
     S.scan.ensure(size_t(m) + 1);
-    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, c.nodes.center.p, c.nodes.radius.p,
+    k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, B.off.p, rlo, rhi, c.nodes.center.p,
+                                                           c.nodes.radius.p,
                                                            c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
                                                            cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
                                                            S.packed.p);
@@ -689,6 +699,9 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   k_root_pairs<<<2, 256, 0, c.stream>>>(S.F0.p);
   SSUM_LAUNCH_CHECK();
   const int* cnt = B.cnt.p;
+  const int* off = B.off.p;
+  int rlo = c.restrict_on ? static_cast<int>(c.rp0) : 0;
+  int rhi = c.restrict_on ? static_cast<int>(c.rp1) : 0x7fffffff;
   const double *center = c.nodes.center.p, *radius = c.nodes.radius.p;
   const int *level = c.nodes.level.p, *child_base = c.nodes.child_base.p;
   double theta = cfg.theta;
@@ -701,7 +714,8 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   int* out = S.dm.p;
   long long* ne = S.debase.p;
   int* flags = c.d_flags.p;
-  void* args[] = {&cnt, &center, &radius, &level, &child_base, &theta, &thr, &max_depth, &pc_only, &f0, &f1,
+  void* args[] = {&cnt, &off, &rlo, &rhi, &center, &radius, &level, &child_base, &theta, &thr, &max_depth,
+                  &pc_only, &f0, &f1,
                   &fcap, &e, &k, &ecap, &action, &loc, &btot, &out, &ne, &flags};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs), dim3(nb), dim3(kBfsThreads), args, 0, c.stream) !=
       cudaSuccess) {
@@ -835,7 +849,9 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
 
   trace().mark("lists.group_slots");
   // ---- range and tile counts for leaves and fit nodes, one read-back
-  const int nl = B.n_leaves;
+  // leaves to build tiles for: all of them, or this part's (restricted call)
+  const int* leaves = B.d_leaves.p + (c.restrict_on ? c.rl0 : 0);
+  const int nl = c.restrict_on ? c.rl1 - c.rl0 : B.n_leaves;
   const int nf = L.n_fit;
   S.nr.ensure(size_t(nl) + 1);
   S.nt.ensure(size_t(nl) + 1);
@@ -846,8 +862,8 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.nr.p + nl, 0, 4, c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.nt.p + nl, 0, 4, c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(S.fnr.p + nf, 0, 4, c.stream));
-  k_leaf_count<<<grid_for(nl, 128), 128, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, B.cnt.p, S.nr.p,
-                                                         S.nt.p);
+  k_leaf_count<<<grid_for(std::max(nl, 1), 128), 128, 0, c.stream>>>(leaves, nl, c.nodes.parent.p, S.seg.p, B.cnt.p,
+                                                                      S.nr.p, S.nt.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   exclusive_scan(c, S.nr.p, S.nr_off.p, nl + 1);
@@ -873,7 +889,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   L.leaf_ranges.ensure(size_t(std::max<int64_t>(L.n_leaf_ranges, 1)));
   L.leaf_tiles.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
   L.leaf_cost.ensure(size_t(std::max(L.n_leaf_tiles, 1)));
-  k_leaf_fill<<<grid_for(nl, kFillWarps), 32 * kFillWarps, 0, c.stream>>>(B.d_leaves.p, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
+  k_leaf_fill<<<grid_for(std::max(nl, 1), kFillWarps), 32 * kFillWarps, 0, c.stream>>>(leaves, nl, c.nodes.parent.p, S.seg.p, S.sorted_e.p,
                                                         L.inter.p, B.cnt.p, B.off.p, L.pslot.p, c.nodes.center.p,
                                                         c.nodes.radius.p, S.nr_off.p, S.nt_off.p, N, P,
                                                         L.leaf_ranges.p, L.leaf_tiles.p, L.leaf_cost.p,
@@ -922,9 +938,54 @@ void finalize_counts(Ctx& c) {
   }
   L.visits[0] = h[10];
   L.visits[1] = h[11];
-  if (c.nparts <= 1)
+  if (L.local_is_all)
     for (int k = 0; k < 4; ++k) L.local_evals[k] = L.evals[k];
   L.counts_pending = false;
+}
+
+// First leaf (depth-first index) starting at or after tree position x, for
+// the two cut positions of this part: [0] p0, [1] p1, [2] l0, [3] l1.
+__global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* __restrict__ off, long long n,
+                            long long x0, long long x1, long long* out) {
+  if (threadIdx.x >= 2) return;
+  const long long x = threadIdx.x == 0 ? x0 : x1;
+  int lo = 0, hi = nl;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (off[leaves[mid]] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  out[threadIdx.x] = lo < nl ? off[leaves[lo]] : n;
+  out[2 + threadIdx.x] = lo;
+}
+
+// Restricted multi-part call: once a full multi-part call has placed the
+// cost-balanced cuts (partition_targets), later calls with the same N and
+// part count snap those positions to leaf starts of the current binning and
+// traverse / build lists for this part's targets only. The lists of a target
+// are the same pairs in the same order as in the full traversal (dropping
+// pairs keeps the relative emission order), so the union of the parts stays
+// bitwise the single-part result.
+bool plan_restriction(Ctx& c) {
+  c.restrict_on = false;
+  const Binned& B = c.bins;
+  if (c.nparts <= 1 || c.cuts.n != B.n || c.cuts.nparts != c.nparts || B.n_leaves == 0) return false;
+  long long* d_out = reinterpret_cast<long long*>(c.d_flags.p + 40);  // ints [40, 48)
+  k_snap_cuts<<<1, 32, 0, c.stream>>>(B.d_leaves.p, B.n_leaves, B.off.p, B.n, c.cuts.pos[size_t(c.part)],
+                                      c.cuts.pos[size_t(c.part) + 1], d_out);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+  long long h[4];
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.rp0 = h[0];
+  c.rp1 = h[1];
+  c.rl0 = static_cast<int>(h[2]);
+  c.rl1 = static_cast<int>(h[3]);
+  c.restrict_on = true;
+  return true;
 }
 
 // Multi-GPU target partition: leaf tiles are in depth-first
@@ -947,7 +1008,15 @@ void partition_targets(Ctx& c) {
   L.local_evals[1] = L.evals[1];
   L.local_evals[2] = L.evals[2];
   L.local_evals[3] = L.evals[3];
-  if (c.nparts <= 1 || L.n_leaf_tiles == 0) return;
+  L.local_is_all = true;
+  if (c.nparts <= 1) return;
+  if (c.restrict_on) {  // the lists hold exactly this part's targets
+    L.p0 = c.rp0;
+    L.p1 = c.rp1;
+    return;
+  }
+  L.local_is_all = false;
+  if (L.n_leaf_tiles == 0) return;
   const int nt = L.n_leaf_tiles;
   std::vector<ulonglong2> cost(static_cast<size_t>(nt));
   std::vector<Tile> tiles(static_cast<size_t>(nt));
@@ -960,11 +1029,16 @@ void partition_targets(Ctx& c) {
   std::vector<double> pre(static_cast<size_t>(nt) + 1, 0.0);
   for (int t = 0; t < nt; ++t) pre[size_t(t) + 1] = pre[size_t(t)] + double(cost[size_t(t)].x + cost[size_t(t)].y) + 1.0;
   const double total = pre[size_t(nt)];
+  // cut before the first tile at or after the cost goal that starts a leaf
+  // (a leaf's tiles share list_begin): parts never split a leaf, so the
+  // positions are leaf starts, as restricted calls' snapped cuts are
   auto cut = [&](int r) {
     if (r <= 0) return 0;
     if (r >= c.nparts) return nt;
     const double goal = total * r / c.nparts;
-    return static_cast<int>(std::lower_bound(pre.begin(), pre.end(), goal) - pre.begin());
+    int t = static_cast<int>(std::lower_bound(pre.begin(), pre.end(), goal) - pre.begin());
+    while (t > 0 && t < nt && tiles[size_t(t)].list_begin == tiles[size_t(t) - 1].list_begin) ++t;
+    return std::min(t, nt);
   };
   const int t0 = std::min(cut(c.part), nt), t1 = std::max(std::min(cut(c.part + 1), nt), t0);
   L.leaf_t0 = t0;
@@ -979,6 +1053,14 @@ void partition_targets(Ctx& c) {
   for (int t = t0; t < t1; ++t) {
     L.local_evals[0] += cost[size_t(t)].x;
     L.local_evals[1] += cost[size_t(t)].y;
+  }
+  // the cut positions of every part, for the next (restricted) calls
+  c.cuts.n = N;
+  c.cuts.nparts = c.nparts;
+  c.cuts.pos.assign(size_t(c.nparts) + 1, N);
+  for (int r = 0; r <= c.nparts; ++r) {
+    const int ct = std::min(cut(r), nt);
+    c.cuts.pos[size_t(r)] = ct < nt ? tiles[size_t(ct)].tgt_begin : N;
   }
   std::vector<int> fit_nodes(static_cast<size_t>(L.n_fit_tiles));
   if (L.n_fit_tiles > 0) {

@@ -1,0 +1,46 @@
+"""Device time of one rank's share of a config-4 evaluation at G parts:
+every part's call is timed on this GPU in turn (after the first full call has
+placed the cost-balanced cuts, each part bins, traverses and lists its own
+targets only). The max over parts approximates one G-GPU step before the row
+all-gather; nothing here waits on another rank.
+
+    python tools/part_bench.py [G ...]
+"""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2401_07361_b200 as ss  # noqa: E402
+
+parts = [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]
+xyz, area = ss.make_icosa_mesh(9)
+q = ss.rh4_vorticity(xyz) * area
+n = xyz.shape[0]
+dev = torch.device("cuda", 0)
+d_xyz = torch.from_numpy(xyz).to(dev)
+d_q = torch.from_numpy(q).to(dev)
+d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+res = {}
+for G in parts:
+    tree = ss.FaceTree(0)
+    tree.set_stream(torch.cuda.current_stream().cuda_stream)
+    per = []
+    for r in range(G):
+        tree.set_partition(r, G)
+        for _ in range(3):  # warm-up (the first call of part 0 places the cuts)
+            ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
+                                   d_out.data_ptr())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
+                                   d_out.data_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        per.append(e0.elapsed_time(e1) / 5)
+    res[G] = {"max_part_ms": max(per), "min_part_ms": min(per), "parts_ms": per}
+    print(json.dumps({"G": G, **res[G]}), flush=True)
