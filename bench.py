@@ -426,9 +426,17 @@ def sampled_direct_error(xyz, q, u_tree, dev, u_ref=None, m=2048, seed=2024):
         ut = torch.from_numpy(np.ascontiguousarray(u[idx])).to(dev)
         return float(torch.linalg.norm(ut - u_dir) / torch.linalg.norm(u_dir))
 
-    return {"value": rel(u_tree), "reference_same_targets": rel(u_ref) if u_ref is not None else None,
-            "targets": int(len(idx)), "seed": seed, "survey_reference_E_config4": 2.38e-6,
-            "definition": "||u_tree - u_direct||_2 / ||u_direct||_2 over the sampled targets"}
+    e_tree = rel(u_tree)
+    e_ref = rel(u_ref) if u_ref is not None else None
+    out = {"value": e_tree, "reference_same_targets": e_ref,
+           "targets": int(len(idx)), "seed": seed, "survey_reference_E_config4": 2.38e-6,
+           "definition": "||u_tree - u_direct||_2 / ||u_direct||_2 over the sampled targets"}
+    if e_ref is not None:
+        # the two tree codes agree to ~1e-13 (parity), so E differs only in
+        # rounding: "no worse" is judged to 1e-6 relative, as in the tests
+        out["relative_difference"] = (e_tree - e_ref) / e_ref
+        out["not_worse_than_reference"] = bool(e_tree <= e_ref * (1 + 1e-6))
+    return out
 
 
 def main():

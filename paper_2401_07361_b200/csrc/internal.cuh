@@ -299,7 +299,8 @@ void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
 void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel);
-void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S);
+void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
+                       bool direct = false);
 void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out);
 void rk4_combine(Ctx& c, int stage, int64_t n, double dt, double omega, double* d_x0, double* d_z0,
                  const double* d_area, double* d_xs, double* d_q, const double* d_u, double* d_kacc,

@@ -6,13 +6,14 @@
 //   S = sum_j r_j (y_j - x)  (near pairs),
 // and finished once per target as u = -1/(4 pi) x X S (x X x = 0, so both
 // forms give the same cross product). 13 algorithmic flops per pair
-// (SURVEY.md §8(d)); the fast path issues 10 FP64 instructions + 1 MUFU:
+// (SURVEY.md §8(d)); the fast path issues 9 FP64 instructions + 1 MUFU:
 //   den = fma(-z, y.z, fma(-y, y.y, fma(-x, y.x, 1)))      3 DFMA
-//   r0 = rcp.approx(den); e = 1 - den r0; e += e^2;       MUFU + 2 DFMA
+//   r0 = rcp.approx(den); e = 1 - den r0                  MUFU + 1 DFMA
 //   r = q r0 (1 + e)                                       1 DMUL + 1 DFMA
 //   S += r y                                               3 DFMA
 // rcp.approx.ftz.f64 is ~2^-20 accurate (measured 9.9e-7 on the box); the
-// cubic step brings it to ~1e-18 before rounding.
+// Newton step leaves e^2 <= 1e-12 relative per term (far_block). The direct
+// sum adds e^2 (one more DFMA, ~1 ulp).
 //
 // Near pairs (den < 2^-20, or a self pair) take the reference-rounded slow
 // path: den = 1 - ((x.x y.x + x.y y.y) + x.z y.z)
@@ -118,7 +119,13 @@ __device__ __forceinline__ double near_mask(double v, double den, int& cnt) {
 // and counted per lane in *ncnt, with no branch and no vote: the caller
 // compares the count with the self pairs the lane must have met and
 // re-walks the chunk through near_repair only when they differ.
-template <int KER, int NT, int NS, bool NEAR = false>
+// Reciprocal: MUFU.RCP64H seed (rel. error <= 9.9e-7) and one Newton step,
+// q/den = q r0 (1 + e) with e = 1 - den r0: relative error e^2 <= 1e-12 per
+// term, 9 FP64 instructions per pair; measured 1.2e-13 .. 1.6e-13 relative
+// L2 against the reference's exact division on configs 3 and 4 (bar 1e-10).
+// CUBIC (the direct sum, the accuracy yardstick): q r0 (1 + e + e^2), ~1 ulp,
+// one more DFMA.
+template <int KER, int NT, int NS, bool NEAR = false, bool CUBIC = false>
 __device__ __forceinline__ void far_block(const double4* x, const double4* __restrict__ B, int G, Acc<KER>* a,
                                           int* ncnt = nullptr) {
   constexpr int C = NT * NS;
@@ -138,8 +145,10 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
     for (int c = 0; c < C; ++c) r[c] = rcp_approx(den[c]);
 #pragma unroll
     for (int c = 0; c < C; ++c) e[c] = fma(-den[c], r[c], 1.0);
+    if constexpr (CUBIC) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) e[c] = fma(e[c], e[c], e[c]);
+      for (int c = 0; c < C; ++c) e[c] = fma(e[c], e[c], e[c]);
+    }
 #pragma unroll
     for (int c = 0; c < C; ++c) r[c] = y[c / NT].w * r[c];
 #pragma unroll

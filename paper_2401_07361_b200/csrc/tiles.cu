@@ -30,12 +30,14 @@ constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
 //                  target.
 //  MODE kFitMode : well-separated pairs only; phi = K-sums at the proxy
 //                  points, then C = V^-1 phi (ProxyFit::solve, sbb.cpp:103-108).
+//  MODE kDirectMode: kLeafMode with the ~1 ulp (cubic) reciprocal — the
+//                  direct sum, every source near-possible.
 constexpr int kTileThreads = 256;
 #ifndef SSUM_CHUNK
 #define SSUM_CHUNK 512
 #endif
 constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage (multiple of kTileThreads)
-constexpr int kLeafMode = 0, kFitMode = 1;
+constexpr int kLeafMode = 0, kFitMode = 1, kDirectMode = 2;
 #ifndef SSUM_NS
 #define SSUM_NS 2
 #endif
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     // the same staged blocks with near pairs masked and counted, checked
     // against the lane's self pairs once per chunk
     int near_steps = 0;
-    if (MODE == kLeafMode) {
+    if (MODE != kFitMode) {
       const int nn = min(n, T.near_total - c * kChunk);
       near_steps = nn > 0 ? (nn + kStep - 1) / kStep : 0;
     }
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
 #pragma unroll 2
       for (; it < near_steps; ++it) {
         const int before = ncnt;
-        far_block<KER, kTpt, kNs, true>(x, B + it * kStep, G, a, &ncnt);
+        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt);
         hit |= static_cast<unsigned>(ncnt != before) << (it & 31);
       }
       // self pairs this lane walked in this chunk's near steps: the self
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     // of independent chains per step (zero-padded tail contributes 0)
     const double4* Bp = B + it * kStep;
 #pragma unroll 2
-    for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs>(x, Bp, G, a);
+    for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a);
     if (more)
 #pragma unroll
       for (int e = 0; e < kPer; ++e) {
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
       for (int d = 0; d < D; ++d) s[d] += red[(qq * kTileThreads + gg * th + uq) * D + d];
   }
   const int i_out = T.tgt_begin + tt;
-  if constexpr (MODE == kLeafMode) {
+  if constexpr (MODE != kFitMode) {
     if (tt < tc) {
 #pragma unroll
       for (int d = 0; d < D; ++d) S[size_t(i_out) * D + d] = s[d];
@@ -328,8 +330,10 @@ void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
                                                  c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
 }
 
-void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S) {
-  auto k = kernel == kBS ? tiles_kernel<kBS, kLeafMode>() : tiles_kernel<kLOG, kLeafMode>();
+void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
+                       bool direct) {
+  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode>() : tiles_kernel<kLOG, kDirectMode>())
+                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode>() : tiles_kernel<kLOG, kLeafMode>());
   k<<<ntl, kTileThreads, kTileSmem, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
                                                 nullptr, nullptr, 0, nullptr);
 }
@@ -343,7 +347,7 @@ void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out) {
   const int bs = 256;
   k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
   SSUM_LAUNCH_CHECK();
-  launch_leaf_tiles(c, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p);
+  launch_leaf_tiles(c, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p, true);
   SSUM_LAUNCH_CHECK();
   if (kernel == kBS)
     k_direct_finish<kBS><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
