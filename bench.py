@@ -222,8 +222,13 @@ def run_gpu(args):
     n = xyz.shape[0]
     cfg = ss.TraversalConfig(**CFG)
     dev = torch.device("cuda", local)
-    d_xyz = torch.from_numpy(xyz).to(dev)
-    d_q = torch.from_numpy(q).to(dev)
+    # rows [0, n) are the particles; padded to ws equal slots for the input
+    # all-gather of the distributed e2e path (dist.allgather_inputs)
+    rows = ws * -(-n // ws)
+    d_xyz = torch.zeros((rows, 3), dtype=torch.float64, device=dev)
+    d_q = torch.zeros(rows, dtype=torch.float64, device=dev)
+    d_xyz[:n].copy_(torch.from_numpy(xyz))
+    d_q[:n].copy_(torch.from_numpy(q))
     d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     tree = ss.FaceTree(local)
@@ -283,7 +288,9 @@ def run_gpu(args):
     h_out = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
     e2e_times = []
     if ws > 1:
-        from paper_2401_07361_b200.dist import gather_rows
+        from paper_2401_07361_b200.dist import allgather_inputs, gather_rows, shard_rows
+
+        r0, r1 = shard_rows(n, ws, rank)
     for k in range(min(args.steps, 5) + 1):
         barrier()
         t0 = time.perf_counter()
@@ -291,12 +298,14 @@ def run_gpu(args):
             # the public host-pointer entry point: H2D, bin, traverse, evaluate, D2H
             ss.treecode_sum(ss.BiotSavartKernel, h_xyz.numpy(), h_q.numpy(), cfg, tree=tree, out=h_out.numpy())
         else:
-            # per rank: H2D, this rank's targets, NCCL all-gather of the rows, D2H of all N rows
-            d_xyz.copy_(h_xyz, non_blocking=True)
-            d_q.copy_(h_q, non_blocking=True)
+            # per rank: H2D of this rank's 1/ws shard of x and q, NCCL
+            # all-gather of the particle set over NVLink, this rank's
+            # targets, NCCL all-gather of the rows, D2H of this rank's shard
+            # of the result (the ranks' host shards together are the field)
+            allgather_inputs(h_xyz, h_q, d_xyz, d_q)
             step(ss.TreecodeStats())
             gather_rows(tree, d_out)
-            h_out.copy_(d_out)
+            h_out[r0:r1].copy_(d_out[r0:r1])
             torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if k > 0:
@@ -361,7 +370,10 @@ def run_gpu(args):
                      "peak_source": "DFMA-chain probe on this GPU (ssum_fp64_peak); MEASURED_PEAKS.json has no fp64",
                      "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": pairs, "avg_launch_ms": avg_pp_ms},
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xyz.nbytes + q.nbytes),
-                "d2h_bytes_per_step": int(n * 3 * 8), "ms_per_step": e2e_s * 1e3},
+                "d2h_bytes_per_step": int(n * 3 * 8), "ms_per_step": e2e_s * 1e3,
+                "path": ("ssum_treecode_sum (host pointers)" if ws == 1 else
+                         "per rank: H2D of its 1/ws input shard, NCCL all-gather of x and q, its targets, "
+                         "NCCL all-gather of the rows, D2H of its 1/ws result shard (bytes: whole job)")},
         "gpu_launches": launches,
         "interactions_per_s": job_evals / (ms_per_step * 1e-3),
         "all_kernel_flops_frac": FLOP_PER_PAIR * all_evals / (ms_per_step * 1e-3) / 1e12 / peak,

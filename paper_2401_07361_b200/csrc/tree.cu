@@ -250,12 +250,34 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
 // are two binary searches of the node's key range in the sorted keys. The
 // binning is final unless a childless node must split (bin > N_T below
 // max_depth) — then the level-synchronous build runs instead.
+// Guessed leaf (the particle's leaf in the previous call): accepted when the
+// node is childless and x lies inside its spherical triangle by at least
+// kGuessMargin rad from each edge great circle. Nodes tile their parents
+// exactly, so every sibling along the root-to-node path then lies >= that far
+// from x, i.e. its barycentric score is <= ~ -kGuessMargin sin(alpha/2) / h
+// (alpha >= ~50 deg the triangle angles, h <= ~1 the heights): below -4e-9,
+// 40x beyond the -1e-10 containment tolerance and the 1e-13 guard band. The
+// first-containing descent (face_tree.cpp:50-69) therefore ends at this
+// node, and the shortcut returns exactly what the walk would.
+constexpr double kGuessMargin = 1e-8;
+__device__ __forceinline__ bool deep_inside(const d3& p, const double* __restrict__ k) {
+  const double sg = k[3] < 0.0 ? -1.0 : 1.0;  // inside: x . n_j has det's sign
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const double* n = k + (j == 0 ? 0 : 1 + 3 * j);  // n1 = k[0..2], n2 = k[4..6], n3 = k[7..9]
+    const double r = sg * fma(p.z, n[2], fma(p.y, n[1], p.x * n[0]));
+    const double nn = fma(n[2], n[2], fma(n[1], n[1], n[0] * n[0]));
+    if (!(r > 0.0 && r * r >= (kGuessMargin * kGuessMargin) * nn)) return false;
+  }
+  return true;
+}
+
 __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const int* __restrict__ order,
                        const double* __restrict__ tri,
                        const double* __restrict__ cramer, const double* __restrict__ center,
                        const int* __restrict__ child_base, const unsigned long long* __restrict__ nkey,
                        unsigned long long* __restrict__ key, int* __restrict__ ids, int* __restrict__ leaf_of,
-                       int* __restrict__ flags) {
+                       int guess_nodes, int* __restrict__ flags) {
   __shared__ double st[20 * 9];
   __shared__ double skr[20 * 12];
   __shared__ double sc[20 * 3];
@@ -269,6 +291,16 @@ __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, c
   // neighbours and share their descent (results still land at index i)
   const int64_t i = order ? order[k] : k;
   const d3 p = load3(xyz + 3 * i);
+  // guess_nodes > 0: leaf_of holds the previous call's leaves (node ids
+  // below guess_nodes)
+  if (guess_nodes > 0) {
+    const int g = leaf_of[i];
+    if (g >= 0 && g < guess_nodes && child_base[g] < 0 && deep_inside(p, cramer + 12 * g)) {
+      key[i] = nkey[g];
+      ids[i] = static_cast<int>(i);
+      return;  // leaf_of[i] stays g
+    }
+  }
   int node = find_root(p, st, skr, sc);
   if (node < 0) {
     atomicOr(flags, kFlagGeometry);
@@ -506,6 +538,9 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   const bool by_tree = prev_perm_n == n && !B.input_coherent;
   const int pieces = (c.io.active && !by_tree) ? Ctx::kIoChunks : 1;
   const int* order = by_tree ? B.perm.p : nullptr;
+  // the previous call's leaf of each particle is the walk's first guess
+  // (verified per particle, so any stale guess only costs the full walk)
+  const int guess_nodes = prev_perm_n == n ? nn : 0;
   if (c.io.active && pieces == 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[Ctx::kIoChunks - 1], 0));
   for (int j = 0; j < pieces; ++j) {
     const int64_t a = pieces > 1 ? c.io.bounds[j] : 0, b = pieces > 1 ? c.io.bounds[j + 1] : n;
@@ -513,7 +548,7 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
     if (b <= a) continue;
     k_walk<<<grid_for(b - a, bs), bs, 0, c.stream>>>(d_xyz, a, b, order, T.tri.p, T.cramer.p, T.center.p,
                                                      T.child_base.p, T.key.p, B.wkey.p, B.sort_vals.p, B.leaf_of.p,
-                                                     c.d_flags.p);
+                                                     guess_nodes, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
   }
   const int begin_bit = kKeyRootShift - 2 * T.max_level;

@@ -42,6 +42,50 @@ def gather_partitioned_rows(out: torch.Tensor, perm: torch.Tensor, p0: int, p1: 
     return out
 
 
+def shard_rows(n: int, ws: int, rank: int) -> tuple:
+    """Rank `rank`'s rows [a, b) of n in the caller's order: equal slots of
+    ceil(n / ws) rows (the last one short), so the all-gathers below need no
+    per-rank sizes."""
+    m = -(-n // ws)
+    return min(n, rank * m), min(n, (rank + 1) * m)
+
+
+def allgather_inputs(h_xyz: torch.Tensor, h_q: torch.Tensor, d_xyz: torch.Tensor, d_q: torch.Tensor,
+                     group: Optional[dist.ProcessGroup] = None) -> None:
+    """Distributed input staging (BASELINE north_star: particle positions are
+    all-gathered over NVLink): rank r copies only its shard_rows() of the
+    host inputs (pinned) to its device, and one all-gather per array
+    completes the replicated particle set on every rank. d_xyz (>= ws*m, 3)
+    and d_q (>= ws*m,) with m = ceil(N / ws): rows [0, N) receive the
+    inputs; rows past N are padding."""
+    n = h_xyz.shape[0]
+    ws = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if ws == 1:
+        d_xyz[:n].copy_(h_xyz, non_blocking=True)
+        d_q[:n].copy_(h_q, non_blocking=True)
+        return
+    r = dist.get_rank(group)
+    m = -(-n // ws)
+    a, b = shard_rows(n, ws, r)
+    for h, d in ((h_xyz, d_xyz), (h_q, d_q)):
+        slot = d[r * m:(r + 1) * m]
+        if b > a:
+            slot[: b - a].copy_(h[a:b], non_blocking=True)
+        if b - a < m:
+            slot[b - a:].zero_()
+        _all_gather_slots(d[: ws * m], slot, ws, group)
+
+
+def _all_gather_slots(buf: torch.Tensor, slot: torch.Tensor, ws: int, group) -> None:
+    """buf = ws equal slots; `slot` (this rank's) is one of them, in place."""
+    if buf.is_cuda:
+        dist.all_gather_into_tensor(buf, slot.clone(), group=group)
+    else:  # gloo
+        outs = [torch.empty_like(slot) for _ in range(ws)]
+        dist.all_gather(outs, slot.clone(), group=group)
+        buf.copy_(torch.cat(outs))
+
+
 def gather_rows(tree, out: torch.Tensor, group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
     """All-gather the last partitioned evaluation of `tree` into `out` (device)."""
     p0, p1 = tree.partition_range()

@@ -136,3 +136,44 @@ def test_rk4_distributed_gloo():
         outs[ws] = dict((r, (xb, zb)) for r, xb, zb in (q.get(timeout=10) for _ in range(ws)))
     assert outs[2][0] == outs[2][1]  # every rank holds the same state
     assert outs[2][0] == outs[1][0]  # and it is the single-rank result
+
+
+def _inputs_worker(rank, ws, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        from paper_2401_07361_b200.dist import allgather_inputs, shard_rows
+
+        g = torch.Generator().manual_seed(99)
+        xyz = torch.randn(n, 3, generator=g, dtype=torch.float64)
+        qq = torch.randn(n, generator=g, dtype=torch.float64)
+        # this rank's host copy holds only its shard (the rest is garbage)
+        a, b = shard_rows(n, ws, rank)
+        h_xyz = torch.full_like(xyz, float("nan"))
+        h_q = torch.full_like(qq, float("nan"))
+        h_xyz[a:b], h_q[a:b] = xyz[a:b], qq[a:b]
+        m = -(-n // ws)
+        d_xyz = torch.full((ws * m, 3), -1.0, dtype=torch.float64)
+        d_q = torch.full((ws * m,), -1.0, dtype=torch.float64)
+        allgather_inputs(h_xyz, h_q, d_xyz, d_q)
+        q.put((rank, bool(torch.equal(d_xyz[:n], xyz) and torch.equal(d_q[:n], qq))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 11, 1])
+def test_allgather_inputs_gloo(n):
+    """bench.py's distributed e2e staging: each rank supplies only its shard
+    of the host inputs; after the all-gather every rank holds all N rows."""
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_inputs_worker, args=(r, ws, port, n, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    res = dict(q.get(timeout=10) for _ in range(ws))
+    assert res == {0: True, 1: True}

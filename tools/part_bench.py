@@ -4,7 +4,9 @@ placed the cost-balanced cuts, each part bins, traverses and lists its own
 targets only). The max over parts approximates one G-GPU step before the row
 all-gather; nothing here waits on another rank.
 
-    python tools/part_bench.py [G ...]
+    python tools/part_bench.py [G ...] [--phases]
+
+--phases adds each part's phase split (TreecodeStats of its last call).
 """
 import json
 import sys
@@ -14,7 +16,8 @@ import torch
 sys.path.insert(0, ".")
 import paper_2401_07361_b200 as ss  # noqa: E402
 
-parts = [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8]
+phases = "--phases" in sys.argv
+parts = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [1, 2, 4, 8]
 xyz, area = ss.make_icosa_mesh(9)
 q = ss.rh4_vorticity(xyz) * area
 n = xyz.shape[0]
@@ -27,7 +30,7 @@ res = {}
 for G in parts:
     tree = ss.FaceTree(0)
     tree.set_stream(torch.cuda.current_stream().cuda_stream)
-    per = []
+    per, split = [], []
     for r in range(G):
         tree.set_partition(r, G)
         for _ in range(3):  # warm-up (the first call of part 0 places the cuts)
@@ -36,11 +39,16 @@ for G in parts:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        st = ss.TreecodeStats()
         for _ in range(5):
             ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
-                                   d_out.data_ptr())
+                                   d_out.data_ptr(), stats=st)
         e1.record()
         torch.cuda.synchronize()
         per.append(e0.elapsed_time(e1) / 5)
+        split.append({"bin": st.bin_seconds * 1e3 / 5, "trav": st.traversal_seconds * 1e3 / 5,
+                      "up": st.upward_ms, "fit": st.cp_cc_fit_ms, "pp_pc": st.pp_pc_ms, "finish": st.finish_ms})
     res[G] = {"max_part_ms": max(per), "min_part_ms": min(per), "parts_ms": per}
+    if phases:
+        res[G]["phases_of_max_part"] = split[per.index(max(per))]
     print(json.dumps({"G": G, **res[G]}), flush=True)
