@@ -299,15 +299,7 @@ void ssum_destroy(ssum_ctx* h) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  // DBuf members free their memory through release(); walk the obvious ones.
-  c->pts.release();
-  c->S.release();
-  c->coeff.release();
-  c->wpart.release();
-  c->in_xyz.release();
-  c->in_q.release();
-  c->out_buf.release();
-  c->rk_state.release();
+  // device buffers (DBuf) free themselves when the context is deleted below
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->io.xyz) if (e) cudaEventDestroy(e);
   for (auto& e : c->io.out) if (e) cudaEventDestroy(e);

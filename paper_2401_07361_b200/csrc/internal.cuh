@@ -45,6 +45,19 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t cap = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;  // owns device memory: freed once, by the owner
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap) { o.p = nullptr, o.cap = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, cap = o.cap;
+      o.p = nullptr, o.cap = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
   void ensure(size_t n, bool keep = false, cudaStream_t s = 0) {
     if (n <= cap) return;
     size_t nc = cap ? cap : 1024;
@@ -247,8 +260,6 @@ struct Ctx {
   DBuf<Tile> direct_tiles;
   DBuf<SrcRange> direct_range;
   DBuf<double> rk_state;             // RK4 scratch
-  double* h_stage = nullptr;         // pinned staging
-  size_t h_stage_bytes = 0;
   cudaEvent_t ev[8];
   // Host-pointer entry (ssum_treecode_sum): the inputs travel on copy_stream
   // in kIoChunks pieces (the tree walk starts on each piece as it lands, q is

@@ -509,3 +509,27 @@ def test_config5_size_properties(ss, mesh_fixture):
     u3 = ss.treecode_sum(ss.BiotSavartKernel, xyz, 2.0 * q, c, tree=t)
     assert np.array_equal(u3, 2.0 * u1)
     assert np.isfinite(u1).all()
+
+
+def test_context_destroy_frees_device_memory(ss, mesh_fixture):
+    """ssum_destroy returns every device buffer of a context (tree, lists,
+    tiles, staging): repeated create / evaluate / destroy cycles leave the
+    free device memory where it was."""
+    import torch
+
+    xyz, q, a = mesh_fixture(6)
+
+    def cycle():
+        tree = ss.FaceTree(0)
+        ss.treecode_sum(ss.BiotSavartKernel, xyz, q, cfg(ss, deg=8), tree=tree)
+        ss.direct_sum(ss.BiotSavartKernel, xyz[:2000], q[:2000], tree=tree)
+        tree.close()
+
+    cycle()  # first-use allocations of the runtime and libraries
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(0)[0]
+    for _ in range(4):
+        cycle()
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info(0)[0]
+    assert free0 - free1 < 8 << 20, (free0, free1)
