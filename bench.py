@@ -53,6 +53,15 @@ CONFIGS = {
                cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
                workload="config2: L8 icosahedral mesh N=655,362, RH4, Voronoi areas, Biot-Savart, d=8, "
                         "theta=0.7, cluster-cluster; one full treecode_sum per step"),
+    "c2pc": dict(metric="BVE tree-code velocity evals/s (N=655k, PC-only, fp64)", mesh=8,
+                 cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10, pc_only=True),
+                 workload="config2 PC-only mode: L8 icosahedral mesh N=655,362, RH4, Voronoi areas, Biot-Savart, "
+                          "d=8, theta=0.7, particle-cluster traversal (CP->PP, CC->PC; not in the reference: "
+                          "CPU baseline is the oracle port, single thread)"),
+    "c2log": dict(metric="BVE tree-code stream-function evals/s (N=655k, fp64)", mesh=8, kernel=1,
+                  cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
+                  workload="config2 stream function: L8 icosahedral mesh N=655,362, RH4, Voronoi areas, "
+                           "log kernel (psi), d=8, theta=0.7, cluster-cluster"),
     "c3": dict(metric="BVE tree-code velocity evals/s (N=4.2M random cap, fp64)", cap=1 << 22,
                cfg=dict(theta=0.7, n_threshold=64, degree=8, max_depth=10),
                workload="config3: 2^22 seeded points (half uniform, half in a 10 deg cap at lat 40), Gaussian "
@@ -66,12 +75,21 @@ CONFIG = "c4"
 METRIC = CONFIGS[CONFIG]["metric"]
 CFG = CONFIGS[CONFIG]["cfg"]
 WORKLOAD = CONFIGS[CONFIG]["workload"]
+KERNEL = 0  # 0 Biot-Savart (velocity, D = 3), 1 log (stream function, D = 1)
+DIM = 3
 
 
 def use_config(name):
-    global CONFIG, METRIC, CFG, WORKLOAD
+    global CONFIG, METRIC, CFG, WORKLOAD, KERNEL, DIM, FLOP_PER_PAIR
     CONFIG = name
     METRIC, CFG, WORKLOAD = CONFIGS[name]["metric"], CONFIGS[name]["cfg"], CONFIGS[name]["workload"]
+    KERNEL = CONFIGS[name].get("kernel", 0)
+    DIM = 3 if KERNEL == 0 else 1
+    FLOP_PER_PAIR = 13 if KERNEL == 0 else 9  # F_BS, F_log
+
+
+def kernel_class(ss):
+    return ss.BiotSavartKernel if KERNEL == 0 else ss.LogPotentialKernel
 
 
 def dist_env():
@@ -160,10 +178,21 @@ def cpu_model():
     return None
 
 
+def reference_kind():
+    """The CPU baseline of this config: the unmodified reference (oracle/_ref,
+    all host threads), or — PC-only mode, which the reference lacks — the
+    oracle port (one thread)."""
+    return "port" if CFG.get("pc_only") else "reference"
+
+
 def reference_step(ol, xyz, q, workers):
     t0 = time.perf_counter()
-    out, st = ol.ref_treecode(0, xyz, q, CFG["theta"], CFG["n_threshold"], CFG["degree"], CFG["max_depth"],
-                              workers)
+    if CFG.get("pc_only"):
+        out, st = ol.orc_treecode(KERNEL, xyz, q, CFG["theta"], CFG["n_threshold"], CFG["degree"],
+                                  CFG["max_depth"], pc_only=True)
+    else:
+        out, st = ol.ref_treecode(KERNEL, xyz, q, CFG["theta"], CFG["n_threshold"], CFG["degree"],
+                                  CFG["max_depth"], workers)
     return time.perf_counter() - t0, out, st
 
 
@@ -176,7 +205,7 @@ def run_reference(args):
     if not ol.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libspheresum_ref.so not built"}))
         return
-    cores = os.cpu_count() or 1
+    cores = (os.cpu_count() or 1) if reference_kind() == "reference" else 1
     xyz, q, area = fixture()
     n = xyz.shape[0]
     # warm-up on a level-5 sample (threads, page cache, lattice_fit cache)
@@ -185,7 +214,7 @@ def run_reference(args):
     wx, wa = ss.make_icosa_mesh(5)
     wq = ss.rh4_vorticity(wx) * wa
     for _ in range(args.warmup):
-        ol.ref_treecode(0, wx, wq, CFG["theta"], CFG["n_threshold"], CFG["degree"], CFG["max_depth"], cores)
+        reference_step(ol, wx, wq, cores)
     times = []
     budget = 240.0
     for k in range(args.steps):
@@ -200,7 +229,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, **CFG, "n": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "cpu": cpu_model(),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": reference_kind(), "cpu": cpu_model(),
                          "sample": f"full {CONFIG} treecode_sum per step ({len(times)} timed of {args.steps} "
                                    f"requested, 240 s budget); warm-up steps on a level-5 mesh"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -229,7 +258,7 @@ def run_gpu(args):
     d_q = torch.zeros(rows, dtype=torch.float64, device=dev)
     d_xyz[:n].copy_(torch.from_numpy(xyz))
     d_q[:n].copy_(torch.from_numpy(q))
-    d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    d_out = torch.zeros((n, DIM), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     tree = ss.FaceTree(local)
     tree.set_stream(stream.cuda_stream)
@@ -238,7 +267,7 @@ def run_gpu(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
     def step(st):
-        ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
+        ss.treecode_sum_device(tree, kernel_class(ss), cfg, d_xyz.data_ptr(), d_q.data_ptr(), n,
                                d_out.data_ptr(), stats=st)
 
     clocks = ClockSampler(local).__enter__()
@@ -285,7 +314,7 @@ def run_gpu(args):
     # e2e through the host-pointer C-ABI entry point with pinned buffers
     h_xyz = torch.from_numpy(xyz).pin_memory()
     h_q = torch.from_numpy(q).pin_memory()
-    h_out = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
+    h_out = torch.zeros((n, DIM), dtype=torch.float64).pin_memory()
     e2e_times = []
     if ws > 1:
         from paper_2401_07361_b200.dist import allgather_inputs, gather_rows, shard_rows
@@ -296,7 +325,7 @@ def run_gpu(args):
         t0 = time.perf_counter()
         if ws == 1:
             # the public host-pointer entry point: H2D, bin, traverse, evaluate, D2H
-            ss.treecode_sum(ss.BiotSavartKernel, h_xyz.numpy(), h_q.numpy(), cfg, tree=tree, out=h_out.numpy())
+            ss.treecode_sum(kernel_class(ss), h_xyz.numpy(), h_q.numpy(), cfg, tree=tree, out=h_out.numpy())
         else:
             # per rank: H2D of this rank's 1/ws shard of x and q, NCCL
             # all-gather of the particle set over NVLink, this rank's
@@ -346,8 +375,9 @@ def run_gpu(args):
     base = 21 + 3 * (deg - 1)
     up_flop = stats.up_visits * (base + 4 * p_pts) + stats.weight_nodes * 2 * p_pts * p_pts
     up_bytes = 32 * stats.up_visits
-    down_flop = stats.down_visits * (base + 8 * p_pts) + stats.fit_nodes * 6 * p_pts * p_pts
-    down_bytes = (32 + 24) * n
+    per_term = 2 + 2 * DIM  # basis product (2 mul) + DIM FMAs per coefficient
+    down_flop = stats.down_visits * (base + per_term * p_pts) + stats.fit_nodes * 2 * DIM * p_pts * p_pts
+    down_bytes = (32 + 8 * DIM) * n
 
     def _pass(flop, byts, ms):
         s = max(ms, 1e-9) * 1e-3
@@ -357,7 +387,7 @@ def run_gpu(args):
     passes = {"visits": {"upward": stats.up_visits, "downward": stats.down_visits},
               "upward": _pass(up_flop, up_bytes, stats.upward_ms),
               "downward": _pass(down_flop, down_bytes, stats.finish_ms),
-              "flop_per_visit": {"upward": base + 4 * p_pts, "downward": base + 8 * p_pts},
+              "flop_per_visit": {"upward": base + 4 * p_pts, "downward": base + per_term * p_pts},
               "hbm_peak_gbs": hbm}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -370,7 +400,7 @@ def run_gpu(args):
                      "peak_source": "DFMA-chain probe on this GPU (ssum_fp64_peak); MEASURED_PEAKS.json has no fp64",
                      "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": pairs, "avg_launch_ms": avg_pp_ms},
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xyz.nbytes + q.nbytes),
-                "d2h_bytes_per_step": int(n * 3 * 8), "ms_per_step": e2e_s * 1e3,
+                "d2h_bytes_per_step": int(n * DIM * 8), "ms_per_step": e2e_s * 1e3,
                 "path": ("ssum_treecode_sum (host pointers)" if ws == 1 else
                          "per rank: H2D of its 1/ws input shard, NCCL all-gather of x and q, its targets, "
                          "NCCL all-gather of the rows, D2H of its 1/ws result shard (bytes: whole job)")},
@@ -390,14 +420,15 @@ def run_gpu(args):
         import oracle_lib as ol
 
         if ol.ref_available():
-            cores = os.cpu_count() or 1
+            kind = reference_kind()
+            cores = (os.cpu_count() or 1) if kind == "reference" else 1
             dt, ref_out, _ = reference_step(ol, xyz, q, cores)
             ref_u = ref_out
             mine = h_out.numpy()
-            line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            what = f"unmodified reference, workers={cores}" if kind == "reference" else "oracle port, 1 thread"
+            line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": cores, "kind": kind,
                                     "cpu": cpu_model(),
-                                    "sample": f"one full {CONFIG} treecode_sum (unmodified reference, "
-                                              f"workers={cores}), {dt:.1f} s"}
+                                    "sample": f"one full {CONFIG} treecode_sum ({what}), {dt:.1f} s"}
             line["parity_rel_l2_vs_reference"] = ol.rel_l2(mine, ref_out)
         else:
             line["cpu_baseline"] = None
@@ -425,17 +456,26 @@ def sampled_direct_error(xyz, q, u_tree, dev, u_ref=None, m=2048, seed=2024):
     Q = torch.from_numpy(q).to(dev)
     tid = torch.from_numpy(idx).to(dev)
     T = X[tid]
-    S = torch.zeros_like(T)
+    S = torch.zeros_like(T) if KERNEL == 0 else torch.zeros(len(idx), dtype=torch.float64, device=dev)
     chunk = 1 << 18
     for c0 in range(0, n, chunk):
         c1 = min(n, c0 + chunk)
         den = 1.0 - T @ X[c0:c1].T
         own = (tid >= c0) & (tid < c1)  # self pairs excluded
-        den[own.nonzero().squeeze(1), (tid[own] - c0)] = float("inf")
-        S += (Q[c0:c1] / den) @ X[c0:c1]
-    u_dir = (-1.0 / (4.0 * np.pi)) * torch.cross(T, S, dim=1)
+        rows, cols = own.nonzero().squeeze(1), (tid[own] - c0)
+        if KERNEL == 0:
+            den[rows, cols] = float("inf")
+            S += (Q[c0:c1] / den) @ X[c0:c1]
+        else:
+            lg = torch.log(den)
+            lg[rows, cols] = 0.0
+            S += lg @ Q[c0:c1]
+    if KERNEL == 0:
+        u_dir = (-1.0 / (4.0 * np.pi)) * torch.cross(T, S, dim=1)  # velocity
+    else:
+        u_dir = (-1.0 / (4.0 * np.pi)) * S  # stream function (LogPotentialKernel, prefactor 1)
     def rel(u):
-        ut = torch.from_numpy(np.ascontiguousarray(u[idx])).to(dev)
+        ut = torch.from_numpy(np.ascontiguousarray(u[idx])).to(dev).reshape(u_dir.shape)
         return float(torch.linalg.norm(ut - u_dir) / torch.linalg.norm(u_dir))
 
     e_tree = rel(u_tree)
