@@ -108,7 +108,7 @@ EXPORTED_SYMBOLS = (
     "ssum_treecode_sum", "ssum_treecode_sum_device", "ssum_direct_sum", "ssum_direct_sum_device",
     "ssum_bin_particles", "ssum_tree_node_count", "ssum_tree_export", "ssum_dual_traversal",
     "ssum_rk4", "ssum_mesh_vertex_count", "ssum_make_icosa_mesh", "ssum_rh4_vorticity",
-    "ssum_make_random_cap", "ssum_fp64_peak", "ssum_set_partition", "ssum_partition_range",
+    "ssum_make_random_cap", "ssum_fp64_peak", "ssum_probe_log_far", "ssum_set_partition", "ssum_partition_range",
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
     "ssum_rk4_step_end",
 )
@@ -148,6 +148,7 @@ def load_library():
         "ssum_rh4_vorticity": (ctypes.c_int, [_P, _I64, _P]),
         "ssum_make_random_cap": (ctypes.c_int, [_I64, ctypes.c_uint64, _P, _P, _P]),
         "ssum_fp64_peak": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+        "ssum_probe_log_far": (ctypes.c_int, [_P, _P, _I64, _P]),
         "ssum_set_partition": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
         "ssum_partition_range": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
         "ssum_tree_perm": (ctypes.c_int, [_P, _P, ctypes.c_int]),
@@ -352,6 +353,14 @@ class FaceTree:
         v = ctypes.c_double()
         self._check(self._lib.ssum_fp64_peak(self._h, int(reps), ctypes.byref(v)))
         return v.value
+
+    def probe_log_far(self, x: np.ndarray) -> np.ndarray:
+        """The far-pair log of the log kernel (kernels.cuh log_far) on the
+        device, for accuracy tests."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty_like(x)
+        self._check(self._lib.ssum_probe_log_far(self._h, _ptr(x), x.size, _ptr(out)))
+        return out
 
     def set_partition(self, part: int, nparts: int) -> None:
         """Compute only part `part` of `nparts` cost-balanced target ranges

@@ -5,7 +5,7 @@
 // `reps` launches timed with CUDA events on the context's stream.
 #include <algorithm>
 
-#include "internal.cuh"
+#include "kernels.cuh"
 
 namespace ssum {
 namespace {
@@ -29,10 +29,36 @@ __global__ void k_dfma_chain(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
 }
 
+__global__ void k_log_far(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = log_far(x[i]);
+}
+
 }  // namespace
 }  // namespace ssum
 
 using namespace ssum;
+
+// Accuracy probe of the far-pair log (kernels.cuh log_far), host arrays.
+extern "C" int ssum_probe_log_far(ssum_ctx* h, const double* x, int64_t n, double* out) {
+  Ctx* c = reinterpret_cast<Ctx*>(h);
+  if (!c || (n > 0 && (!x || !out)) || n < 0) return SSUM_INVALID;
+  try {
+    cudaSetDevice(c->device);
+    if (n == 0) return SSUM_OK;
+    DBuf<double> buf;
+    buf.ensure(size_t(2 * n));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(buf.p, x, size_t(n) * 8, cudaMemcpyHostToDevice, c->stream));
+    k_log_far<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(buf.p, n, buf.p + n);
+    SSUM_LAUNCH_CHECK();
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(out, buf.p + n, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    return SSUM_OK;
+  } catch (const Error& e) {
+    c->last_error = e.what();
+    return e.code;
+  }
+}
 
 extern "C" int ssum_fp64_peak(ssum_ctx* h, int reps, double* tflops) {
   Ctx* c = reinterpret_cast<Ctx*>(h);

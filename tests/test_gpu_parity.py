@@ -533,3 +533,21 @@ def test_context_destroy_frees_device_memory(ss, mesh_fixture):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info(0)[0]
     assert free0 - free1 < 8 << 20, (free0, free1)
+
+
+def test_log_far_accuracy(ss):
+    """kernels.cuh log_far (the log kernel's far pairs, den >= 2^-20) against
+    numpy's log: within 2 ulp over [2^-20, 4] (log-uniform), the range
+    reduction's boundaries (sqrt(1/2), sqrt(2)), powers of two and 1 +- eps."""
+    rng = np.random.default_rng(7)
+    x = np.exp(rng.uniform(np.log(2.0 ** -20), np.log(4.0), 200_000))
+    edges = [2.0 ** -20, 0.25, 0.5, 1.0, 2.0, 4.0, np.sqrt(0.5), np.sqrt(2.0), np.nextafter(1.0, 0.0),
+             np.nextafter(1.0, 2.0), 1 - 1e-9, 1 + 1e-9, np.nextafter(np.sqrt(0.5), 0.0),
+             np.nextafter(np.sqrt(2.0), 4.0), 0.70710676, 1.4142135]
+    x = np.concatenate([x, edges])
+    tree = ss.FaceTree(0)
+    got = tree.probe_log_far(x)
+    ref = np.log(x)
+    ulps = np.abs(got - ref) / np.spacing(np.abs(ref) + np.finfo(float).tiny)
+    assert ulps.max() <= 2.0, (ulps.max(), x[np.argmax(ulps)])
+    assert got[np.where(x == 1.0)[0][0]] == 0.0
