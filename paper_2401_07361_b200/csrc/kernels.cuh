@@ -211,15 +211,19 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
 // other than its self pairs: adds the reference-rounded contribution of each
 // near pair of distinct points (pair_slow, which also raises the singular
 // flag), and takes back the fast term of a self pair that was not near (only
-// possible for input points off the unit sphere).
-template <int KER, int NT, int NS>
-__device__ __forceinline__ void near_repair(const double4* x, const double4* __restrict__ B,
-                                            const int* __restrict__ J, int G, Acc<KER>* a, const int* ti,
-                                            int* flags) {
+// possible for input points off the unit sphere). Source s of the block sits
+// at flattened list position f0 + s G; jof(f) is its point index (-1 for the
+// zero padding past the list).
+template <int KER, int NT, int NS, class JOf>
+__device__ __forceinline__ void near_repair(const double4* x, const double4* __restrict__ B, int f0, JOf jof,
+                                            int G, Acc<KER>* a, const int* ti, int* flags) {
+  int js[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) js[s] = jof(f0 + s * G);
 #pragma unroll
   for (int c = 0; c < NT * NS; ++c) {
     const double4 y = B[(c / NT) * G];
-    const int j = J[(c / NT) * G];
+    const int j = js[c / NT];
     const double4& xx = x[c % NT];
     const double den = fma(-xx.z, y.z, fma(-xx.y, y.y, fma(-xx.x, y.x, 1.0)));
     const bool nr = __double2hiint(den) < kNearHi;

@@ -16,10 +16,12 @@ constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
 //  * Thread -> (targets u, u + th with th = ceil(T / 2), source group g)
 //    with G = min(32, 256 / th) groups: a 40-particle leaf keeps 240 of 256
 //    lanes busy (th 20, 12 groups), a p = 45 fit node 253 (th 23, 11 groups).
-//  * The source ranges are streamed as ONE flattened list in chunks of 512
-//    (each thread fetches two sources, locating their ranges by binary search
-//    on the ranges' prefix counts), double-buffered through shared memory:
-//    chunk c+1 is in flight in registers while chunk c is consumed. Every
+//  * The source ranges are streamed as ONE flattened list in chunks of 512,
+//    double-buffered through shared memory by the copy engine: warp 0 issues
+//    one cp.async.bulk per (range, chunk) overlap — each range is a
+//    contiguous run of double4 points — completing on the stage's mbarrier,
+//    so chunk c+1 lands while chunk c is consumed, with no register staging
+//    and no per-source address search. Every
 //    thread walks the chunk with stride G, 2 sources x 2 targets per step
 //    (far_block), so all warps run the same trip count (the chunk tail is
 //    zero-padded: q = 0 adds nothing).
@@ -36,7 +38,7 @@ constexpr int kTileThreads = 256;
 #ifndef SSUM_CHUNK
 #define SSUM_CHUNK 512
 #endif
-constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage (multiple of kTileThreads)
+constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage
 constexpr int kLeafMode = 0, kFitMode = 1, kDirectMode = 2;
 #ifndef SSUM_NS
 #define SSUM_NS 2
@@ -49,25 +51,58 @@ constexpr int kPad = 32 * SSUM_NS;
 #ifndef SSUM_TILE_MINB
 #define SSUM_TILE_MINB 4
 #endif
+#ifndef SSUM_FIT_MINB
+#define SSUM_FIT_MINB 4
+#endif
 #ifndef SSUM_TPT
 #define SSUM_TPT 2
 #endif
 constexpr int kRangeCap = 512;
 constexpr int kTpt = SSUM_TPT;  // targets per thread (register tile)
 
+// Bulk-copy (TMA, non-tensor) helpers: the source ranges of a chunk are
+// copied global -> shared by the copy engine, completion counted in bytes on
+// an mbarrier (no register staging, no per-source address search).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
 template <int KER, int MODE>
-__global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
+__global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB : SSUM_TILE_MINB)
     k_tiles(const Tile* __restrict__ tiles, int ntiles, const int* __restrict__ sel,
             const SrcRange* __restrict__ ranges, const double4* __restrict__ pts, double* __restrict__ S,
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
             const double* __restrict__ vinv, int P, double* __restrict__ coeff) {
   constexpr int D = KDim<KER>::D;
-  // dynamic shared memory (kTileSmem bytes): two source stages, their
-  // indices, and the range table
+  // dynamic shared memory (kTileSmem bytes): two source stages and the range
+  // table; two mbarriers (one per stage)
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long bar[2];
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
-  auto sid = reinterpret_cast<int(*)[kChunk + kPad]>(smem + 2 * sizeof(double4) * (kChunk + kPad));
-  int2* rtab = reinterpret_cast<int2*>(smem + 2 * (sizeof(double4) + sizeof(int)) * (kChunk + kPad));
+  int2* rtab = reinterpret_cast<int2*>(smem + 2 * sizeof(double4) * (kChunk + kPad));
   static_assert(sizeof(double) * kTileThreads * D * kTpt <= 2 * sizeof(double4) * (kChunk + kPad), "red alias");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
@@ -76,7 +111,7 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
   const int tc = T.tgt_count;
   const int th = (tc + kTpt - 1) / kTpt;  // thread-targets; thread slot u holds targets u, u + th, ...
   const int G = min(32, kTileThreads / th);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int u = tid % th, g = (tid / th) % G;
   int ti[kTpt];
   double4 x[kTpt];
@@ -88,11 +123,14 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
   }
   const int total = (T.list_end > T.list_begin) ? ranges[T.list_end - 1].pad + ranges[T.list_end - 1].count : 0;
   const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
-  if (tid < kPad) {  // zero tail: the stride-G walk may read up to G - 1 entries past the chunk
+  if (tid < kPad) {  // zero tail: the stride-G walk may read up to kNs G - 1 entries past the chunk
     buf[0][kChunk + tid] = zero4;
     buf[1][kChunk + tid] = zero4;
-    sid[0][kChunk + tid] = -1;
-    sid[1][kChunk + tid] = -1;
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nr = T.list_end - T.list_begin;
   const bool in_smem = nr <= kRangeCap;
@@ -102,47 +140,52 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
       rtab[r] = make_int2(R.begin, R.pad);
     }
   __syncthreads();
-  // flattened position -> source index: binary search over the range
-  // prefixes. Thread tid fetches positions e * 256 + tid of each chunk
-  // (coalesced loads and shared stores; one search each — measured faster
-  // than consecutive positions with one search per thread).
-  constexpr int kPer = kChunk / kTileThreads;  // sources fetched per thread per chunk
-  auto slot = [](int e, int t) { return e * kTileThreads + t; };
   auto rbegin = [&](int r) { return in_smem ? rtab[r].x : ranges[T.list_begin + r].begin; };
   auto rpad = [&](int r) { return in_smem ? rtab[r].y : ranges[T.list_begin + r].pad; };
+  // flattened list position -> range (binary search over the range prefixes)
   auto locate = [&](int f) {
     int lo = 0, hi = nr - 1;
-    if (in_smem) {
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (rtab[mid].y <= f)
-          lo = mid;
-        else
-          hi = mid - 1;
-      }
-    } else {
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (ranges[T.list_begin + mid].pad <= f)
-          lo = mid;
-        else
-          hi = mid - 1;
-      }
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rpad(mid) <= f)
+        lo = mid;
+      else
+        hi = mid - 1;
     }
     return lo;
   };
-  auto fetch = [&](int c0, double4* v, int* j) {
-#pragma unroll
-    for (int e = 0; e < kPer; ++e) {
-      const int f = c0 + e * kTileThreads + tid;
-      if (f < total) {
-        const int lo = locate(f);
-        j[e] = rbegin(lo) + (f - rpad(lo));
-        v[e] = pts[j[e]];
-      } else {
-        v[e] = zero4;
-        j[e] = -1;
+  // point index of flattened position f (-1 past the list): near repair only
+  auto jof = [&](int f) {
+    if (f >= total) return -1;
+    const int r = locate(f);
+    return rbegin(r) + (f - rpad(r));
+  };
+  // Warp 0 issues chunk cc: one bulk copy per (range ∩ chunk), lane-parallel
+  // over the ranges; the stage's mbarrier expects the chunk's bytes. A
+  // partial (last) chunk's tail up to the zero pad is cleared with generic
+  // stores, visible to the block after the barrier that ends the previous
+  // chunk (or the prologue's).
+  auto issue = [&](int cc) {
+    const int c0 = cc * kChunk;
+    const int cn = min(kChunk, total - c0);
+    double4* dst = buf[cc & 1];
+    if (lane == 0) mbar_expect_tx(&bar[cc & 1], static_cast<unsigned>(cn) * sizeof(double4));
+    __syncwarp();
+    for (int e = cn + lane; e < min(kChunk, cn + kPad); e += 32) dst[e] = zero4;
+    for (int r = locate(c0) + lane;; r += 32) {
+      bool more_r = false;
+      if (r < nr) {
+        const int pad = rpad(r);
+        if (pad < c0 + cn) {
+          more_r = true;
+          const int end = (r + 1 < nr) ? rpad(r + 1) : total;
+          const int lo = max(pad, c0), hi = min(end, c0 + cn);
+          if (hi > lo)
+            bulk_g2s(dst + (lo - c0), pts + rbegin(r) + (lo - pad), static_cast<unsigned>(hi - lo) * sizeof(double4),
+                     &bar[cc & 1]);
+        }
       }
+      if (!__any_sync(0xffffffffu, more_r)) break;
     }
   };
   Acc<KER> a[kTpt];
@@ -154,21 +197,14 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
   const int kStep = kNs * G;
   const int steps_full = (kChunk + kStep - 1) / kStep;
   const int steps_last = (total - (nch - 1) * kChunk + kStep - 1) / kStep;
-  double4 v[kPer];
-  int j[kPer];
-  fetch(0, v, j);
-#pragma unroll
-  for (int e = 0; e < kPer; ++e) {
-    buf[0][slot(e, tid)] = v[e];
-    sid[0][slot(e, tid)] = j[e];
-  }
-  __syncthreads();
+  if (nch > 0 && tid < 32) issue(0);
+  if (nch == 1) __syncthreads();  // its zeroed tail (later chunks: the barrier ending the chunk before)
   for (int c = 0; c < nch; ++c) {
     const bool more = c + 1 < nch;
-    if (more) fetch((c + 1) * kChunk, v, j);
+    if (more && tid < 32) issue(c + 1);  // stage (c + 1) & 1 was released by the barrier ending chunk c - 1
+    mbar_wait(&bar[c & 1], (c >> 1) & 1);
     const int n = min(kChunk, total - c * kChunk);
     const double4* B = buf[c & 1] + g;  // this lane's sources: B[m G], m = 0, 1, ...
-    const int* J = sid[c & 1] + g;
     const int steps = more ? steps_full : steps_last;
     // steps covering the chunk's near-possible prefix [0, near_total - c kChunk):
     // the same staged blocks with near pairs masked and counted, checked
@@ -205,16 +241,17 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
       if (__any_sync(0xffffffffu, ncnt != nself)) {
         // only the steps that met a masked pair (dense inputs: a handful of
         // the chunk's near steps)
+        const int f0 = c * kChunk + g;
         if (near_steps <= 32) {
 #pragma unroll 1
           for (unsigned m = hit; m; m &= m - 1) {
             const int r = __ffs(m) - 1;
-            near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
+            near_repair<KER, kTpt, kNs>(x, B + r * kStep, f0 + r * kStep, jof, G, a, ti, flags);
           }
         } else {
 #pragma unroll 1
           for (int r = 0; r < near_steps; ++r)
-            near_repair<KER, kTpt, kNs>(x, B + r * kStep, J + r * kStep, G, a, ti, flags);
+            near_repair<KER, kTpt, kNs>(x, B + r * kStep, f0 + r * kStep, jof, G, a, ti, flags);
         }
       }
     }
@@ -223,12 +260,6 @@ __global__ void __launch_bounds__(kTileThreads, SSUM_TILE_MINB)
     const double4* Bp = B + it * kStep;
 #pragma unroll 2
     for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a);
-    if (more)
-#pragma unroll
-      for (int e = 0; e < kPer; ++e) {
-        buf[(c + 1) & 1][slot(e, tid)] = v[e];
-        sid[(c + 1) & 1][slot(e, tid)] = j[e];
-      }
     __syncthreads();
   }
 #pragma unroll
@@ -306,7 +337,7 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
                   static_cast<int>(n), 0, 1, 0};
 }
 
-constexpr size_t kTileSmem = 2 * (sizeof(double4) + sizeof(int)) * (kChunk + kPad) + sizeof(int2) * kRangeCap;
+constexpr size_t kTileSmem = 2 * sizeof(double4) * (kChunk + kPad) + sizeof(int2) * kRangeCap;
 
 // k_tiles instantiation with its dynamic shared-memory limit raised once
 // (per process; every context's device is an sm_100a part)
