@@ -16,11 +16,13 @@ constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
 //  * Thread -> (targets u, u + th with th = ceil(T / 2), source group g)
 //    with G = min(32, 256 / th) groups: a 40-particle leaf keeps 240 of 256
 //    lanes busy (th 20, 12 groups), a p = 45 fit node 253 (th 23, 11 groups).
-//  * The source ranges are streamed as ONE flattened list in chunks of 512,
-//    double-buffered through shared memory by the copy engine: warp 0 issues
-//    one cp.async.bulk per (range, chunk) overlap — each range is a
-//    contiguous run of double4 points — completing on the stage's mbarrier,
-//    so chunk c+1 lands while chunk c is consumed, with no register staging
+//  * The source ranges are streamed as ONE flattened list in chunks of
+//    kChunk sources through kStages shared-memory stages filled by the copy
+//    engine: warp 0 issues one cp.async.bulk per (range, chunk) overlap —
+//    each range is a contiguous run of double4 points — completing on the
+//    stage's full mbarrier; each warp releases a stage on its empty mbarrier
+//    when done, so warps never wait on each other inside the tile and
+//    chunks land while earlier ones are consumed, with no register staging
 //    and no per-source address search. Every
 //    thread walks the chunk with stride G, 2 sources x 2 targets per step
 //    (far_block), so all warps run the same trip count (the chunk tail is
@@ -34,11 +36,23 @@ constexpr double kInv4Pi = 0.07957747154594767;  // 1 / (4 pi)
 //                  points, then C = V^-1 phi (ProxyFit::solve, sbb.cpp:103-108).
 //  MODE kDirectMode: kLeafMode with the ~1 ulp (cubic) reciprocal — the
 //                  direct sum, every source near-possible.
-constexpr int kTileThreads = 256;
-#ifndef SSUM_CHUNK
-#define SSUM_CHUNK 512
+// Launch shapes (threads per tile block, sources per chunk stage, resident
+// blocks per SM for the register budget), leaf/direct and fit separately.
+#ifndef SSUM_LEAF_THREADS
+#define SSUM_LEAF_THREADS 256
 #endif
-constexpr int kChunk = SSUM_CHUNK;  // sources per shared-memory stage
+#ifndef SSUM_CHUNK
+#define SSUM_CHUNK 768
+#endif
+#ifndef SSUM_FIT_CHUNK
+#define SSUM_FIT_CHUNK 768
+#endif
+constexpr int kLeafThreads = SSUM_LEAF_THREADS, kFitThreads = 256;
+constexpr int kLeafChunk = SSUM_CHUNK, kFitChunk = SSUM_FIT_CHUNK;
+#ifndef SSUM_STAGES
+#define SSUM_STAGES 2
+#endif
+constexpr int kStages = SSUM_STAGES;  // chunk buffers in flight
 constexpr int kLeafMode = 0, kFitMode = 1, kDirectMode = 2;
 #ifndef SSUM_NS
 #define SSUM_NS 2
@@ -54,10 +68,14 @@ constexpr int kPad = 32 * SSUM_NS;
 #ifndef SSUM_FIT_MINB
 #define SSUM_FIT_MINB 4
 #endif
+constexpr int kLeafMinB = SSUM_TILE_MINB, kFitMinB = SSUM_FIT_MINB;
 #ifndef SSUM_TPT
 #define SSUM_TPT 2
 #endif
-constexpr int kRangeCap = 512;
+#ifndef SSUM_RANGE_CAP
+#define SSUM_RANGE_CAP 128
+#endif
+constexpr int kRangeCap = SSUM_RANGE_CAP;
 constexpr int kTpt = SSUM_TPT;  // targets per thread (register tile)
 
 // Bulk-copy (TMA, non-tensor) helpers: the source ranges of a chunk are
@@ -72,6 +90,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned coun
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   unsigned done;
@@ -90,8 +111,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-template <int KER, int MODE>
-__global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB : SSUM_TILE_MINB)
+template <int KER, int MODE, int NTH, int CHUNK, int MINB>
+__global__ void __launch_bounds__(NTH, MINB)
     k_tiles(const Tile* __restrict__ tiles, int ntiles, const int* __restrict__ sel,
             const SrcRange* __restrict__ ranges, const double4* __restrict__ pts, double* __restrict__ S,
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
@@ -100,17 +121,21 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
   // dynamic shared memory (kTileSmem bytes): two source stages and the range
   // table; two mbarriers (one per stage)
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long bar[2];
+  // full[s]: the stage's bytes landed (producer arrival + transaction
+  // count); empty[s]: every warp is done reading it (one arrival per warp)
+  __shared__ unsigned long long full[kStages], empty[kStages];
+  constexpr int kChunk = CHUNK;
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
-  int2* rtab = reinterpret_cast<int2*>(smem + 2 * sizeof(double4) * (kChunk + kPad));
-  static_assert(sizeof(double) * kTileThreads * D * kTpt <= 2 * sizeof(double4) * (kChunk + kPad), "red alias");
+  int2* rtab = reinterpret_cast<int2*>(smem + kStages * sizeof(double4) * (kChunk + kPad));
+  static_assert(sizeof(double) * NTH * D * kTpt <= kStages * sizeof(double4) * (kChunk + kPad), "red alias");
+  static_assert(kPad <= NTH, "zero tail");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
   const int tix = sel ? sel[blockIdx.x] : static_cast<int>(blockIdx.x);
   const Tile T = tiles[tix];
   const int tc = T.tgt_count;
   const int th = (tc + kTpt - 1) / kTpt;  // thread-targets; thread slot u holds targets u, u + th, ...
-  const int G = min(32, kTileThreads / th);
+  const int G = min(32, NTH / th);
   const int tid = threadIdx.x, lane = tid & 31;
   const int u = tid % th, g = (tid / th) % G;
   int ti[kTpt];
@@ -124,18 +149,21 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
   const int total = (T.list_end > T.list_begin) ? ranges[T.list_end - 1].pad + ranges[T.list_end - 1].count : 0;
   const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
   if (tid < kPad) {  // zero tail: the stride-G walk may read up to kNs G - 1 entries past the chunk
-    buf[0][kChunk + tid] = zero4;
-    buf[1][kChunk + tid] = zero4;
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) buf[st][kChunk + tid] = zero4;
   }
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NTH / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const int nr = T.list_end - T.list_begin;
   const bool in_smem = nr <= kRangeCap;
   if (in_smem)
-    for (int r = tid; r < nr; r += kTileThreads) {
+    for (int r = tid; r < nr; r += NTH) {
       const SrcRange R = ranges[T.list_begin + r];
       rtab[r] = make_int2(R.begin, R.pad);
     }
@@ -160,18 +188,22 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
     const int r = locate(f);
     return rbegin(r) + (f - rpad(r));
   };
-  // Warp 0 issues chunk cc: one bulk copy per (range ∩ chunk), lane-parallel
-  // over the ranges; the stage's mbarrier expects the chunk's bytes. A
-  // partial (last) chunk's tail up to the zero pad is cleared with generic
-  // stores, visible to the block after the barrier that ends the previous
-  // chunk (or the prologue's).
+  // Warp 0 issues chunk cc into stage cc % kStages once every warp has
+  // released the stage's previous chunk: one bulk copy per (range ∩ chunk),
+  // lane-parallel over the ranges; the stage's full barrier expects the
+  // chunk's bytes. A partial (last) chunk's tail up to the zero pad is
+  // cleared with generic stores before the producer's arrival (release), so
+  // every warp that sees the phase complete sees the zeros.
   auto issue = [&](int cc) {
+    const int st = cc % kStages;
     const int c0 = cc * kChunk;
     const int cn = min(kChunk, total - c0);
-    double4* dst = buf[cc & 1];
-    if (lane == 0) mbar_expect_tx(&bar[cc & 1], static_cast<unsigned>(cn) * sizeof(double4));
-    __syncwarp();
+    double4* dst = buf[st];
+    if (cc >= kStages) mbar_wait(&empty[st], ((cc / kStages) - 1) & 1);
     for (int e = cn + lane; e < min(kChunk, cn + kPad); e += 32) dst[e] = zero4;
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(&full[st], static_cast<unsigned>(cn) * sizeof(double4));
+    __syncwarp();
     for (int r = locate(c0) + lane;; r += 32) {
       bool more_r = false;
       if (r < nr) {
@@ -182,7 +214,7 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
           const int lo = max(pad, c0), hi = min(end, c0 + cn);
           if (hi > lo)
             bulk_g2s(dst + (lo - c0), pts + rbegin(r) + (lo - pad), static_cast<unsigned>(hi - lo) * sizeof(double4),
-                     &bar[cc & 1]);
+                     &full[st]);
         }
       }
       if (!__any_sync(0xffffffffu, more_r)) break;
@@ -197,14 +229,14 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
   const int kStep = kNs * G;
   const int steps_full = (kChunk + kStep - 1) / kStep;
   const int steps_last = (total - (nch - 1) * kChunk + kStep - 1) / kStep;
-  if (nch > 0 && tid < 32) issue(0);
-  if (nch == 1) __syncthreads();  // its zeroed tail (later chunks: the barrier ending the chunk before)
+  if (tid < 32)
+    for (int cc = 0; cc < min(nch, kStages - 1); ++cc) issue(cc);
   for (int c = 0; c < nch; ++c) {
     const bool more = c + 1 < nch;
-    if (more && tid < 32) issue(c + 1);  // stage (c + 1) & 1 was released by the barrier ending chunk c - 1
-    mbar_wait(&bar[c & 1], (c >> 1) & 1);
+    if (tid < 32 && c + kStages - 1 < nch) issue(c + kStages - 1);
+    mbar_wait(&full[c % kStages], (c / kStages) & 1);
     const int n = min(kChunk, total - c * kChunk);
-    const double4* B = buf[c & 1] + g;  // this lane's sources: B[m G], m = 0, 1, ...
+    const double4* B = buf[c % kStages] + g;  // this lane's sources: B[m G], m = 0, 1, ...
     const int steps = more ? steps_full : steps_last;
     // steps covering the chunk's near-possible prefix [0, near_total - c kChunk):
     // the same staged blocks with near pairs masked and counted, checked
@@ -260,46 +292,59 @@ __global__ void __launch_bounds__(kTileThreads, MODE == kFitMode ? SSUM_FIT_MINB
     const double4* Bp = B + it * kStep;
 #pragma unroll 2
     for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a);
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[c % kStages]);  // this warp is done with the stage
   }
+  __syncthreads();  // every warp done with every stage: red may alias them
 #pragma unroll
   for (int q = 0; q < kTpt; ++q)
 #pragma unroll
-    for (int d = 0; d < D; ++d) red[(q * kTileThreads + tid) * D + d] = a[q].s[d];
+    for (int d = 0; d < D; ++d) red[(q * NTH + tid) * D + d] = a[q].s[d];
   __syncthreads();
   // target tt = u + q th lives in slot (q, g * th + u) for every group g
-  double s[D];
-  const int tt = tid;
-  const int uq = tt % th, qq = tt / th;
-  if (tt < tc) {
+  constexpr int kOut = (kTileTargets + NTH - 1) / NTH;  // targets per thread in the epilogue
+  double s[kOut][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) s[d] = red[(qq * kTileThreads + uq) * D + d];
-    for (int gg = 1; gg < G; ++gg)
-#pragma unroll
-      for (int d = 0; d < D; ++d) s[d] += red[(qq * kTileThreads + gg * th + uq) * D + d];
-  }
-  const int i_out = T.tgt_begin + tt;
-  if constexpr (MODE != kFitMode) {
+  for (int o = 0; o < kOut; ++o) {
+    const int tt = tid + o * NTH;
+    const int uq = tt % th, qq = tt / th;
     if (tt < tc) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) S[size_t(i_out) * D + d] = s[d];
+      for (int d = 0; d < D; ++d) s[o][d] = red[(qq * NTH + uq) * D + d];
+      for (int gg = 1; gg < G; ++gg)
+#pragma unroll
+        for (int d = 0; d < D; ++d) s[o][d] += red[(qq * NTH + gg * th + uq) * D + d];
+    }
+  }
+  if constexpr (MODE != kFitMode) {
+#pragma unroll
+    for (int o = 0; o < kOut; ++o) {
+      const int tt = tid + o * NTH;
+      if (tt < tc) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) S[size_t(T.tgt_begin + tt) * D + d] = s[o][d];
+      }
     }
   } else {
     __syncthreads();  // red is reused for phi below
     double* phi = red;
-    if (tt < tc) {
-      const double4 xo = pts[i_out];
-      if constexpr (KER == kBS) {
-        phi[tt] = xo.y * s[2] - xo.z * s[1];
-        phi[P + tt] = xo.z * s[0] - xo.x * s[2];
-        phi[2 * P + tt] = xo.x * s[1] - xo.y * s[0];
-      } else {
-        phi[tt] = -kInv4Pi * s[0];
+#pragma unroll
+    for (int o = 0; o < kOut; ++o) {
+      const int tt = tid + o * NTH;
+      if (tt < tc) {
+        const double4 xo = pts[T.tgt_begin + tt];
+        if constexpr (KER == kBS) {
+          phi[tt] = xo.y * s[o][2] - xo.z * s[o][1];
+          phi[P + tt] = xo.z * s[o][0] - xo.x * s[o][2];
+          phi[2 * P + tt] = xo.x * s[o][1] - xo.y * s[o][0];
+        } else {
+          phi[tt] = -kInv4Pi * s[o][0];
+        }
       }
     }
     __syncthreads();
     const int slot = pslot[fit_nodes[tix]];
-    for (int kk = tid; kk < P; kk += kTileThreads) {
+    for (int kk = tid; kk < P; kk += NTH) {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
         double acc = 0.0;
@@ -328,51 +373,58 @@ __global__ void k_direct_finish(int64_t n, const double4* __restrict__ pts, cons
 
 __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nt = (n + kTileThreads - 1) / kTileThreads;
+  const int64_t nt = (n + kTileTargets - 1) / kTileTargets;
   if (t == 0) *range = SrcRange{0, static_cast<int>(n), 1, 0};
   if (t >= nt) return;
-  const int64_t rem = n - t * kTileThreads;
+  const int64_t rem = n - t * kTileTargets;
   // one range [0, n): the self source of target i sits at flattened position i
-  tiles[t] = Tile{static_cast<int>(t * kTileThreads), static_cast<int>(rem < kTileThreads ? rem : kTileThreads), 0, 1,
+  tiles[t] = Tile{static_cast<int>(t * kTileTargets), static_cast<int>(rem < kTileTargets ? rem : kTileTargets), 0, 1,
                   static_cast<int>(n), 0, 1, 0};
 }
 
-constexpr size_t kTileSmem = 2 * sizeof(double4) * (kChunk + kPad) + sizeof(int2) * kRangeCap;
+template <int CHUNK>
+constexpr size_t tile_smem() {
+  return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap;
+}
 
 // k_tiles instantiation with its dynamic shared-memory limit raised once
 // (per process; every context's device is an sm_100a part)
-template <int KER, int MODE>
+template <int KER, int MODE, int NTH, int CHUNK, int MINB>
 auto tiles_kernel() {
   static const bool ready = [] {
-    SSUM_CUDA_CHECK(cudaFuncSetAttribute(k_tiles<KER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kTileSmem)));
+    SSUM_CUDA_CHECK(cudaFuncSetAttribute(k_tiles<KER, MODE, NTH, CHUNK, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(tile_smem<CHUNK>())));
     return true;
   }();
   (void)ready;
-  return k_tiles<KER, MODE>;
+  return k_tiles<KER, MODE, NTH, CHUNK, MINB>;
 }
 
 }  // namespace
 
 void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
   Lists& L = c.lists;
-  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode>() : tiles_kernel<kLOG, kFitMode>();
-  k<<<nfit, kTileThreads, kTileSmem, c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
+  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>()
+                          : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>();
+  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
                                                  c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
 }
 
 void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct) {
-  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode>() : tiles_kernel<kLOG, kDirectMode>())
-                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode>() : tiles_kernel<kLOG, kLeafMode>());
-  k<<<ntl, kTileThreads, kTileSmem, c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
+  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>()
+                                   : tiles_kernel<kLOG, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>())
+                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>()
+                                   : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>());
+  k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
                                                 nullptr, nullptr, 0, nullptr);
 }
 
 // Direct sum (treecode.cpp:246-264): every target against one range [0, n)
 // in the caller's order.
 void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out) {
-  const int64_t nt = (n + kTileThreads - 1) / kTileThreads;
+  const int64_t nt = (n + kTileTargets - 1) / kTileTargets;
   c.direct_tiles.ensure(size_t(nt));
   c.direct_range.ensure(1);
   const int bs = 256;
