@@ -147,7 +147,7 @@ struct Tile {
   int near_total;            // sources in the leading near-possible ranges
   int self_shift;  // self source of target i at flattened list position i + self_shift
   int has_self;    // 0: no range holds the targets themselves
-  int pad;
+  int total;       // sources in the flattened list (sum of the ranges' counts)
 };
 // Arc-length margin below which a (target leaf, source node) pair may hold a
 // near pair: den = 2 sin^2(arc/2) < 2^-20 <=> arc < 1.3811e-3 rad.

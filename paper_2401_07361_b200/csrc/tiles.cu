@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     ti[q] = T.tgt_begin + (tt < tc ? tt : u);  // padding slots repeat target u (discarded)
     x[q] = pts[ti[q]];
   }
-  const int total = (T.list_end > T.list_begin) ? ranges[T.list_end - 1].pad + ranges[T.list_end - 1].count : 0;
+  const int total = T.total;
   const double4 zero4 = make_double4(0.0, 0.0, 0.0, 0.0);
   if (tid < kPad) {  // zero tail: the stride-G walk may read up to kNs G - 1 entries past the chunk
 #pragma unroll
@@ -162,12 +162,6 @@ __global__ void __launch_bounds__(NTH, MINB)
   }
   const int nr = T.list_end - T.list_begin;
   const bool in_smem = nr <= kRangeCap;
-  if (in_smem)
-    for (int r = tid; r < nr; r += NTH) {
-      const SrcRange R = ranges[T.list_begin + r];
-      rtab[r] = make_int2(R.begin, R.pad);
-    }
-  __syncthreads();
   auto rbegin = [&](int r) { return in_smem ? rtab[r].x : ranges[T.list_begin + r].begin; };
   auto rpad = [&](int r) { return in_smem ? rtab[r].y : ranges[T.list_begin + r].pad; };
   // flattened list position -> range (binary search over the range prefixes)
@@ -194,7 +188,9 @@ __global__ void __launch_bounds__(NTH, MINB)
   // chunk's bytes. A partial (last) chunk's tail up to the zero pad is
   // cleared with generic stores before the producer's arrival (release), so
   // every warp that sees the phase complete sees the zeros.
-  auto issue = [&](int cc) {
+  // glob: read the ranges from global memory (chunk 0, issued before the
+  // range table is in shared memory)
+  auto issue = [&](int cc, bool glob) {
     const int st = cc % kStages;
     const int c0 = cc * kChunk;
     const int cn = min(kChunk, total - c0);
@@ -204,36 +200,53 @@ __global__ void __launch_bounds__(NTH, MINB)
     __syncwarp();
     if (lane == 0) mbar_expect_tx(&full[st], static_cast<unsigned>(cn) * sizeof(double4));
     __syncwarp();
-    for (int r = locate(c0) + lane;; r += 32) {
+    for (int r = (c0 == 0 ? 0 : locate(c0)) + lane;; r += 32) {
       bool more_r = false;
       if (r < nr) {
-        const int pad = rpad(r);
+        int pad, beg, end;
+        if (glob) {
+          const SrcRange R = ranges[T.list_begin + r];
+          pad = R.pad, beg = R.begin, end = R.pad + R.count;
+        } else {
+          pad = rpad(r), beg = rbegin(r), end = (r + 1 < nr) ? rpad(r + 1) : total;
+        }
         if (pad < c0 + cn) {
           more_r = true;
-          const int end = (r + 1 < nr) ? rpad(r + 1) : total;
           const int lo = max(pad, c0), hi = min(end, c0 + cn);
           if (hi > lo)
-            bulk_g2s(dst + (lo - c0), pts + rbegin(r) + (lo - pad), static_cast<unsigned>(hi - lo) * sizeof(double4),
+            bulk_g2s(dst + (lo - c0), pts + beg + (lo - pad), static_cast<unsigned>(hi - lo) * sizeof(double4),
                      &full[st]);
         }
       }
       if (!__any_sync(0xffffffffu, more_r)) break;
     }
   };
+  // chunk 0 goes out first (warp 0, ranges straight from global memory),
+  // while the block stages the range table and its target points
+  const int nch = (total + kChunk - 1) / kChunk;
+  if (tid < 32 && nch > 0) {
+    __syncwarp();  // barrier init (thread 0) before the first arrival
+    issue(0, true);
+  }
+  if (in_smem)
+    for (int r = tid; r < nr; r += NTH) {
+      const SrcRange R = ranges[T.list_begin + r];
+      rtab[r] = make_int2(R.begin, R.pad);
+    }
+  __syncthreads();
   Acc<KER> a[kTpt];
 #pragma unroll
   for (int q = 0; q < kTpt; ++q) a[q].zero();
-  const int nch = (total + kChunk - 1) / kChunk;
   // steps of kNs sources per lane per chunk: a chunk of n sources takes
   // ceil(n / (kNs G)) steps (the zero-padded tail contributes nothing)
   const int kStep = kNs * G;
   const int steps_full = (kChunk + kStep - 1) / kStep;
   const int steps_last = (total - (nch - 1) * kChunk + kStep - 1) / kStep;
   if (tid < 32)
-    for (int cc = 0; cc < min(nch, kStages - 1); ++cc) issue(cc);
+    for (int cc = 1; cc < min(nch, kStages - 1); ++cc) issue(cc, false);
   for (int c = 0; c < nch; ++c) {
     const bool more = c + 1 < nch;
-    if (tid < 32 && c + kStages - 1 < nch) issue(c + kStages - 1);
+    if (tid < 32 && c + kStages - 1 < nch) issue(c + kStages - 1, false);
     mbar_wait(&full[c % kStages], (c / kStages) & 1);
     const int n = min(kChunk, total - c * kChunk);
     const double4* B = buf[c % kStages] + g;  // this lane's sources: B[m G], m = 0, 1, ...
@@ -379,7 +392,7 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
   const int64_t rem = n - t * kTileTargets;
   // one range [0, n): the self source of target i sits at flattened position i
   tiles[t] = Tile{static_cast<int>(t * kTileTargets), static_cast<int>(rem < kTileTargets ? rem : kTileTargets), 0, 1,
-                  static_cast<int>(n), 0, 1, 0};
+                  static_cast<int>(n), 0, 1, static_cast<int>(n)};
 }
 
 template <int CHUNK>

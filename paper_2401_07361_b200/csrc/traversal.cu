@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       t.near_total = near_total;
       t.self_shift = self_shift;
       t.has_self = has_self;
-      t.pad = 0;
+      t.total = cur.src;
       tiles[tile_off[k] + j] = t;
       const unsigned long long tc = static_cast<unsigned long long>(t.tgt_count);
       tile_cost[tile_off[k] + j] = make_ulonglong2(tc * src_pp - tc, tc * src_pc);  // self pairs excluded
@@ -578,7 +578,8 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       tl.list_begin = w0;
       tl.list_end = w0 + cur.w;
       tl.near_total = 0;  // CP / CC pairs are well separated
-      tl.self_shift = tl.has_self = tl.pad = 0;
+      tl.self_shift = tl.has_self = 0;
+      tl.total = cur.src;
       tiles[k] = tl;
       cp = static_cast<unsigned long long>(P) * static_cast<unsigned long long>(ncp);
       cc = static_cast<unsigned long long>(P) * static_cast<unsigned long long>(P) * static_cast<unsigned long long>(ncc);
