@@ -259,6 +259,85 @@ __global__ void k_finish(int64_t p0, int64_t p1, const double4* __restrict__ pts
   }
 }
 
+// Phase 4 downward part + finish over tree positions [p0, p1) (one thread
+// each, consecutive positions share their ancestors): the same arithmetic as
+// k_finish, but each fit ancestor's D x P coefficients and Cramer constants
+// are staged once per warp in shared memory and read back as warp-uniform
+// (broadcast) shared loads — k_finish's per-lane global loads of them kept
+// the L1 data pipe ~88% busy. Lanes walk their ancestor chains in lockstep;
+// at each step the warp stages every distinct fit ancestor among its lanes in
+// turn (normally one, two where the warp straddles a node boundary).
+constexpr int kFinWarps = 4;
+template <int KER, int DEG>
+__global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
+    int64_t p0, int64_t p1, const double4* __restrict__ pts, const double* __restrict__ S,
+    const int* __restrict__ pos_leaf, const int* __restrict__ parent, const int* __restrict__ pslot,
+    const unsigned char* __restrict__ is_fit, const double* __restrict__ cramer, const double* __restrict__ coeff,
+    const int* __restrict__ perm, double* __restrict__ out) {
+  constexpr int D = KDim<KER>::D;
+  constexpr int P = Sbb<DEG>::P;
+  constexpr int DP = D == 3 ? 4 : 1;  // staged row: (c_0, c_1, c_2, pad) per basis function
+  __shared__ __align__(16) double cs[kFinWarps][P * DP];
+  __shared__ __align__(16) double cr[kFinWarps][12];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const int64_t k = p0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool valid = k < p1;
+  const double4 x = valid ? pts[k] : make_double4(0.0, 0.0, 0.0, 0.0);
+  double val[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) val[d] = 0.0;
+  int a = valid ? pos_leaf[k] : -1;
+  while (__any_sync(full, a >= 0)) {
+    const bool fit = a >= 0 && is_fit[a];
+    unsigned pend = __ballot_sync(full, fit);
+    while (pend) {
+      const int an = __shfl_sync(full, a, __ffs(pend) - 1);
+      const bool mine = fit && a == an;
+      const double* c = coeff + size_t(pslot[an]) * D * P;
+      for (int i = lane; i < D * P; i += 32) cs[w][(i % P) * DP + i / P] = c[i];
+      if (lane < 12) cr[w][lane] = cramer[12 * an + lane];
+      __syncwarp();
+      if (mine) {
+        double b1, b2, b3;
+        bary(cr[w], x.x, x.y, x.z, b1, b2, b3);
+        double q1[DEG + 1], q2[DEG + 1], q3[DEG + 1];
+        powers<DEG>(b1, b2, b3, q1, q2, q3);
+        int m = 0;
+#pragma unroll
+        for (int kk = 0; kk <= DEG; ++kk) {
+#pragma unroll
+          for (int jj = 0; jj <= DEG - kk; ++jj, ++m) {
+            const double B = q1[DEG - kk - jj] * q2[jj] * q3[kk];
+            if constexpr (D == 3) {
+              const double2 c01 = *reinterpret_cast<const double2*>(&cs[w][m * 4]);
+              val[0] = fma(c01.x, B, val[0]);
+              val[1] = fma(c01.y, B, val[1]);
+              val[2] = fma(cs[w][m * 4 + 2], B, val[2]);
+            } else {
+              val[0] = fma(cs[w][m], B, val[0]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      pend &= ~__ballot_sync(full, mine);
+    }
+    a = a >= 0 ? parent[a] : -1;
+  }
+  if (!valid) return;
+  const int64_t o = perm[k];
+  if constexpr (KER == kBS) {
+    const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
+    const double pref = -kInv4Pi;  // BiotSavartKernel::prefactor (kernels.hpp:54)
+    out[3 * size_t(o)] = pref * ((x.y * s2 - x.z * s1) + val[0]);
+    out[3 * size_t(o) + 1] = pref * ((x.z * s0 - x.x * s2) + val[1]);
+    out[3 * size_t(o) + 2] = pref * ((x.x * s1 - x.y * s0) + val[2]);
+  } else {
+    out[o] = -kInv4Pi * S[k] + val[0];
+  }
+}
+
 __global__ void k_inv_perm(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k < n) inv[perm[k]] = static_cast<int>(k);
@@ -273,10 +352,15 @@ void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, 
   if (n <= 0) return;
 #define SSUM_FINISH_CASE(DG)                                                                                   \
   case DG:                                                                                                    \
-    k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p,          \
-                                                             c.nodes.parent.p, L.pslot.p, L.is_fit.p,         \
-                                                             c.nodes.cramer.p, c.coeff.p, B.perm.p, d_out,    \
-                                                             inv, i0, i1);                                    \
+    if (inv)                                                                                                  \
+      k_finish<KER, DG><<<grid_for(n, bs), bs, 0, c.stream>>>(L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p,        \
+                                                               c.nodes.parent.p, L.pslot.p, L.is_fit.p,       \
+                                                               c.nodes.cramer.p, c.coeff.p, B.perm.p, d_out,  \
+                                                               inv, i0, i1);                                  \
+    else                                                                                                      \
+      k_finish_tree<KER, DG><<<grid_for(n, 32 * kFinWarps), 32 * kFinWarps, 0, c.stream>>>(                   \
+          L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p, c.nodes.parent.p, L.pslot.p, L.is_fit.p, c.nodes.cramer.p, \
+          c.coeff.p, B.perm.p, d_out);                                                                        \
     break;
   switch (degree) {
     SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
