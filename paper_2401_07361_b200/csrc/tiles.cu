@@ -69,6 +69,14 @@ constexpr int kPad = 32 * SSUM_NS;
 #define SSUM_FIT_MINB 4
 #endif
 constexpr int kLeafMinB = SSUM_TILE_MINB, kFitMinB = SSUM_FIT_MINB;
+#ifndef SSUM_FAST_UNROLL
+#define SSUM_FAST_UNROLL 4
+#endif
+#ifndef SSUM_NEAR_UNROLL
+#define SSUM_NEAR_UNROLL 2
+#endif
+// far_block steps per loop trip (fast loop: leaf/direct tiles; fit tiles 2)
+constexpr int kFastUnroll = SSUM_FAST_UNROLL, kNearUnroll = SSUM_NEAR_UNROLL;
 #ifndef SSUM_TPT
 #define SSUM_TPT 2
 #endif
@@ -118,6 +126,7 @@ __global__ void __launch_bounds__(NTH, MINB)
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
             const double* __restrict__ vinv, int P, double* __restrict__ coeff) {
   constexpr int D = KDim<KER>::D;
+  constexpr int kFU = MODE == kFitMode ? 2 : kFastUnroll;
   // dynamic shared memory (kTileSmem bytes): two source stages and the range
   // table; two mbarriers (one per stage)
   extern __shared__ __align__(16) unsigned char smem[];
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(NTH, MINB)
       // past 32 are all re-walked when a repair is needed
       int ncnt = 0;
       unsigned hit = 0;
-#pragma unroll 2
+#pragma unroll kNearUnroll
       for (; it < near_steps; ++it) {
         const int before = ncnt;
         far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt);
@@ -303,7 +312,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     // well-separated sources only: branch-free, kNs sources x kTpt targets
     // of independent chains per step (zero-padded tail contributes 0)
     const double4* Bp = B + it * kStep;
-#pragma unroll 2
+#pragma unroll kFU
     for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[c % kStages]);  // this warp is done with the stage

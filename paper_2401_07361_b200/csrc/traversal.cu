@@ -161,7 +161,7 @@ __global__ void k_root_pairs(PairEntry* F) {
 // traversal step by step). out: [0] steps, [1] overflow, [2] largest frontier.
 constexpr int kBfsThreads = 256;
 #ifndef SSUM_BFS_MINB
-#define SSUM_BFS_MINB 1
+#define SSUM_BFS_MINB 4
 #endif
 __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
     k_bfs(const int* __restrict__ cnt, const int* __restrict__ off, int rlo, int rhi,
@@ -188,13 +188,17 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
     const int per = (m + nb - 1) / nb;
     const int lo = min(m, b * per), hi = min(m, lo + per);
     unsigned long long run = 0;  // (emissions << 32) | child slots, this block so far
+    // decide the whole slice first (no block-wide sync between pairs, so
+    // each thread keeps several pairs' node loads in flight), then scan it
+#pragma unroll 4
+    for (int k = lo + tid; k < hi; k += kBfsThreads)
+      action[k] = pair_action(Fc[k].t, Fc[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
+                              max_depth, pc_only);
     for (int base = lo; base < hi; base += kBfsThreads) {
       const int k = base + tid;
       unsigned long long v = 0;
       if (k < hi) {
-        const int a = pair_action(Fc[k].t, Fc[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta,
-                                  thr, max_depth, pc_only);
-        action[k] = a;
+        const int a = action[k];  // this thread's own store
         v = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
       }
       unsigned long long ex, agg;
