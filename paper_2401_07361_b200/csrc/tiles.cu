@@ -186,10 +186,16 @@ __global__ void __launch_bounds__(NTH, MINB)
     return lo;
   };
   // point index of flattened position f (-1 past the list): near repair only
+  // (a lane's repairs visit non-decreasing positions within a chunk: one
+  // search per chunk, then a forward scan from the last range found)
+  int rcur = -1;
   auto jof = [&](int f) {
     if (f >= total) return -1;
-    const int r = locate(f);
-    return rbegin(r) + (f - rpad(r));
+    if (rcur < 0)
+      rcur = locate(f);
+    else
+      while (rcur + 1 < nr && rpad(rcur + 1) <= f) ++rcur;
+    return rbegin(rcur) + (f - rpad(rcur));
   };
   // Warp 0 issues chunk cc into stage cc % kStages once every warp has
   // released the stage's previous chunk: one bulk copy per (range ∩ chunk),
@@ -274,14 +280,14 @@ __global__ void __launch_bounds__(NTH, MINB)
     int it = 0;
     if (near_steps > 0) {
       // bit `it` of hit: step `it` met a masked pair (self or near); steps
-      // past 32 are all re-walked when a repair is needed
+      // past 64 are all re-walked when a repair is needed
       int ncnt = 0;
-      unsigned hit = 0;
+      unsigned long long hit = 0;
 #pragma unroll kNearUnroll
       for (; it < near_steps; ++it) {
         const int before = ncnt;
         far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt);
-        hit |= static_cast<unsigned>(ncnt != before) << (it & 31);
+        hit |= static_cast<unsigned long long>(ncnt != before) << (it & 63);
       }
       // self pairs this lane walked in this chunk's near steps: the self
       // source of target ti sits at flattened position ti + T.self_shift
@@ -296,10 +302,11 @@ __global__ void __launch_bounds__(NTH, MINB)
         // only the steps that met a masked pair (dense inputs: a handful of
         // the chunk's near steps)
         const int f0 = c * kChunk + g;
-        if (near_steps <= 32) {
+        rcur = -1;
+        if (near_steps <= 64) {
 #pragma unroll 1
-          for (unsigned m = hit; m; m &= m - 1) {
-            const int r = __ffs(m) - 1;
+          for (unsigned long long m = hit; m; m &= m - 1) {
+            const int r = __ffsll(static_cast<long long>(m)) - 1;
             near_repair<KER, kTpt, kNs>(x, B + r * kStep, f0 + r * kStep, jof, G, a, ti, flags);
           }
         } else {

@@ -258,7 +258,13 @@ __global__ void k_descend(const double* __restrict__ xyz, int64_t n, int* __rest
 // (alpha >= ~50 deg the triangle angles, h <= ~1 the heights): below -4e-9,
 // 40x beyond the -1e-10 containment tolerance and the 1e-13 guard band. The
 // first-containing descent (face_tree.cpp:50-69) therefore ends at this
-// node, and the shortcut returns exactly what the walk would.
+// node, and the shortcut returns exactly what the walk would. The same holds
+// for any node x lies that deep inside (a node contains its descendants, so
+// x is at least as deep inside every ancestor): when the guessed leaf fails
+// the test — x moved, or sits on the leaf's boundary, as a third of the
+// mesh vertices do — the walk resumes from the guess's deepest ancestor that
+// passes it, descending from there with the ordinary child choice, and only
+// falls back to the root when none does.
 constexpr double kGuessMargin = 1e-8;
 __device__ __forceinline__ bool deep_inside(const d3& p, const double* __restrict__ k) {
   const double sg = k[3] < 0.0 ? -1.0 : 1.0;  // inside: x . n_j has det's sign
@@ -275,7 +281,8 @@ __device__ __forceinline__ bool deep_inside(const d3& p, const double* __restric
 __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const int* __restrict__ order,
                        const double* __restrict__ tri,
                        const double* __restrict__ cramer, const double* __restrict__ center,
-                       const int* __restrict__ child_base, const unsigned long long* __restrict__ nkey,
+                       const int* __restrict__ child_base, const int* __restrict__ parent,
+                       const unsigned long long* __restrict__ nkey,
                        unsigned long long* __restrict__ key, int* __restrict__ ids, int* __restrict__ leaf_of,
                        int guess_nodes, int* __restrict__ flags) {
   __shared__ double st[20 * 9];
@@ -293,15 +300,23 @@ __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, c
   const d3 p = load3(xyz + 3 * i);
   // guess_nodes > 0: leaf_of holds the previous call's leaves (node ids
   // below guess_nodes)
+  int node = -1;
   if (guess_nodes > 0) {
     const int g = leaf_of[i];
-    if (g >= 0 && g < guess_nodes && child_base[g] < 0 && deep_inside(p, cramer + 12 * g)) {
-      key[i] = nkey[g];
-      ids[i] = static_cast<int>(i);
-      return;  // leaf_of[i] stays g
+    if (g >= 0 && g < guess_nodes) {
+      if (child_base[g] < 0 && deep_inside(p, cramer + 12 * g)) {
+        key[i] = nkey[g];
+        ids[i] = static_cast<int>(i);
+        return;  // leaf_of[i] stays g
+      }
+      for (int a = parent[g]; a >= 0; a = parent[a])
+        if (deep_inside(p, cramer + 12 * a)) {
+          node = a;
+          break;
+        }
     }
   }
-  int node = find_root(p, st, skr, sc);
+  if (node < 0) node = find_root(p, st, skr, sc);
   if (node < 0) {
     atomicOr(flags, kFlagGeometry);
     key[i] = ~0ull;
@@ -547,8 +562,8 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
     if (pieces > 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[j], 0));
     if (b <= a) continue;
     k_walk<<<grid_for(b - a, bs), bs, 0, c.stream>>>(d_xyz, a, b, order, T.tri.p, T.cramer.p, T.center.p,
-                                                     T.child_base.p, T.key.p, B.wkey.p, B.sort_vals.p, B.leaf_of.p,
-                                                     guess_nodes, c.d_flags.p);
+                                                     T.child_base.p, T.parent.p, T.key.p, B.wkey.p, B.sort_vals.p,
+                                                     B.leaf_of.p, guess_nodes, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
   }
   const int begin_bit = kKeyRootShift - 2 * T.max_level;
