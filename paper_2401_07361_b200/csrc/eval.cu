@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
     a = a >= 0 ? parent[a] : -1;
   }
   if (!valid) return;
-  const int64_t o = perm[k];
+  const int64_t o = perm ? perm[k] : k;  // no perm: tree order (in place over S is safe: own row only)
   if constexpr (KER == kBS) {
     const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
     const double pref = -kInv4Pi;  // BiotSavartKernel::prefactor (kernels.hpp:54)
@@ -338,13 +338,29 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
   }
 }
 
+// Caller-order rows [i0, i1) of a tree-order result (host pieces after a
+// tree-order finish); rows outside this part's positions [p0, p1) are left
+// as they are, like k_finish leaves them.
+__global__ void k_gather_rows(const double* __restrict__ R, const int* __restrict__ inv, int64_t i0, int64_t i1,
+                              int64_t p0, int64_t p1, int D, double* __restrict__ out) {
+  const int64_t o = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= i1) return;
+  const int64_t k = inv[o];
+  if (k < p0 || k >= p1) return;
+  for (int d = 0; d < D; ++d) out[o * D + d] = R[k * D + d];
+}
+
 __global__ void k_inv_perm(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k < n) inv[perm[k]] = static_cast<int>(k);
 }
 
+// inv: finish caller-order rows [i0, i1) (per-lane k_finish); otherwise the
+// part's tree positions with k_finish_tree, written to d_out in caller order
+// (perm) or, with tree_order, in tree order.
 template <int KER>
-void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, int64_t i0 = 0, int64_t i1 = 0) {
+void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, int64_t i0 = 0, int64_t i1 = 0,
+                   bool tree_order = false) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   const int bs = 128;
@@ -360,7 +376,7 @@ void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, 
     else                                                                                                      \
       k_finish_tree<KER, DG><<<grid_for(n, 32 * kFinWarps), 32 * kFinWarps, 0, c.stream>>>(                   \
           L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p, c.nodes.parent.p, L.pslot.p, L.is_fit.p, c.nodes.cramer.p, \
-          c.coeff.p, B.perm.p, d_out);                                                                        \
+          c.coeff.p, tree_order ? nullptr : B.perm.p, d_out);                                                 \
     break;
   switch (degree) {
     SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
@@ -571,12 +587,30 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     k_inv_perm<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, c.inv_perm.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
+    // Spatially coherent caller order (a warp's rows share ancestors): finish
+    // each piece directly in caller order. Otherwise (e.g. random input) the
+    // per-lane finish would walk unrelated ancestors in every lane: finish
+    // in tree order in place over S, then gather each piece's rows.
+    const bool gather = !B.input_coherent;
+    if (gather) {
+      if (kernel == kBS)
+        launch_finish<kBS>(c, degree, c.S.p, nullptr, 0, 0, true);
+      else
+        launch_finish<kLOG>(c, degree, c.S.p, nullptr, 0, 0, true);
+    }
     for (int j = 0; j < Ctx::kIoChunks; ++j) {
       const int64_t a = c.io.bounds[j], b = c.io.bounds[j + 1];
-      if (kernel == kBS)
+      if (gather) {
+        if (b > a) {
+          k_gather_rows<<<grid_for(b - a, bs), bs, 0, c.stream>>>(c.S.p, c.inv_perm.p, a, b, L.p0, L.p1, D, d_out);
+          SSUM_LAUNCH_CHECK();
+          c.launches++;
+        }
+      } else if (kernel == kBS) {
         launch_finish<kBS>(c, degree, d_out, c.inv_perm.p, a, b);
-      else
+      } else {
         launch_finish<kLOG>(c, degree, d_out, c.inv_perm.p, a, b);
+      }
       SSUM_CUDA_CHECK(cudaEventRecord(c.io.out[j], c.stream));
       SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, c.io.out[j], 0));
       if (j == 0) SSUM_CUDA_CHECK(cudaEventRecord(c.io.t0, c.copy_stream));

@@ -1,8 +1,9 @@
-"""Phase trace of the host-pointer entry (ssum_treecode_sum) at config 4 from
-pinned buffers: wall time of each call, its H2D / D2H seconds and, with
-SSUM_TRACE=1, the library's host-side phase marks (stderr).
+"""Phase trace of the host-pointer entry (ssum_treecode_sum) from pinned
+buffers at one BASELINE config (bench.py's fixtures; default c4): wall time
+of each call, its H2D / D2H seconds and, with SSUM_TRACE=1, the library's
+host-side phase marks (stderr).
 
-    SSUM_TRACE=1 python tools/e2e_trace.py [calls]
+    SSUM_TRACE=1 python tools/e2e_trace.py [calls] [config]
 """
 import json
 import sys
@@ -13,14 +14,16 @@ import torch
 sys.path.insert(0, ".")
 import paper_2401_07361_b200 as ss  # noqa: E402
 
+import bench  # noqa: E402
+
 calls = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-xyz, area = ss.make_icosa_mesh(9)
-q = ss.rh4_vorticity(xyz) * area
+bench.use_config(sys.argv[2] if len(sys.argv) > 2 else "c4")
+xyz, q, _ = bench.fixture()
 n = xyz.shape[0]
 h_xyz = torch.from_numpy(xyz).pin_memory()
 h_q = torch.from_numpy(q).pin_memory()
 h_out = torch.zeros((n, 3), dtype=torch.float64).pin_memory()
-cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+cfg = ss.TraversalConfig(**bench.CFG)
 tree = ss.FaceTree(0)
 for k in range(calls):
     st = ss.TreecodeStats()
