@@ -7,6 +7,8 @@ Prints one JSON line. With SSUM_TRACE=1 each evaluation's phases go to stderr
 (bin.reuse = walk + sort through the existing tree).
 
     python tools/rk4_bench.py [--steps 3] [--level 9] [--reference]
+
+(--steps 49: config 4's full 50-step run, the warm-up step included.)
 """
 import argparse
 import json
@@ -41,6 +43,15 @@ line = {"metric": "BVE RK4 velocity evals/s (config 4, fp64)", "value": n * eval
         "n": n, "rk4_steps": args.steps, "evaluations": evals, "ms_per_evaluation": dt * 1e3 / evals,
         "dt": 0.01, "omega": 2 * np.pi,
         "note": "wall time of ss.rk4 (one H2D of x, zeta, A and one D2H at the ends); tree reused across stages"}
+# invariants after 1 + steps RK4 steps from the initial state: absolute
+# vorticity zeta + 2 Omega z is carried by each particle (d zeta/dt =
+# -2 Omega u_z, dz/dt = u_z), and positions stay on the unit sphere
+om = 2 * np.pi
+drift = np.abs((z1 + 2 * om * x1[:, 2]) - (zeta + 2 * om * xyz[:, 2]))
+line["invariants"] = {"rk4_steps_total": 1 + args.steps,
+                      "max_abs_vorticity_drift": float(drift.max()),
+                      "max_abs_zeta": float(np.abs(zeta).max()),
+                      "max_unit_norm_error": float(np.abs(np.linalg.norm(x1, axis=1) - 1.0).max())}
 if args.reference:
     import oracle_lib as ol
 
