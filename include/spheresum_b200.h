@@ -175,7 +175,7 @@ int ssum_rk4_step_end(ssum_ctx* ctx, double dt, int64_t n, double* d_x0, double*
  * (best of `reps` launches). MEASURED_PEAKS.json has no fp64 entry. */
 int ssum_fp64_peak(ssum_ctx* ctx, int reps, double* tflops);
 /* Accuracy probe of the log the tree code's far pairs use (log kernel,
- * kernels.cuh log_far): out[i] = log(x[i]) for x[i] in [2^-20, 4]. Host arrays. */
+ * kernels.cuh log_tab): out[i] = log(x[i]) for x[i] in [2^-20, 4]. Host arrays. */
 int ssum_probe_log_far(ssum_ctx* ctx, const double* x, int64_t n, double* out);
 
 /* ---- fixtures (BASELINE.json configs; host-side generators) -------------- */

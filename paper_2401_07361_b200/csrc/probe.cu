@@ -30,8 +30,11 @@ __global__ void k_dfma_chain(double* out, int iters, double a, double b) {
 }
 
 __global__ void k_log_far(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double2 tab[kLogTabN];  // as the log tiles stage it
+  for (int j = threadIdx.x; j < kLogTabN; j += blockDim.x) tab[j] = kLogTab[j];
+  __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = log_far(x[i]);
+  if (i < n) out[i] = log_tab(x[i], tab);
 }
 
 }  // namespace
@@ -39,7 +42,7 @@ __global__ void k_log_far(const double* __restrict__ x, int64_t n, double* __res
 
 using namespace ssum;
 
-// Accuracy probe of the far-pair log (kernels.cuh log_far), host arrays.
+// Accuracy probe of the far-pair log (kernels.cuh log_tab), host arrays.
 extern "C" int ssum_probe_log_far(ssum_ctx* h, const double* x, int64_t n, double* out) {
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c || (n > 0 && (!x || !out)) || n < 0) return SSUM_INVALID;

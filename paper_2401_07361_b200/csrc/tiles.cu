@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   constexpr int kChunk = CHUNK;
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
   int2* rtab = reinterpret_cast<int2*>(smem + kStages * sizeof(double4) * (kChunk + kPad));
+  double2* ltab = reinterpret_cast<double2*>(rtab + kRangeCap);  // log kernel: kLogTab staged
   static_assert(sizeof(double) * NTH * D * kTpt <= kStages * sizeof(double4) * (kChunk + kPad), "red alias");
   static_assert(kPad <= NTH, "zero tail");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
@@ -161,6 +162,8 @@ __global__ void __launch_bounds__(NTH, MINB)
 #pragma unroll
     for (int st = 0; st < kStages; ++st) buf[st][kChunk + tid] = zero4;
   }
+  if constexpr (KER == kLOG)
+    for (int j = tid; j < kLogTabN; j += NTH) ltab[j] = kLogTab[j];
   if (tid == 0) {
 #pragma unroll
     for (int st = 0; st < kStages; ++st) {
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(NTH, MINB)
 #pragma unroll kNearUnroll
       for (; it < near_steps; ++it) {
         const int before = ncnt;
-        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt);
+        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt, ltab);
         hit |= static_cast<unsigned long long>(ncnt != before) << (it & 63);
       }
       // self pairs this lane walked in this chunk's near steps: the self
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     // of independent chains per step (zero-padded tail contributes 0)
     const double4* Bp = B + it * kStep;
 #pragma unroll kFU
-    for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a);
+    for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a, nullptr, ltab);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[c % kStages]);  // this warp is done with the stage
   }
@@ -413,7 +416,7 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
 
 template <int CHUNK>
 constexpr size_t tile_smem() {
-  return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap;
+  return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap + sizeof(double2) * kLogTabN;
 }
 
 // k_tiles instantiation with its dynamic shared-memory limit raised once
