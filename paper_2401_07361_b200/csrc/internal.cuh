@@ -146,12 +146,21 @@ struct Tile {
   int list_begin, list_end;  // into the range list
   int near_total;            // sources in the leading near-possible ranges
   int self_shift;  // self source of target i at flattened list position i + self_shift
-  int has_self;    // 0: no range holds the targets themselves
+  int has_self;    // bit 0: a range holds the targets themselves; bit 1 (kTileDense):
+                   // dense leaf — near-possible ranges evaluated with reference rounding
   int total;       // sources in the flattened list (sum of the ranges' counts)
 };
 // Arc-length margin below which a (target leaf, source node) pair may hold a
 // near pair: den = 2 sin^2(arc/2) < 2^-20 <=> arc < 1.3811e-3 rad.
 constexpr double kNearArc = 2.0e-3;
+// Leaf point spacing below which near pairs (den < 2^-20, arc < 1.38e-3)
+// are common enough that masking and repairing them costs more than
+// evaluating the near-possible ranges with reference rounding outright.
+constexpr int kTileDense = 2;
+#ifndef SSUM_DENSE_SPACING
+#define SSUM_DENSE_SPACING 1.5e-3
+#endif
+constexpr double kDenseSpacing = SSUM_DENSE_SPACING;
 // Source range in the unified point array. near != 0 marks a particle (PP)
 // range, which may hold near-singular or self pairs; pad is the number of
 // sources in the tile's list before this range (the flattened-list prefix).

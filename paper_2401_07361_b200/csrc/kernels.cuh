@@ -248,6 +248,36 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
   }
 }
 
+// Near-possible block of a dense leaf tile (Biot-Savart): every pair with
+// the reference's rounding (den = 1 - ((x.x y.x + x.y y.y) + x.z y.z),
+// separately rounded; singular guard on that value, kernels.hpp:19,27-29),
+// the self pair excluded by list position (treecode.cpp:388), and the
+// Sterbenz-exact r (y - x) accumulation (x cross (y - x) = x cross y) with a
+// ~1 ulp q / den — no mask, no repair. Source s of the block sits at
+// flattened position f0 + s G; selfpos[q] is target q's own position (-1:
+// none in the list).
+template <int NT, int NS>
+__device__ __forceinline__ void near_exact_block(const double4* x, const double4* __restrict__ B, int G,
+                                                 Acc<kBS>* a, int f0, const int* selfpos, int* flags) {
+  double4 y[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) y[s] = B[s * G];
+#pragma unroll
+  for (int c = 0; c < NT * NS; ++c) {
+    const double4& xx = x[c % NT];
+    const double4& yy = y[c / NT];
+    const double den = __dsub_rn(1.0, __dadd_rn(__dadd_rn(__dmul_rn(xx.x, yy.x), __dmul_rn(xx.y, yy.y)),
+                                                __dmul_rn(xx.z, yy.z)));
+    const bool self = f0 + (c / NT) * G == selfpos[c % NT];
+    const bool sing = den <= kSingularTol;
+    if (sing && !self) atomicOr(flags, kFlagSingular);
+    const double r = (self || sing) ? 0.0 : q_over(yy.w, den);
+    a[c % NT].s[0] = fma(r, __dsub_rn(yy.x, xx.x), a[c % NT].s[0]);
+    a[c % NT].s[1] = fma(r, __dsub_rn(yy.y, xx.y), a[c % NT].s[1]);
+    a[c % NT].s[2] = fma(r, __dsub_rn(yy.z, xx.z), a[c % NT].s[2]);
+  }
+}
+
 // Second walk over one far_block<..., true> block whose warp saw a near pair
 // other than its self pairs: adds the reference-rounded contribution of each
 // near pair of distinct points (pair_slow, which also raises the singular

@@ -281,7 +281,18 @@ __global__ void __launch_bounds__(NTH, MINB)
     near_steps = 0;
 #endif
     int it = 0;
-    if (near_steps > 0) {
+    if constexpr (KER == kBS && MODE == kLeafMode) {
+      if (near_steps > 0 && (T.has_self & kTileDense)) {
+        // dense leaf: the near-possible steps with reference rounding
+        int selfpos[kTpt];
+#pragma unroll
+        for (int q = 0; q < kTpt; ++q) selfpos[q] = (T.has_self & 1) ? ti[q] + T.self_shift : -1;
+        const int f0 = c * kChunk + g;
+#pragma unroll 1
+        for (; it < near_steps; ++it) near_exact_block<kTpt, kNs>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos, flags);
+      }
+    }
+    if (it < near_steps) {
       // bit `it` of hit: step `it` met a masked pair (self or near); steps
       // past 64 are all re-walked when a repair is needed
       int ncnt = 0;
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(NTH, MINB)
 #pragma unroll
       for (int q = 0; q < kTpt; ++q) {
         const int o = ti[q] + T.self_shift - c * kChunk;
-        nself += (T.has_self && o >= 0 && o < o_end && o % G == g) ? 1 : 0;
+        nself += ((T.has_self & 1) && o >= 0 && o < o_end && o % G == g) ? 1 : 0;
       }
       if (__any_sync(0xffffffffu, ncnt != nself)) {
         // only the steps that met a masked pair (dense inputs: a handful of

@@ -509,7 +509,11 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       t.list_end = w0 + w;
       t.near_total = near_total;
       t.self_shift = self_shift;
-      t.has_self = has_self;
+      // dense leaf: estimated point spacing sqrt(area / count), area ~ 1.3 r^2
+      // of the leaf triangle in its circumcircle of angular radius r
+      const double rl = radius[leaf];
+      const bool dense = near_total > 0 && 1.3 * rl * rl < kDenseSpacing * kDenseSpacing * double(c);
+      t.has_self = has_self | (dense ? kTileDense : 0);
       t.total = cur.src;
       tiles[tile_off[k] + j] = t;
       const unsigned long long tc = static_cast<unsigned long long>(t.tgt_count);
