@@ -77,6 +77,9 @@ typedef struct {
   int64_t gpu_launches;           /* kernels launched by the last call            */
   double pp_pc_ms, cp_cc_fit_ms, upward_ms, finish_ms; /* device time per pass     */
   uint64_t up_visits, down_visits; /* (particle, weight node) / (particle, fit node) pairs */
+  double tiles_ms;                /* CP/CC+fit and PP+PC tiles together (they run
+                                     concurrently on two streams: pp_pc_ms and
+                                     cp_cc_fit_ms are each kernel's own span)   */
 } ssum_stats;
 
 /* ---- context ------------------------------------------------------------ */

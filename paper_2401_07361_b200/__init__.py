@@ -95,7 +95,8 @@ class _Stats(ctypes.Structure):
                 ("fit_nodes", ctypes.c_int64), ("gpu_launches", ctypes.c_int64),
                 ("pp_pc_ms", ctypes.c_double), ("cp_cc_fit_ms", ctypes.c_double),
                 ("upward_ms", ctypes.c_double), ("finish_ms", ctypes.c_double),
-                ("up_visits", ctypes.c_uint64), ("down_visits", ctypes.c_uint64)]
+                ("up_visits", ctypes.c_uint64), ("down_visits", ctypes.c_uint64),
+                ("tiles_ms", ctypes.c_double)]
 
 
 _LIB = None
@@ -253,6 +254,7 @@ class TreecodeStats:
     finish_ms: float = 0.0
     up_visits: int = 0      # (particle, weight node) pairs of the upward pass
     down_visits: int = 0    # (particle, fit node) pairs of the downward pass
+    tiles_ms: float = 0.0   # CP/CC+fit and PP+PC tiles together (concurrent streams)
 
     def _to_c(self) -> _Stats:
         s = _Stats()

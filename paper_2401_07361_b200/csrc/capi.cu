@@ -275,6 +275,11 @@ int ssum_create(int device, ssum_ctx** out) {
     c->stream = c->own_stream;
     for (auto& e : c->ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
     SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    for (auto& e : c->side_ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
+    if (const char* v = std::getenv("SSUM_OVERLAP_TILES")) c->overlap_tiles = std::atoi(v) != 0;
     for (auto& e : c->io.xyz) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->io.out) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->io.q, cudaEventDisableTiming));
@@ -307,6 +312,10 @@ void ssum_destroy(ssum_ctx* h) {
   if (c->io.t0) cudaEventDestroy(c->io.t0);
   if (c->io.t1) cudaEventDestroy(c->io.t1);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  for (auto& e : c->side_ev) if (e) cudaEventDestroy(e);
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);

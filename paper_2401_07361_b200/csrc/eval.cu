@@ -561,21 +561,34 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   trace().mark("eval.upward_host");
   cudaEventRecord(c.ev[2], c.stream);
 
-  // ---- CP/CC + fit
+  // ---- CP/CC + fit (c.stream) and PP + PC (this part's contiguous tile
+  // range; side_stream). The two only read pts and write disjoint buffers
+  // (coeff / S), so with overlap_tiles the leaf blocks start as soon as the
+  // fit kernel has no blocks left to dispatch and fill its tail.
   const int nfit = L.fit_sel_all ? L.n_fit_tiles : L.n_fit_sel;
+  const int ntl = L.leaf_t1 - L.leaf_t0;
+  const bool fork = c.overlap_tiles && nfit > 0 && ntl > 0;
+  cudaStream_t leaf_stream = fork ? c.side_stream : c.stream;
+  if (fork) {
+    SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
+  }
   if (nfit > 0) {
     launch_fit_tiles(c, kernel, P, nfit, L.fit_sel_all ? nullptr : L.fit_sel.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
   cudaEventRecord(c.ev[3], c.stream);
-
-  // ---- PP + PC (this part's contiguous tile range)
-  const int ntl = L.leaf_t1 - L.leaf_t0;
+  cudaEventRecord(c.side_ev[0], leaf_stream);
   if (ntl > 0) {
-    launch_leaf_tiles(c, kernel, L.leaf_tiles.p + L.leaf_t0, ntl, L.leaf_ranges.p, c.S.p);
+    launch_leaf_tiles(c, leaf_stream, kernel, L.leaf_tiles.p + L.leaf_t0, ntl, L.leaf_ranges.p, c.S.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
+  }
+  cudaEventRecord(c.side_ev[1], leaf_stream);
+  if (fork) {
+    SSUM_CUDA_CHECK(cudaEventRecord(c.join_ev, c.side_stream));
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
   }
   cudaEventRecord(c.ev[4], c.stream);
 
@@ -631,7 +644,10 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ms[k], c.ev[k], c.ev[k + 1]);
     st->upward_ms = ms[0] + ms[1];
     st->cp_cc_fit_ms = ms[2];
-    st->pp_pc_ms = ms[3];
+    float leaf_ms = 0.f;
+    cudaEventElapsedTime(&leaf_ms, c.side_ev[0], c.side_ev[1]);
+    st->pp_pc_ms = leaf_ms;
+    st->tiles_ms = ms[2] + ms[3];
     st->finish_ms = ms[4];
   }
 }

@@ -270,6 +270,12 @@ struct Ctx {
   DBuf<SrcRange> direct_range;
   DBuf<double> rk_state;             // RK4 scratch
   cudaEvent_t ev[8];
+  // Leaf tiles (PP+PC) run on side_stream concurrently with the fit tiles
+  // (CP/CC+fit): both only read pts and write disjoint buffers, and the leaf
+  // blocks fill the SMs the fit kernel's tail leaves idle (eval.cu).
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, side_ev[2] = {};
+  bool overlap_tiles = true;
   // Host-pointer entry (ssum_treecode_sum): the inputs travel on copy_stream
   // in kIoChunks pieces (the tree walk starts on each piece as it lands, q is
   // waited for only at the gather) and the result leaves in pieces as the
@@ -319,7 +325,7 @@ void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
 void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel);
-void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
+void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct = false);
 void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out);
 void rk4_combine(Ctx& c, int stage, int64_t n, double dt, double omega, double* d_x0, double* d_z0,

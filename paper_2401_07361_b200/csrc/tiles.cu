@@ -454,13 +454,13 @@ void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
                                                  c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
 }
 
-void launch_leaf_tiles(Ctx& c, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
+void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct) {
   auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>()
                                    : tiles_kernel<kLOG, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>())
                   : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>()
                                    : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>());
-  k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), c.stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
+  k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
                                                 nullptr, nullptr, 0, nullptr);
 }
 
@@ -473,7 +473,7 @@ void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out) {
   const int bs = 256;
   k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
   SSUM_LAUNCH_CHECK();
-  launch_leaf_tiles(c, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p, true);
+  launch_leaf_tiles(c, c.stream, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p, true);
   SSUM_LAUNCH_CHECK();
   if (kernel == kBS)
     k_direct_finish<kBS><<<grid_for(n, bs), bs, 0, c.stream>>>(n, c.pts.p, c.S.p, d_out);
