@@ -95,7 +95,16 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
     ~Unrestrict() { c.restrict_on = false; }
   } unrestrict{c};
   plan_restriction(c);
+  struct Early {  // build_lists starts the upward pass early (start_prep)
+    Ctx& c;
+    ~Early() {
+      c.early = Ctx::Early{};
+      c.prep_started = false;
+    }
+  } early{c};
+  c.early = Ctx::Early{d_xyz, d_q, cfg.degree, kernel == SSUM_BIOT_SAVART ? 3 : 1};
   traverse_and_build_lists(c, cfg, false);
+  c.early = Ctx::Early{};
   tr.mark("lists.done");
   const auto t2 = clk::now();
   evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
@@ -275,11 +284,16 @@ int ssum_create(int device, ssum_ctx** out) {
     c->stream = c->own_stream;
     for (auto& e : c->ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
     SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    SSUM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SSUM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_hi));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->side_ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
+    for (auto& e : c->leaf_ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
+    SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->prep_ev, cudaEventDisableTiming));
     if (const char* v = std::getenv("SSUM_OVERLAP_TILES")) c->overlap_tiles = std::atoi(v) != 0;
+    if (const char* v = std::getenv("SSUM_EARLY_PREP")) c->early_prep = std::atoi(v) != 0;
     for (auto& e : c->io.xyz) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->io.out) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->io.q, cudaEventDisableTiming));
@@ -316,6 +330,8 @@ void ssum_destroy(ssum_ctx* h) {
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   for (auto& e : c->side_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : c->leaf_ev) if (e) cudaEventDestroy(e);
+  if (c->prep_ev) cudaEventDestroy(c->prep_ev);
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);

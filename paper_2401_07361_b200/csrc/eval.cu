@@ -392,11 +392,11 @@ void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, 
 }
 
 // nchunks: host upper bound (grid size); d_nchunks: the device-side count.
-void launch_up_partial(Ctx& c, int degree, int nchunks, const int* d_nchunks) {
+void launch_up_partial(Ctx& c, cudaStream_t stream, int degree, int nchunks, const int* d_nchunks) {
   const unsigned grid = static_cast<unsigned>((nchunks + kUpWarps - 1) / kUpWarps);
 #define SSUM_UP_CASE(DG)                                                                                  \
   case DG:                                                                                                \
-    k_up_partial<DG><<<grid, 32 * kUpWarps, 0, c.stream>>>(c.wchunks.p, d_nchunks, c.pts.p, c.nodes.cramer.p, \
+    k_up_partial<DG><<<grid, 32 * kUpWarps, 0, stream>>>(c.wchunks.p, d_nchunks, c.pts.p, c.nodes.cramer.p,   \
                                                            c.wpart.p);                                    \
     break;
   switch (degree) {
@@ -497,34 +497,25 @@ void ensure_vinv(Ctx& c, int degree) {
   c.vinv_degree = degree;
 }
 
-void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q, int64_t n,
-              double* d_out, ssum_stats* st) {
+// Particle gather, proxy points and the upward pass (Phases 1-2), on stream
+// s: everything the tile kernels read from pts. tmp: cub scratch private to s.
+void launch_prep(Ctx& c, cudaStream_t s, DBuf<unsigned char>& tmp, int degree, const double* d_xyz,
+                 const double* d_q, int64_t n) {
   Lists& L = c.lists;
   Binned& B = c.bins;
-  const int degree = cfg.degree;
   const int P = (degree + 1) * (degree + 2) / 2;
-  const int D = kernel == kBS ? 3 : 1;
-  if (n == 0) return;
-  ensure_vinv(c, degree);
-  const int64_t npts = n + int64_t(L.n_proxy) * P;
-  if (npts > 0x7fffffff) throw Error(SSUM_INVALID, "point count exceeds int32 indexing");
-  c.pts.ensure(size_t(npts));
-  c.S.ensure(size_t(n) * D);
-  c.coeff.ensure(std::max<size_t>(size_t(L.n_proxy) * D * P, 1));
   const int bs = 256;
-
-  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.q, 0));  // q of a host-pointer call
-  cudaEventRecord(c.ev[0], c.stream);
-  k_gather<<<grid_for(n, bs), bs, 0, c.stream>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
+  cudaEventRecord(c.ev[0], s);
+  k_gather<<<grid_for(n, bs), bs, 0, s>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   if (L.n_proxy > 0) {
-    k_proxy<<<grid_for(int64_t(L.n_proxy) * P, bs), bs, 0, c.stream>>>(c.trav.slot_node.p, L.n_proxy, degree,
-                                                                         c.nodes.tri.p, n, c.pts.p);
+    k_proxy<<<grid_for(int64_t(L.n_proxy) * P, bs), bs, 0, s>>>(c.trav.slot_node.p, L.n_proxy, degree,
+                                                                  c.nodes.tri.p, n, c.pts.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
-  cudaEventRecord(c.ev[1], c.stream);
+  cudaEventRecord(c.ev[1], s);
 
   // ---- upward pass: chunk table (weight node bins cut into <= 1024-particle
   // chunks) built on the device
@@ -532,12 +523,12 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     const int nw = L.n_weight;
     c.wcount.ensure(size_t(nw) + 1);
     c.wcount_off.ensure(size_t(nw) + 1);
-    k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, c.stream>>>(L.weight_nodes.p, nw, B.cnt.p, c.wcount.p);
+    k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.cnt.p, c.wcount.p);
     SSUM_LAUNCH_CHECK();
     size_t tb = 0;
-    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
-    c.cub_tmp.ensure(tb);
-    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(c.cub_tmp.p, tb, c.wcount.p, c.wcount_off.p, nw + 1, c.stream));
+    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, s));
+    tmp.ensure(tb);
+    SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, c.wcount.p, c.wcount_off.p, nw + 1, s));
     // chunk count without a read-back: a particle lies in at most one node
     // per level, so sum_w ceil(cnt_w / kUpChunk) <= nw + N (levels) / kUpChunk
     const int64_t nch_bound =
@@ -546,46 +537,97 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     c.wchunks.ensure(size_t(nch) + size_t(nw));
     c.wpart.ensure(size_t(nch) * P);
     int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
-    k_up_fill<<<grid_for(nw, 256), 256, 0, c.stream>>>(L.weight_nodes.p, nw, B.off.p, B.cnt.p, c.wcount_off.p,
-                                                       c.wchunks.p, d_crange);
+    k_up_fill<<<grid_for(nw, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.off.p, B.cnt.p, c.wcount_off.p,
+                                                 c.wchunks.p, d_crange);
     SSUM_LAUNCH_CHECK();
     c.launches += 4;
-    if (nch > 0) launch_up_partial(c, degree, nch, c.wcount_off.p + nw);
+    if (nch > 0) launch_up_partial(c, s, degree, nch, c.wcount_off.p + nw);
     const int bt = ((P + 31) / 32) * 32;
-    k_up_final<<<L.n_weight, bt, size_t(P) * 8, c.stream>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
-                                                             P, L.pslot.p, n, c.pts.p);
+    k_up_final<<<L.n_weight, bt, size_t(P) * 8, s>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
+                                                      P, L.pslot.p, n, c.pts.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
-    // (pageable H2D copies have consumed the host vectors when they return)
+  }
+  cudaEventRecord(c.ev[2], s);
+}
+
+void size_eval_buffers(Ctx& c, int degree, int D, int64_t n) {
+  const int P = (degree + 1) * (degree + 2) / 2;
+  ensure_vinv(c, degree);
+  const int64_t npts = n + int64_t(c.lists.n_proxy) * P;
+  if (npts > 0x7fffffff) throw Error(SSUM_INVALID, "point count exceeds int32 indexing");
+  c.pts.ensure(size_t(npts));
+  c.S.ensure(size_t(n) * D);
+  c.coeff.ensure(std::max<size_t>(size_t(c.lists.n_proxy) * D * P, 1));
+}
+
+// Called by build_lists as soon as the proxy slots and weight nodes exist:
+// the gather, proxy points and upward pass need nothing else from the lists,
+// so they run on side_stream while the main stream builds the range lists
+// and tiles (k_leaf_fill / k_fit_fill are latency-bound; the upward pass is
+// FP64 work). evaluate() joins on prep_ev.
+void start_prep(Ctx& c) {
+  if (!c.early.xyz || !c.early_prep || c.bins.n == 0) return;
+  const int64_t n = c.bins.n;
+  size_eval_buffers(c, c.early.degree, c.early.dim, n);
+  SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
+  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.io.q, 0));  // q of a host-pointer call
+  launch_prep(c, c.side_stream, c.cub_tmp_side, c.early.degree, c.early.xyz, c.early.q, n);
+  SSUM_CUDA_CHECK(cudaEventRecord(c.prep_ev, c.side_stream));
+  c.prep_started = true;
+}
+
+void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q, int64_t n,
+              double* d_out, ssum_stats* st) {
+  Lists& L = c.lists;
+  Binned& B = c.bins;
+  const int degree = cfg.degree;
+  const int P = (degree + 1) * (degree + 2) / 2;
+  const int D = kernel == kBS ? 3 : 1;
+  if (n == 0) return;
+  if (!c.prep_started) size_eval_buffers(c, degree, D, n);
+  const int bs = 256;
+
+  if (c.prep_started) {
+    // gather + proxy points + upward pass already running on side_stream
+    // (start_prep, launched from build_lists once the slots were known)
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.prep_ev, 0));
+    c.prep_started = false;
+  } else {
+    if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.q, 0));  // q of a host-pointer call
+    launch_prep(c, c.stream, c.cub_tmp, degree, d_xyz, d_q, n);
   }
   trace().mark("eval.upward_host");
-  cudaEventRecord(c.ev[2], c.stream);
 
-  // ---- CP/CC + fit (c.stream) and PP + PC (this part's contiguous tile
-  // range; side_stream). The two only read pts and write disjoint buffers
-  // (coeff / S), so with overlap_tiles the leaf blocks start as soon as the
-  // fit kernel has no blocks left to dispatch and fill its tail.
+  // ---- CP/CC + fit (side_stream, high priority) and PP + PC (this part's
+  // contiguous tile range; c.stream). The two only read pts and write
+  // disjoint buffers (coeff / S): the fit blocks (the larger tiles) are
+  // dispatched first and the leaf blocks fill the SMs as the fit kernel's
+  // tail drains.
   const int nfit = L.fit_sel_all ? L.n_fit_tiles : L.n_fit_sel;
   const int ntl = L.leaf_t1 - L.leaf_t0;
   const bool fork = c.overlap_tiles && nfit > 0 && ntl > 0;
-  cudaStream_t leaf_stream = fork ? c.side_stream : c.stream;
+  cudaStream_t fit_stream = fork ? c.side_stream : c.stream;
+  cudaEventRecord(c.ev[3], c.stream);
   if (fork) {
     SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
     SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
   }
+  cudaEventRecord(c.side_ev[0], fit_stream);
   if (nfit > 0) {
-    launch_fit_tiles(c, kernel, P, nfit, L.fit_sel_all ? nullptr : L.fit_sel.p);
+    launch_fit_tiles(c, fit_stream, kernel, P, nfit, L.fit_sel_all ? nullptr : L.fit_sel.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
-  cudaEventRecord(c.ev[3], c.stream);
-  cudaEventRecord(c.side_ev[0], leaf_stream);
+  cudaEventRecord(c.side_ev[1], fit_stream);
+  cudaEventRecord(c.leaf_ev[0], c.stream);
   if (ntl > 0) {
-    launch_leaf_tiles(c, leaf_stream, kernel, L.leaf_tiles.p + L.leaf_t0, ntl, L.leaf_ranges.p, c.S.p);
+    launch_leaf_tiles(c, c.stream, kernel, L.leaf_tiles.p + L.leaf_t0, ntl, L.leaf_ranges.p, c.S.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
-  cudaEventRecord(c.side_ev[1], leaf_stream);
+  cudaEventRecord(c.leaf_ev[1], c.stream);
   if (fork) {
     SSUM_CUDA_CHECK(cudaEventRecord(c.join_ev, c.side_stream));
     SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
@@ -640,15 +682,18 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   cudaEventRecord(c.ev[5], c.stream);
   check_flags(c, "treecode_sum");
   if (st) {
-    float ms[5];
-    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&ms[k], c.ev[k], c.ev[k + 1]);
-    st->upward_ms = ms[0] + ms[1];
-    st->cp_cc_fit_ms = ms[2];
-    float leaf_ms = 0.f;
-    cudaEventElapsedTime(&leaf_ms, c.side_ev[0], c.side_ev[1]);
-    st->pp_pc_ms = leaf_ms;
-    st->tiles_ms = ms[2] + ms[3];
-    st->finish_ms = ms[4];
+    // upward: ev[0..2] (on side_stream when it started early); each tile
+    // kernel's own span on its stream; tiles: both together
+    auto span = [](cudaEvent_t e0, cudaEvent_t e1) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      return static_cast<double>(ms);
+    };
+    st->upward_ms = span(c.ev[0], c.ev[2]);
+    st->cp_cc_fit_ms = span(c.side_ev[0], c.side_ev[1]);
+    st->pp_pc_ms = span(c.leaf_ev[0], c.leaf_ev[1]);
+    st->tiles_ms = span(c.ev[3], c.ev[4]);
+    st->finish_ms = span(c.ev[4], c.ev[5]);
   }
 }
 

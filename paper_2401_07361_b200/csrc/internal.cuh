@@ -270,12 +270,25 @@ struct Ctx {
   DBuf<SrcRange> direct_range;
   DBuf<double> rk_state;             // RK4 scratch
   cudaEvent_t ev[8];
-  // Leaf tiles (PP+PC) run on side_stream concurrently with the fit tiles
-  // (CP/CC+fit): both only read pts and write disjoint buffers, and the leaf
-  // blocks fill the SMs the fit kernel's tail leaves idle (eval.cu).
+  // The fit tiles (CP/CC+fit) run on side_stream (highest priority)
+  // concurrently with the leaf tiles (PP+PC): both only read pts and write
+  // disjoint buffers, and the leaf blocks fill the SMs the fit kernel's
+  // tail leaves idle (eval.cu).
   cudaStream_t side_stream = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, side_ev[2] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, side_ev[2] = {}, leaf_ev[2] = {};
   bool overlap_tiles = true;
+  // The gather + proxy points + upward pass start on side_stream from
+  // build_lists (start_prep) when the treecode entry set `early` (the inputs
+  // of the evaluation that follows); evaluate() waits on prep_ev.
+  struct Early {
+    const double* xyz = nullptr;
+    const double* q = nullptr;
+    int degree = 0, dim = 0;
+  } early;
+  bool prep_started = false;
+  bool early_prep = true;
+  cudaEvent_t prep_ev = nullptr;
+  DBuf<unsigned char> cub_tmp_side;
   // Host-pointer entry (ssum_treecode_sum): the inputs travel on copy_stream
   // in kIoChunks pieces (the tree walk starts on each piece as it lands, q is
   // waited for only at the gather) and the result leaves in pieces as the
@@ -324,7 +337,8 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
-void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel);
+void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel);
+void start_prep(Ctx& c);
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct = false);
 void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out);

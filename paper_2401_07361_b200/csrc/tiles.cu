@@ -446,11 +446,11 @@ auto tiles_kernel() {
 
 }  // namespace
 
-void launch_fit_tiles(Ctx& c, int kernel, int P, int nfit, const int* sel) {
+void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel) {
   Lists& L = c.lists;
   auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>()
                           : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>();
-  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), c.stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
+  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
                                                  c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
 }
 

@@ -855,6 +855,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     L.n_weight = tail[2];
     L.n_fit = tail[3];
   }
+  start_prep(c);  // gather + proxies + upward on side_stream, overlapping the rest
 
   trace().mark("lists.group_slots");
   // ---- range and tile counts for leaves and fit nodes, one read-back
