@@ -13,9 +13,9 @@ steps except the persistent tree geometry (FaceTree semantics).
   e2e   : the same through the C-ABI host-pointer entry point
           (ssum_treecode_sum) from pinned host buffers: H2D of xyz+q and D2H
           of the velocities inside every timed step.
-  roofline : the dominant kernels — the interaction tiles, k_tiles<leaf>
-          (PP + PC pairs, side stream) running concurrently with
-          k_tiles<fit> (CP + CC pairs + fit) — algorithmic flops (13 per
+  roofline : the dominant kernels — the interaction tiles, k_tiles<fit>
+          (CP + CC pairs + fit, high-priority side stream) running
+          concurrently with k_tiles<leaf> (PP + PC pairs) — algorithmic flops (13 per
           pair; the fit epilogue's flops not counted) / the
           event-timed span of the two together,
           against the DFMA peak measured live on this GPU (no fp64 entry in
@@ -399,12 +399,12 @@ def run_gpu(args):
         "config": {"workload": WORKLOAD, **CFG, "n": n, "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"target-leaf partition x{ws}" if ws > 1 else "single GPU"},
         "roofline": {"bound": "fp64",
-                     "kernel": "k_tiles<leaf> (PP+PC, side stream) + k_tiles<fit> (CP+CC+fit), concurrent", "achieved": achieved, "peak": peak,
+                     "kernel": "k_tiles<fit> (CP+CC+fit, high-priority side stream) + k_tiles<leaf> (PP+PC), concurrent", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "DFMA-chain probe on this GPU (ssum_fp64_peak); MEASURED_PEAKS.json has no fp64",
                      "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": pairs, "avg_launch_ms": avg_pp_ms,
-                     "timing": "CUDA events: fork on the main stream before k_tiles<fit> to the join after "
-                               "k_tiles<leaf> on the side stream"},
+                     "timing": "CUDA events on the main stream: before the fork to k_tiles<fit> (side stream) "
+                               "to after the join behind k_tiles<leaf>"},
         "e2e": {"value": n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(xyz.nbytes + q.nbytes),
                 "d2h_bytes_per_step": int(n * DIM * 8), "ms_per_step": e2e_s * 1e3,
                 "path": ("ssum_treecode_sum (host pointers)" if ws == 1 else
