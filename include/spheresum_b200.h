@@ -80,6 +80,10 @@ typedef struct {
   double tiles_ms;                /* CP/CC+fit and PP+PC tiles together (they run
                                      concurrently on two streams: pp_pc_ms and
                                      cp_cc_fit_ms are each kernel's own span)   */
+  int64_t mac_host_decisions;     /* node pairs whose MAC quotient fell inside the
+                                     guard band around theta and were decided
+                                     with the reference's host arithmetic
+                                     (context total)          */
 } ssum_stats;
 
 /* ---- context ------------------------------------------------------------ */
@@ -87,7 +91,9 @@ int ssum_create(int device, ssum_ctx** out);
 void ssum_destroy(ssum_ctx* ctx);
 const char* ssum_last_error(const ssum_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the
- * context's own stream. */
+ * context's own (non-blocking) stream. The legacy default stream has handle 0,
+ * which reads as NULL here: pass cudaStreamLegacy ((void*)1) for it, so the
+ * library's work stays ordered with work the caller queues there. */
 int ssum_set_stream(ssum_ctx* ctx, void* cuda_stream);
 /* Drop the persistent tree geometry (a freshly constructed FaceTree,
  * face_tree.cpp:9-16). */
@@ -137,6 +143,27 @@ int ssum_dual_traversal(ssum_ctx* ctx, const ssum_config* cfg, int* tsk, int64_t
 int ssum_eval_interaction(ssum_ctx* ctx, int kernel, const ssum_config* cfg, const double* xyz,
                           const double* q, int64_t n, int target, int source, int kind,
                           double* field);
+
+/* compute_proxy_weights (treecode.hpp:47-51, treecode.cpp:79-91): the raw
+ * proxy weights w_k = sum_{j in bin(source_node)} B_k(beta(x_j)) q_j of one
+ * node (reference id) of the tree as last binned from these positions;
+ * w: (degree+1)(degree+2)/2 doubles, in SBBBasis index order. */
+int ssum_compute_proxy_weights(ssum_ctx* ctx, int degree, const double* xyz, const double* q, int64_t n,
+                               int source_node, double* w);
+/* Reciprocal condition number carried by the context's last SSUM_CONDITIONING
+ * failure (ConditioningError::rcond, errors.hpp:22-27). */
+double ssum_last_rcond(const ssum_ctx* ctx);
+
+/* ---- SBB interpolation (sbb.hpp; host) ------------------------------------ */
+/* lattice_fit(degree) (sbb.hpp:74-78, sbb.cpp:124-138): V^-1 of the lattice
+ * Vandermonde V[m][k] = B_k(b_m) (row-major P x P, may be NULL) and its
+ * reciprocal condition number (exact 1-norm). Returns SSUM_CONDITIONING when
+ * rcond <= 1e-12 (sbb.cpp:89-93), SSUM_INVALID for a degree outside [1, 20]. */
+int ssum_lattice_fit(int degree, double* vinv, double* rcond);
+/* proxy_points(t, degree).points (sbb.hpp:48, sbb.cpp:46-66): tri = v1, v2,
+ * v3 (9 doubles); pts receives P x 3 doubles in SBBBasis index order, with the
+ * reference's rounding (the tree code's device proxies are bit-identical). */
+int ssum_proxy_points(const double* tri, int degree, double* pts);
 
 /* ---- multi-GPU target partition (no reference equivalent) */
 /* Subsequent treecode evaluations compute only part `part` of `nparts`

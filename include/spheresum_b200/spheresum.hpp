@@ -7,6 +7,11 @@
 // reference recompiles against this header and links libspheresum_dropin.so
 // (+ libspheresum_b200.so) instead of the reference library.
 //
+// Covered: errors.hpp, geometry.hpp, kernels.hpp (pointwise kernels),
+// sbb.hpp, face_tree.hpp, treecode.hpp, plus the RK4 driver and the
+// mesh fixture. Not covered (outside the velocity path): icosa_mesh.hpp's
+// IcosaMesh class, test_cases.hpp, parallel.hpp, forcing.
+//
 // Differences a caller can observe:
 //  * FaceTree is device-resident; node(id) / leaf_of_particle() return a host
 //    snapshot refreshed lazily after each binning (ids are the reference's).
@@ -46,10 +51,32 @@ class ConfigError : public std::runtime_error {
   explicit ConfigError(const std::string& w) : std::runtime_error(w) {}
 };
 
-// ---- geometry.hpp (the types the path's signatures use) --------------------
+// ---- geometry.hpp -------------------------------------------------------------
 struct Vec3 {
   double x = 0.0, y = 0.0, z = 0.0;
+  Vec3& operator+=(const Vec3& o) {
+    x += o.x, y += o.y, z += o.z;
+    return *this;
+  }
+  Vec3& operator-=(const Vec3& o) {
+    x -= o.x, y -= o.y, z -= o.z;
+    return *this;
+  }
+  Vec3& operator*=(double s) {
+    x *= s, y *= s, z *= s;
+    return *this;
+  }
 };
+inline Vec3 operator+(Vec3 a, const Vec3& b) { return a += b; }
+inline Vec3 operator-(Vec3 a, const Vec3& b) { return a -= b; }
+inline Vec3 operator*(Vec3 a, double s) { return a *= s; }
+inline Vec3 operator*(double s, Vec3 a) { return a *= s; }
+inline Vec3 operator-(const Vec3& a) { return {-a.x, -a.y, -a.z}; }
+inline double dot(const Vec3& a, const Vec3& b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline Vec3 cross(const Vec3& a, const Vec3& b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+inline double norm(const Vec3& a) { return std::sqrt(dot(a, a)); }
 
 // Point on the unit sphere; constructors renormalise (geometry.hpp:50-66).
 struct UnitVector3 {
@@ -65,21 +92,121 @@ inline double dot(const UnitVector3& a, const UnitVector3& b) { return a.x * b.x
 inline Vec3 cross(const UnitVector3& a, const UnitVector3& b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
+inline Vec3 operator-(const UnitVector3& a, const UnitVector3& b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 
+struct LatLon {
+  double lat = 0.0;
+  double lon = 0.0;
+};
+struct BarycentricCoords {
+  double b1 = 0.0, b2 = 0.0, b3 = 0.0;
+};
+inline constexpr double kContainTol = -1e-10;
+
+// Counterclockwise spherical triangle; the 3-vertex constructor validates
+// like the reference's (GeometryError, geometry.cpp:27-39).
 struct SphericalTriangle {
   UnitVector3 v1, v2, v3;
+  SphericalTriangle() = default;
+  SphericalTriangle(const UnitVector3& a, const UnitVector3& b, const UnitVector3& c);
 };
 
-// ---- kernels.hpp: kernel descriptors --------------------------------------
+UnitVector3 latlon_to_unit(const LatLon& p);
+LatLon unit_to_latlon(const UnitVector3& v);
+double great_circle_distance(const UnitVector3& a, const UnitVector3& b);
+BarycentricCoords spherical_barycentric(const SphericalTriangle& t, const UnitVector3& p);
+UnitVector3 triangle_circumcenter(const SphericalTriangle& t);
+double triangle_radius(const SphericalTriangle& t);
+bool triangle_contains(const SphericalTriangle& t, const UnitVector3& p);
+double spherical_polygon_area(const std::vector<UnitVector3>& vs);
+double spherical_triangle_area(const SphericalTriangle& t);
+double barycentric_min_score(const UnitVector3& a, const UnitVector3& b, const UnitVector3& c, const UnitVector3& p);
+
+// ---- kernels.hpp ------------------------------------------------------------
+// Pointwise kernels for callers (kernels.hpp:13-61); the sums themselves run
+// on the device.
 inline constexpr double kSingularTol = 1e-14;
+inline double greens_log(const UnitVector3& x, const UnitVector3& y) {
+  const double den = 1.0 - dot(x, y);
+  if (den <= kSingularTol) throw SingularKernelError("log kernel evaluated at its singularity");
+  return -std::log(den) / (4.0 * M_PI);
+}
+inline Vec3 bve_velocity_kernel(const UnitVector3& x, const UnitVector3& y) {
+  const double den = 1.0 - dot(x, y);
+  if (den <= kSingularTol) throw SingularKernelError("velocity kernel evaluated at its singularity");
+  return cross(x, y) * (1.0 / den);
+}
 struct LogPotentialKernel {
   static constexpr int dim = 1;
   static double prefactor() { return 1.0; }
+  static void eval(const UnitVector3& x, const UnitVector3& y, double* out) { out[0] = greens_log(x, y); }
 };
 struct BiotSavartKernel {
   static constexpr int dim = 3;
   static double prefactor() { return -1.0 / (4.0 * M_PI); }
+  static void eval(const UnitVector3& x, const UnitVector3& y, double* out) {
+    const Vec3 v = bve_velocity_kernel(x, y);
+    out[0] = v.x, out[1] = v.y, out[2] = v.z;
+  }
 };
+
+// ---- sbb.hpp ------------------------------------------------------------------
+inline constexpr int kMaxSbbDegree = 20;
+inline constexpr int sbb_basis_size(int degree) { return (degree + 1) * (degree + 2) / 2; }
+
+class SBBBasis {
+ public:
+  explicit SBBBasis(int degree);
+  int degree() const { return degree_; }
+  int size() const { return static_cast<int>(index_set_.size()); }
+  const std::vector<std::array<int, 3>>& index_set() const { return index_set_; }
+  void eval(const BarycentricCoords& b, double* out) const;
+  std::vector<double> eval(const BarycentricCoords& b) const;
+
+ private:
+  int degree_;
+  std::vector<std::array<int, 3>> index_set_;
+};
+
+struct ProxyPointSet {
+  SphericalTriangle triangle;
+  int degree;
+  std::vector<UnitVector3> points;
+  std::vector<BarycentricCoords> barycentric;
+};
+ProxyPointSet proxy_points(const SphericalTriangle& t, int degree);
+ProxyPointSet proxy_points_from_barycentric(const SphericalTriangle& t, int degree,
+                                            std::vector<BarycentricCoords> bary);
+
+// LU of V[m][k] = B_k(b_m) with partial pivoting; ConditioningError (rcond)
+// when the reciprocal condition number is not > 1e-12 (sbb.cpp:74-122).
+class ProxyFit {
+ public:
+  ProxyFit(const SBBBasis& basis, const std::vector<BarycentricCoords>& bary);
+  ~ProxyFit();
+  ProxyFit(ProxyFit&&) noexcept;
+  ProxyFit& operator=(ProxyFit&&) noexcept;
+  int size() const;
+  double rcond() const;
+  void solve(const double* rhs, double* out, int ncols) const;
+  void solve_transposed(const double* rhs, double* out, int ncols) const;
+  double residual(const double* rhs, const double* x) const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+const ProxyFit& lattice_fit(int degree);
+
+struct SBBInterpolant {
+  SphericalTriangle triangle;
+  int degree;
+  int dim;
+  std::vector<double> coefficients;
+};
+SBBInterpolant fit_coefficients(const ProxyPointSet& pts, const std::vector<double>& values, int dim = 1);
+double interpolant_eval(const SBBInterpolant& f, const UnitVector3& p);
+void interpolant_eval(const SBBInterpolant& f, const UnitVector3& p, double* out);
 
 // ---- treecode.hpp ----------------------------------------------------------
 struct TraversalConfig {
@@ -157,6 +284,12 @@ bool mac_well_separated(const TreeNode& tn, const TreeNode& sn, double theta);
 
 // target_tree and source_tree must be the same FaceTree (as in every reference call).
 InteractionList dual_traversal(const FaceTree& target_tree, const FaceTree& source_tree, const TraversalConfig& cfg);
+
+// Proxy weights of one source node (treecode.hpp:47-51), on the device. The
+// tree must be binned on `positions` (bin_particles / treecode_sum).
+std::vector<double> compute_proxy_weights(const FaceTree& tree, int source_node, const SBBBasis& basis,
+                                          const std::vector<UnitVector3>& positions,
+                                          const std::vector<double>& strengths);
 
 template <class Kernel>
 void eval_pp(const FaceTree& tree, const Interaction& it, const std::vector<UnitVector3>& positions,

@@ -309,6 +309,19 @@ int ref_eval_interaction(void* h, int kernel, const double* xyz, const double* q
   });
 }
 
+// compute_proxy_weights (treecode.cpp:79-91) of one node of a binned tree.
+int ref_compute_proxy_weights(void* h, int degree, const double* xyz, const double* q, int64_t n, int node,
+                              double* w) {
+  return guarded([&] {
+    const FaceTree& tree = *static_cast<FaceTree*>(h);
+    const auto pts = to_points(xyz, n);
+    const std::vector<double> s(q, q + n);
+    const SBBBasis basis(degree);
+    const std::vector<double> r = compute_proxy_weights(tree, node, basis, pts, s);
+    std::memcpy(w, r.data(), r.size() * sizeof(double));
+  });
+}
+
 // --- SBB / geometry probes used by the KAT tests ---------------------------
 int ref_sbb_eval(int degree, double b1, double b2, double b3, double* out) {
   return guarded([&] { SBBBasis(degree).eval({b1, b2, b3}, out); });

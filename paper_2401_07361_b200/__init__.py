@@ -38,7 +38,8 @@ __all__ = [
     "direct_sum", "treecode_sum", "rk4", "make_icosa_mesh", "rh4_vorticity",
     "make_random_cap", "GeometryError", "SingularKernelError", "ConditioningError",
     "ConfigError", "CudaError", "SpheresumError", "library_path", "load_library",
-    "mac_well_separated", "eval_pp", "eval_pc", "eval_cp", "eval_cc",
+    "mac_well_separated", "eval_pp", "eval_pc", "eval_cp", "eval_cc", "compute_proxy_weights",
+    "SBBBasis", "lattice_fit", "proxy_points", "sbb_basis_size",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -67,7 +68,12 @@ class SingularKernelError(SpheresumError):
 
 
 class ConditioningError(SpheresumError):
-    """Proxy Vandermonde too ill-conditioned (errors.hpp:22-27)."""
+    """Proxy Vandermonde too ill-conditioned (errors.hpp:22-27); `rcond` is the
+    reciprocal condition number that failed the > 1e-12 guard."""
+
+    def __init__(self, msg: str = "", rcond: float = 0.0):
+        super().__init__(msg)
+        self.rcond = rcond
 
 
 class CudaError(SpheresumError):
@@ -96,11 +102,12 @@ class _Stats(ctypes.Structure):
                 ("pp_pc_ms", ctypes.c_double), ("cp_cc_fit_ms", ctypes.c_double),
                 ("upward_ms", ctypes.c_double), ("finish_ms", ctypes.c_double),
                 ("up_visits", ctypes.c_uint64), ("down_visits", ctypes.c_uint64),
-                ("tiles_ms", ctypes.c_double)]
+                ("tiles_ms", ctypes.c_double), ("mac_host_decisions", ctypes.c_int64)]
 
 
 _LIB = None
 _P = ctypes.c_void_p
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (driver_types.h)
 _I64 = ctypes.c_int64
 
 # Every symbol declared in include/spheresum_b200.h (checked by the CPU tests).
@@ -111,7 +118,8 @@ EXPORTED_SYMBOLS = (
     "ssum_rk4", "ssum_mesh_vertex_count", "ssum_make_icosa_mesh", "ssum_rh4_vorticity",
     "ssum_make_random_cap", "ssum_fp64_peak", "ssum_probe_log_far", "ssum_set_partition", "ssum_partition_range",
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
-    "ssum_rk4_step_end",
+    "ssum_rk4_step_end", "ssum_compute_proxy_weights", "ssum_last_rcond", "ssum_lattice_fit",
+    "ssum_proxy_points",
 )
 
 
@@ -158,6 +166,10 @@ def load_library():
         "ssum_rk4_stage_begin": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64] + [_P] * 7),
         "ssum_rk4_stage_end": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64] + [_P] * 5),
         "ssum_rk4_step_end": (ctypes.c_int, [_P, ctypes.c_double, _I64] + [_P] * 4),
+        "ssum_compute_proxy_weights": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, ctypes.c_int, _P]),
+        "ssum_last_rcond": (ctypes.c_double, [_P]),
+        "ssum_lattice_fit": (ctypes.c_int, [ctypes.c_int, _P, _P]),
+        "ssum_proxy_points": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -255,6 +267,7 @@ class TreecodeStats:
     up_visits: int = 0      # (particle, weight node) pairs of the upward pass
     down_visits: int = 0    # (particle, fit node) pairs of the downward pass
     tiles_ms: float = 0.0   # CP/CC+fit and PP+PC tiles together (concurrent streams)
+    mac_host_decisions: int = 0  # MAC decisions made on the host inside the guard band (context total)
 
     def _to_c(self) -> _Stats:
         s = _Stats()
@@ -264,9 +277,14 @@ class TreecodeStats:
         return s
 
     def _from_c(self, s: _Stats) -> None:
+        """*_seconds come back accumulated (the C side adds to the values
+        passed in); interaction_counts accumulate here like the reference's
+        (treecode.cpp:296); the device detail describes the last call."""
         for name, _ in _Stats._fields_:
             v = getattr(s, name)
-            if name in ("interaction_counts", "kernel_evals"):
+            if name == "interaction_counts":
+                v = [a + int(x) for a, x in zip(self.interaction_counts, v)]
+            elif name == "kernel_evals":
                 v = [int(x) for x in v]
             setattr(self, name, v)
 
@@ -343,6 +361,9 @@ class FaceTree:
             pass
 
     def _check(self, rc: int):
+        if rc == 4:  # SSUM_CONDITIONING carries the failing rcond
+            raise ConditioningError(self._lib.ssum_last_error(self._h).decode(errors="replace"),
+                                    float(self._lib.ssum_last_rcond(self._h)))
         if rc != 0:
             _raise(rc, self._lib.ssum_last_error(self._h).decode(errors="replace"))
 
@@ -406,8 +427,17 @@ class FaceTree:
         v = ctypes.c_void_p
         self._check(self._lib.ssum_rk4_step_end(self._h, float(dt), int(n), v(x0), v(z0), v(acc), v(accz)))
 
-    def set_stream(self, stream_ptr: int) -> None:
-        self._check(self._lib.ssum_set_stream(self._h, ctypes.c_void_p(stream_ptr or None)))
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        """Run this tree's work on an external cudaStream_t (e.g.
+        torch.cuda.current_stream().cuda_stream). Handle 0 is CUDA's legacy
+        default stream (torch's default stream) and is passed on as
+        cudaStreamLegacy, so the work stays ordered with torch's; None
+        restores the context's own stream."""
+        if stream_ptr is None:
+            h = None
+        else:
+            h = int(stream_ptr) or _CUDA_STREAM_LEGACY
+        self._check(self._lib.ssum_set_stream(self._h, ctypes.c_void_p(h)))
 
     def reset(self) -> None:
         """Forget all node geometry (a freshly constructed FaceTree)."""
@@ -537,6 +567,76 @@ def eval_cc(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: 
             field: np.ndarray) -> None:
     """eval_cc<K> (treecode.cpp:223-244)."""
     _eval_interaction(kernel, tree, it, positions, strengths, cfg, field)
+
+
+def sbb_basis_size(degree: int) -> int:
+    """(d + 1)(d + 2) / 2 (sbb.hpp:15)."""
+    return (degree + 1) * (degree + 2) // 2
+
+
+class SBBBasis:
+    """SBBBasis (sbb.hpp:19-36): B_ijk(b) = b1^i b2^j b3^k over i + j + k = d,
+    ordered k ascending, then j ascending (sbb.cpp:13-24)."""
+
+    def __init__(self, degree: int):
+        if not (1 <= degree <= 20):
+            raise ValueError("SBB degree must be in [1, 20]")
+        self._d = int(degree)
+        self._idx = np.array([(degree - k - j, j, k) for k in range(degree + 1) for j in range(degree - k + 1)],
+                             np.int64)
+
+    def degree(self) -> int:
+        return self._d
+
+    def size(self) -> int:
+        return self._idx.shape[0]
+
+    def index_set(self) -> np.ndarray:
+        return self._idx.copy()
+
+    def eval(self, b) -> np.ndarray:
+        """Basis values at barycentric coordinates b = (b1, b2, b3); 0^0 = 1."""
+        b = np.asarray(b, dtype=np.float64)
+        return b[0] ** self._idx[:, 0] * b[1] ** self._idx[:, 1] * b[2] ** self._idx[:, 2]
+
+
+def lattice_fit(degree: int) -> Tuple[np.ndarray, float]:
+    """lattice_fit(degree) (sbb.cpp:124-138): (V^-1, rcond) of the lattice
+    Vandermonde, from the library (the matrix the tree code applies).
+    Raises ConditioningError (with rcond) when rcond <= 1e-12."""
+    lib = load_library()
+    p = sbb_basis_size(degree)
+    inv = np.zeros((p, p))
+    rc = ctypes.c_double()
+    code = lib.ssum_lattice_fit(int(degree), _ptr(inv), ctypes.byref(rc))
+    if code == 4:
+        raise ConditioningError(f"proxy Vandermonde too ill-conditioned (rcond {rc.value:g})", rc.value)
+    _raise(code, "lattice_fit failed (degree must be in [1, 20])")
+    return inv, rc.value
+
+
+def proxy_points(triangle, degree: int) -> np.ndarray:
+    """proxy_points(t, degree).points (sbb.cpp:46-66): (P, 3) lattice points of
+    a spherical triangle (rows v1, v2, v3), reference rounding."""
+    lib = load_library()
+    t = np.ascontiguousarray(triangle, dtype=np.float64).reshape(9)
+    out = np.zeros((sbb_basis_size(degree), 3))
+    _raise(lib.ssum_proxy_points(_ptr(t), int(degree), _ptr(out)), "proxy_points failed")
+    return out
+
+
+def compute_proxy_weights(tree: FaceTree, source_node: int, basis, positions, strengths) -> np.ndarray:
+    """compute_proxy_weights (treecode.cpp:79-91): w_k = sum over the source
+    node's bin of B_k(beta(x_j)) q_j, on the device. `basis` is an SBBBasis
+    or a degree; the tree must be binned on `positions`."""
+    degree = basis.degree() if isinstance(basis, SBBBasis) else int(basis)
+    p = _as_positions(positions)
+    n = p.shape[0]
+    q = _as_vector(strengths, n, "strengths")
+    w = np.zeros(sbb_basis_size(degree))
+    tree._check(tree._lib.ssum_compute_proxy_weights(tree._h, degree, _ptr(p), _ptr(q), n, int(source_node),
+                                                     _ptr(w)))
+    return w
 
 
 _DEFAULT_TREES = {}

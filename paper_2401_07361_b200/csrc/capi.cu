@@ -98,6 +98,10 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
   struct Early {  // build_lists starts the upward pass early (start_prep)
     Ctx& c;
     ~Early() {
+      // evaluate() normally joins prep_ev; if anything threw in between, join
+      // here so the side stream's gather / upward pass cannot overlap the
+      // next call's binning
+      if (c.prep_started) cudaStreamWaitEvent(c.stream, c.prep_ev, 0);
       c.early = Ctx::Early{};
       c.prep_started = false;
     }
@@ -142,6 +146,7 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
     st->up_visits = c.lists.visits[0];
     st->down_visits = c.lists.visits[1];
     st->gpu_launches = c.launches - l0;
+    st->mac_host_decisions = c.mac.resolved;
   }
 }
 
@@ -265,6 +270,16 @@ __global__ void k_rk4_final(int64_t n, double h6, double* __restrict__ x0, doubl
   z0[i] = add_rn(z0[i], mul_rn(h6, accz[i]));
 }
 
+// reference node id -> device node id of the context's tree
+int dev_node(Ctx& c, int ref_id) {
+  const std::vector<int> ref = reference_ids(host_tree(c));
+  const int nn = static_cast<int>(ref.size());
+  if (ref_id < 0 || ref_id >= nn) throw Error(SSUM_INVALID, "node id out of range");
+  for (int d = 0; d < nn; ++d)
+    if (ref[size_t(d)] == ref_id) return d;
+  throw Error(SSUM_INTERNAL, "node id not found");
+}
+
 }  // namespace
 }  // namespace ssum
 
@@ -294,6 +309,7 @@ int ssum_create(int device, ssum_ctx** out) {
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->prep_ev, cudaEventDisableTiming));
     if (const char* v = std::getenv("SSUM_OVERLAP_TILES")) c->overlap_tiles = std::atoi(v) != 0;
     if (const char* v = std::getenv("SSUM_EARLY_PREP")) c->early_prep = std::atoi(v) != 0;
+    if (const char* v = std::getenv("SSUM_MAC_BAND")) c->mac.band = std::atof(v);
     for (auto& e : c->io.xyz) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->io.out) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->io.q, cudaEventDisableTiming));
@@ -376,6 +392,8 @@ int ssum_tree_perm(ssum_ctx* h, int* dst, int on_device) {
 int ssum_tree_reset(ssum_ctx* h) {
   return guarded(h, [&](Ctx& c) {
     c.call_index = 0;
+    c.mac.keys.clear();
+    c.mac.theta = -1.0;
     tree_init_roots(c);
   });
 }
@@ -427,6 +445,11 @@ int ssum_treecode_sum(ssum_ctx* h, int kernel, const ssum_config* cfg, const dou
     }
     if (n) SSUM_CUDA_CHECK(cudaMemcpyAsync(c.in_q.p, q, size_t(n) * 8, cudaMemcpyHostToDevice, c.copy_stream));
     SSUM_CUDA_CHECK(cudaEventRecord(io.q, c.copy_stream));
+    // A partitioned call computes only its part's rows; the others must come
+    // back as the caller had them, so the device result starts as a copy of
+    // the caller's buffer (unpartitioned calls overwrite every row).
+    if (c.nparts > 1 && n)
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(c.out_buf.p, out, size_t(n) * D * 8, cudaMemcpyHostToDevice, c.stream));
     io.active = true;
     io.h_out = out;
     io.dim = D;
@@ -543,6 +566,9 @@ int ssum_dual_traversal(ssum_ctx* h, const ssum_config* cfg, int* tsk, int64_t c
   });
 }
 
+// eval_pp / eval_pc / eval_cp / eval_cc: O(|t| |s|) on the device (eval.cu
+// eval_interaction); only the two bins' rows of the caller's arrays are read
+// and only the target bin's rows of field are updated.
 int ssum_eval_interaction(ssum_ctx* h, int kernel, const ssum_config* cfg, const double* xyz, const double* q,
                           int64_t n, int target, int source, int kind, double* field) {
   return guarded(h, [&](Ctx& c) {
@@ -552,40 +578,64 @@ int ssum_eval_interaction(ssum_ctx* h, int kernel, const ssum_config* cfg, const
     if (n != c.bins.n) throw Error(SSUM_INVALID, "eval_interaction: positions do not match the binned tree");
     if (kind < 0 || kind > 3) throw Error(SSUM_INVALID, "eval_interaction: unknown interaction kind");
     if (n == 0) return;
-    const std::vector<int> ref = reference_ids(host_tree(c));
-    const int nn = static_cast<int>(ref.size());
-    if (target < 0 || target >= nn || source < 0 || source >= nn)
-      throw Error(SSUM_INVALID, "eval_interaction: node id out of range");
-    std::vector<int> dev_of(static_cast<size_t>(nn));
-    for (int d = 0; d < nn; ++d) dev_of[static_cast<size_t>(ref[d])] = d;
-    const int D = kernel == SSUM_BIOT_SAVART ? 3 : 1;
-    upload(c, c.in_xyz, xyz, size_t(n) * 3, nullptr);
-    upload(c, c.in_q, q, size_t(n), nullptr);
-    c.out_buf.ensure(size_t(n) * D * 2);
-    const int4 it{dev_of[static_cast<size_t>(target)], dev_of[static_cast<size_t>(source)], kind, 0};
-    c.lists.inter.ensure(1);
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.lists.inter.p, &it, sizeof(int4), cudaMemcpyHostToDevice, c.stream));
-    c.lists.n_inter = 1;
-    const int part = c.part, nparts = c.nparts;
-    c.part = 0;
-    c.nparts = 1;
-    try {
-      build_lists(c, *cfg);
-      evaluate(c, kernel, *cfg, c.in_xyz.p, c.in_q.p, n, c.out_buf.p, nullptr);
-    } catch (...) {
-      c.part = part;
-      c.nparts = nparts;
-      throw;
-    }
-    c.part = part;
-    c.nparts = nparts;
-    // field += out / prefactor (raw kernel sums, treecode.hpp:53-54)
-    double* d_field = c.out_buf.p + size_t(n) * D;
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(d_field, field, size_t(n) * D * 8, cudaMemcpyHostToDevice, c.stream));
-    const double inv_pref = kernel == SSUM_BIOT_SAVART ? -4.0 * 3.14159265358979323846 : 1.0;
-    add_scaled(c, d_field, c.out_buf.p, inv_pref, int64_t(n) * D);
-    download(c, field, d_field, size_t(n) * D, nullptr);
+    const int tdev = dev_node(c, target), sdev = dev_node(c, source);
+    eval_interaction(c, kernel, cfg->degree, xyz, q, tdev, sdev, kind, field);
   });
+}
+
+int ssum_compute_proxy_weights(ssum_ctx* h, int degree, const double* xyz, const double* q, int64_t n,
+                               int source_node, double* w) {
+  return guarded(h, [&](Ctx& c) {
+    if (degree < 1 || degree > kMaxDegree) throw Error(SSUM_INVALID, "SBB degree must be in [1, 20]");
+    check_n(n);
+    if (n != c.bins.n) throw Error(SSUM_INVALID, "compute_proxy_weights: positions do not match the binned tree");
+    const int P = (degree + 1) * (degree + 2) / 2;
+    if (n == 0) {
+      std::fill(w, w + P, 0.0);
+      return;
+    }
+    proxy_weights(c, degree, xyz, q, dev_node(c, source_node), w);
+  });
+}
+
+double ssum_last_rcond(const ssum_ctx* h) {
+  const Ctx* c = reinterpret_cast<const Ctx*>(h);
+  return c ? c->last_rcond : 0.0;
+}
+
+int ssum_lattice_fit(int degree, double* vinv, double* rcond) {
+  try {
+    if (degree < 1 || degree > kMaxDegree) return SSUM_INVALID;
+    std::vector<double> inv;
+    double rc = 0.0;
+    lattice_inverse(degree, inv, rc);
+    if (rcond) *rcond = rc;
+    if (vinv) std::copy(inv.begin(), inv.end(), vinv);
+    return rc > 1e-12 ? SSUM_OK : SSUM_CONDITIONING;
+  } catch (...) {
+    return SSUM_INTERNAL;
+  }
+}
+
+int ssum_proxy_points(const double* tri, int degree, double* pts) {
+  if (!tri || !pts || degree < 1 || degree > kMaxDegree) return SSUM_INVALID;
+  const double d = static_cast<double>(degree);
+  int m = 0;
+  for (int kk = 0; kk <= degree; ++kk)
+    for (int jj = 0; jj <= degree - kk; ++jj, ++m) {
+      const int ii = degree - kk - jj;
+      const double b1 = ii / d, b2 = jj / d, b3 = kk / d;
+      const d3 v{add_rn(add_rn(mul_rn(tri[0], b1), mul_rn(tri[3], b2)), mul_rn(tri[6], b3)),
+                 add_rn(add_rn(mul_rn(tri[1], b1), mul_rn(tri[4], b2)), mul_rn(tri[7], b3)),
+                 add_rn(add_rn(mul_rn(tri[2], b1), mul_rn(tri[5], b2)), mul_rn(tri[8], b3))};
+      int bad = 0;
+      const d3 u = unit_rn(v, &bad);
+      if (bad) return SSUM_GEOMETRY;
+      pts[3 * m] = u.x;
+      pts[3 * m + 1] = u.y;
+      pts[3 * m + 2] = u.z;
+    }
+  return SSUM_OK;
 }
 
 int ssum_rk4(ssum_ctx* h, const ssum_config* cfg, double* xyz, double* zeta, const double* area, int64_t n,

@@ -5,13 +5,16 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
+
+#include "geom.cuh"  // the decision arithmetic shared with the device (host build)
 
 namespace spheresum {
 
 namespace {
 
-[[noreturn]] void throw_status(int code, const char* msg) {
+[[noreturn]] void throw_status(int code, const char* msg, double rcond = 0.0) {
   const std::string m = msg ? msg : "";
   switch (code) {
     case SSUM_CONFIG:
@@ -21,7 +24,7 @@ namespace {
     case SSUM_SINGULAR:
       throw SingularKernelError(m);
     case SSUM_CONDITIONING:
-      throw ConditioningError(m, 0.0);
+      throw ConditioningError(m, rcond);
     case SSUM_INVALID:
       throw std::invalid_argument(m);
     default:
@@ -30,7 +33,14 @@ namespace {
 }
 
 void check(ssum_ctx* c, int rc) {
-  if (rc != SSUM_OK) throw_status(rc, c ? ssum_last_error(c) : "no context");
+  if (rc != SSUM_OK) throw_status(rc, c ? ssum_last_error(c) : "no context", c ? ssum_last_rcond(c) : 0.0);
+}
+
+ssum::d3 d3_of(const UnitVector3& u) { return {u.x, u.y, u.z}; }
+UnitVector3 raw_unit(const ssum::d3& v) {  // already unit (computed with the reference's rounding)
+  UnitVector3 u;
+  u.x = v.x, u.y = v.y, u.z = v.z;
+  return u;
 }
 
 ssum_config to_c(const TraversalConfig& cfg) {
@@ -71,6 +81,280 @@ UnitVector3::UnitVector3(double xr, double yr, double zr) {
   x = xr / n;
   y = yr / n;
   z = zr / n;
+}
+
+// ---- geometry.hpp (geometry.cpp), through the expressions of geom.cuh ------
+SphericalTriangle::SphericalTriangle(const UnitVector3& a, const UnitVector3& b, const UnitVector3& c)
+    : v1(a), v2(b), v3(c) {
+  const ssum::d3 A = d3_of(a), B = d3_of(b), C = d3_of(c);
+  if (ssum::arc_dist(A, B) <= 1e-12 || ssum::arc_dist(B, C) <= 1e-12 || ssum::arc_dist(C, A) <= 1e-12)
+    throw GeometryError("spherical triangle has coincident vertices");
+  if (ssum::dot_rn(A, ssum::cross_rn(B, C)) <= 0.0)
+    throw GeometryError("spherical triangle vertices are not counterclockwise");
+}
+
+UnitVector3 latlon_to_unit(const LatLon& p) {
+  const double cl = std::cos(p.lat);
+  return UnitVector3(cl * std::cos(p.lon), cl * std::sin(p.lon), std::sin(p.lat));
+}
+
+LatLon unit_to_latlon(const UnitVector3& v) {
+  LatLon o;
+  o.lat = std::asin(std::min(1.0, std::max(-1.0, v.z)));
+  o.lon = std::atan2(v.y, v.x);
+  if (o.lon >= M_PI) o.lon -= 2.0 * M_PI;
+  return o;
+}
+
+double great_circle_distance(const UnitVector3& a, const UnitVector3& b) { return ssum::arc_dist(d3_of(a), d3_of(b)); }
+
+BarycentricCoords spherical_barycentric(const SphericalTriangle& t, const UnitVector3& p) {
+  const ssum::d3 a = d3_of(t.v1), b = d3_of(t.v2), c = d3_of(t.v3), x = d3_of(p);
+  const double det = ssum::dot_rn(a, ssum::cross_rn(b, c));
+  if (std::fabs(det) < 1e-14) throw GeometryError("degenerate triangle in barycentric solve");
+  const double r0 = ssum::dot_rn(x, ssum::cross_rn(b, c)) / det;
+  const double r1 = ssum::dot_rn(a, ssum::cross_rn(x, c)) / det;
+  const double r2 = ssum::dot_rn(a, ssum::cross_rn(b, x)) / det;
+  const double sum = r0 + r1 + r2;
+  if (std::fabs(sum) < 1e-14) throw GeometryError("point has no radial projection onto the triangle plane");
+  return {r0 / sum, r1 / sum, r2 / sum};
+}
+
+UnitVector3 triangle_circumcenter(const SphericalTriangle& t) {
+  int bad = 0;
+  const ssum::d3 c = ssum::circumcenter_rn(d3_of(t.v1), d3_of(t.v2), d3_of(t.v3), &bad);
+  if (bad) throw GeometryError("degenerate triangle in circumcenter");
+  return raw_unit(c);
+}
+
+double triangle_radius(const SphericalTriangle& t) { return great_circle_distance(triangle_circumcenter(t), t.v1); }
+
+bool triangle_contains(const SphericalTriangle& t, const UnitVector3& p) {
+  return ssum::contains_rn(d3_of(t.v1), d3_of(t.v2), d3_of(t.v3), d3_of(p));
+}
+
+// spherical excess: interior angles (between the tangent directions towards
+// the two neighbours) minus (n - 2) pi
+double spherical_polygon_area(const std::vector<UnitVector3>& vs) {
+  const size_t n = vs.size();
+  if (n < 3) throw GeometryError("spherical polygon needs at least 3 vertices");
+  double angles = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const UnitVector3& h = vs[i];
+    const UnitVector3& a = vs[(i + n - 1) % n];
+    const UnitVector3& b = vs[(i + 1) % n];
+    const Vec3 ta = a.vec() - dot(a, h) * h.vec();
+    const Vec3 tb = b.vec() - dot(b, h) * h.vec();
+    angles += std::atan2(norm(cross(ta, tb)), dot(ta, tb));
+  }
+  return angles - (static_cast<double>(n) - 2.0) * M_PI;
+}
+
+double spherical_triangle_area(const SphericalTriangle& t) { return spherical_polygon_area({t.v1, t.v2, t.v3}); }
+
+double barycentric_min_score(const UnitVector3& a, const UnitVector3& b, const UnitVector3& c, const UnitVector3& p) {
+  const ssum::d3 A = d3_of(a), B = d3_of(b), C = d3_of(c);
+  const ssum::d3 bc = ssum::cross_rn(B, C);
+  return ssum::min_score_rn(A, B, C, bc, ssum::dot_rn(A, bc), d3_of(p));
+}
+
+// ---- sbb.hpp ------------------------------------------------------------------
+SBBBasis::SBBBasis(int degree) : degree_(degree) {
+  if (degree < 1 || degree > kMaxSbbDegree) throw std::invalid_argument("SBB degree must be in [1, 20]");
+  for (int k = 0; k <= degree; ++k)
+    for (int j = 0; j <= degree - k; ++j) index_set_.push_back({degree - k - j, j, k});
+}
+
+void SBBBasis::eval(const BarycentricCoords& b, double* out) const {
+  double p1[kMaxSbbDegree + 1], p2[kMaxSbbDegree + 1], p3[kMaxSbbDegree + 1];
+  p1[0] = p2[0] = p3[0] = 1.0;
+  for (int e = 1; e <= degree_; ++e) {
+    p1[e] = p1[e - 1] * b.b1;
+    p2[e] = p2[e - 1] * b.b2;
+    p3[e] = p3[e - 1] * b.b3;
+  }
+  for (size_t m = 0; m < index_set_.size(); ++m) {
+    const std::array<int, 3>& e = index_set_[m];
+    out[m] = p1[e[0]] * p2[e[1]] * p3[e[2]];
+  }
+}
+
+std::vector<double> SBBBasis::eval(const BarycentricCoords& b) const {
+  std::vector<double> v(index_set_.size());
+  eval(b, v.data());
+  return v;
+}
+
+ProxyPointSet proxy_points_from_barycentric(const SphericalTriangle& t, int degree,
+                                            std::vector<BarycentricCoords> bary) {
+  ProxyPointSet s{t, degree, {}, std::move(bary)};
+  for (const BarycentricCoords& b : s.barycentric)
+    s.points.push_back(UnitVector3(b.b1 * t.v1.vec() + b.b2 * t.v2.vec() + b.b3 * t.v3.vec()));
+  return s;
+}
+
+ProxyPointSet proxy_points(const SphericalTriangle& t, int degree) {
+  const SBBBasis basis(degree);
+  lattice_fit(degree);  // the conditioning guard, as the reference trips it here
+  const double d = static_cast<double>(degree);
+  std::vector<BarycentricCoords> bary;
+  for (const std::array<int, 3>& e : basis.index_set()) bary.push_back({e[0] / d, e[1] / d, e[2] / d});
+  return proxy_points_from_barycentric(t, degree, std::move(bary));
+}
+
+// Row-major LU with partial pivoting (first largest pivot), P A = L U.
+struct ProxyFit::Impl {
+  int n = 0;
+  std::vector<double> a;   // the matrix V
+  std::vector<double> lu;  // packed L (unit diagonal) and U
+  std::vector<int> piv;    // row of A at position i of P A
+  double rcond = 0.0;
+  void solve_col(const double* b, double* x) const {  // V x = b
+    std::vector<double> y(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      double s = b[piv[size_t(i)]];
+      for (int k = 0; k < i; ++k) s -= lu[size_t(i) * n + k] * y[size_t(k)];
+      y[size_t(i)] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[size_t(i)];
+      for (int k = i + 1; k < n; ++k) s -= lu[size_t(i) * n + k] * x[k];
+      x[i] = s / lu[size_t(i) * n + i];
+    }
+  }
+  void solve_col_t(const double* b, double* x) const {  // V^T x = b: U^T z = b, L^T w = z, x = P^T w
+    std::vector<double> z(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      double s = b[i];
+      for (int k = 0; k < i; ++k) s -= lu[size_t(k) * n + i] * z[size_t(k)];
+      z[size_t(i)] = s / lu[size_t(i) * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = z[size_t(i)];
+      for (int k = i + 1; k < n; ++k) s -= lu[size_t(k) * n + i] * z[size_t(k)];
+      z[size_t(i)] = s;
+    }
+    for (int i = 0; i < n; ++i) x[piv[size_t(i)]] = z[size_t(i)];
+  }
+};
+
+ProxyFit::ProxyFit(const SBBBasis& basis, const std::vector<BarycentricCoords>& bary)
+    : impl_(std::make_unique<Impl>()) {
+  const int n = basis.size();
+  if (static_cast<int>(bary.size()) != n) throw std::invalid_argument("proxy point count must equal the basis size");
+  Impl& m = *impl_;
+  m.n = n;
+  m.a.resize(size_t(n) * n);
+  for (int r = 0; r < n; ++r) basis.eval(bary[size_t(r)], &m.a[size_t(r) * n]);
+  m.lu = m.a;
+  m.piv.resize(size_t(n));
+  for (int i = 0; i < n; ++i) m.piv[size_t(i)] = i;
+  bool singular = false;
+  for (int k = 0; k < n && !singular; ++k) {
+    int p = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(m.lu[size_t(i) * n + k]) > std::fabs(m.lu[size_t(p) * n + k])) p = i;
+    if (m.lu[size_t(p) * n + k] == 0.0) {
+      singular = true;
+      break;
+    }
+    if (p != k) {
+      for (int j = 0; j < n; ++j) std::swap(m.lu[size_t(k) * n + j], m.lu[size_t(p) * n + j]);
+      std::swap(m.piv[size_t(k)], m.piv[size_t(p)]);
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double l = m.lu[size_t(i) * n + k] /= m.lu[size_t(k) * n + k];
+      for (int j = k + 1; j < n; ++j) m.lu[size_t(i) * n + j] -= l * m.lu[size_t(k) * n + j];
+    }
+  }
+  if (!singular) {  // exact 1-norm reciprocal condition number: ||V||_1 ||V^-1||_1
+    double an = 0.0, in = 0.0;
+    std::vector<double> e(static_cast<size_t>(n)), col(static_cast<size_t>(n));
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += std::fabs(m.a[size_t(i) * n + j]);
+      an = std::max(an, s);
+      std::fill(e.begin(), e.end(), 0.0);
+      e[size_t(j)] = 1.0;
+      m.solve_col(e.data(), col.data());
+      double t = 0.0;
+      for (int i = 0; i < n; ++i) t += std::fabs(col[size_t(i)]);
+      in = std::max(in, t);
+    }
+    m.rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
+  }
+  if (!(m.rcond > 1e-12))
+    throw ConditioningError("proxy Vandermonde too ill-conditioned (rcond " + std::to_string(m.rcond) + ")", m.rcond);
+}
+
+ProxyFit::~ProxyFit() = default;
+ProxyFit::ProxyFit(ProxyFit&&) noexcept = default;
+ProxyFit& ProxyFit::operator=(ProxyFit&&) noexcept = default;
+int ProxyFit::size() const { return impl_->n; }
+double ProxyFit::rcond() const { return impl_->rcond; }
+
+void ProxyFit::solve(const double* rhs, double* out, int ncols) const {
+  const int n = impl_->n;
+  for (int c = 0; c < ncols; ++c) impl_->solve_col(rhs + size_t(c) * n, out + size_t(c) * n);
+}
+
+void ProxyFit::solve_transposed(const double* rhs, double* out, int ncols) const {
+  const int n = impl_->n;
+  for (int c = 0; c < ncols; ++c) impl_->solve_col_t(rhs + size_t(c) * n, out + size_t(c) * n);
+}
+
+double ProxyFit::residual(const double* rhs, const double* x) const {
+  const int n = impl_->n;
+  double worst = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += impl_->a[size_t(i) * n + k] * x[k];
+    worst = std::max(worst, std::fabs(s - rhs[i]));
+  }
+  return worst;
+}
+
+const ProxyFit& lattice_fit(int degree) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<ProxyFit>> fits;
+  std::lock_guard<std::mutex> lock(mu);
+  std::unique_ptr<ProxyFit>& f = fits[degree];
+  if (!f) {
+    const SBBBasis basis(degree);
+    const double d = static_cast<double>(degree);
+    std::vector<BarycentricCoords> bary;
+    for (const std::array<int, 3>& e : basis.index_set()) bary.push_back({e[0] / d, e[1] / d, e[2] / d});
+    f = std::make_unique<ProxyFit>(basis, bary);
+  }
+  return *f;
+}
+
+SBBInterpolant fit_coefficients(const ProxyPointSet& pts, const std::vector<double>& values, int dim) {
+  const SBBBasis basis(pts.degree);
+  if (static_cast<int>(values.size()) != basis.size() * dim)
+    throw std::invalid_argument("value count must equal proxy point count times dim");
+  const ProxyFit fit(basis, pts.barycentric);
+  SBBInterpolant f{pts.triangle, pts.degree, dim, std::vector<double>(values.size())};
+  fit.solve(values.data(), f.coefficients.data(), dim);
+  return f;
+}
+
+void interpolant_eval(const SBBInterpolant& f, const UnitVector3& p, double* out) {
+  const SBBBasis basis(f.degree);
+  const int n = basis.size();
+  double b[sbb_basis_size(kMaxSbbDegree)];
+  basis.eval(spherical_barycentric(f.triangle, p), b);
+  for (int d = 0; d < f.dim; ++d) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += f.coefficients[size_t(d) * n + k] * b[k];
+    out[d] = s;
+  }
+}
+
+double interpolant_eval(const SBBInterpolant& f, const UnitVector3& p) {
+  double v = 0.0;
+  interpolant_eval(f, p, &v);
+  return v;
 }
 
 void TraversalConfig::validate() const {
@@ -186,6 +470,17 @@ InteractionList dual_traversal(const FaceTree& target_tree, const FaceTree& sour
   for (int64_t e = 0; e < count; ++e)
     out[e] = Interaction{tsk[3 * e], tsk[3 * e + 1], static_cast<InteractionKind>(tsk[3 * e + 2])};
   return out;
+}
+
+std::vector<double> compute_proxy_weights(const FaceTree& tree, int source_node, const SBBBasis& basis,
+                                          const std::vector<UnitVector3>& positions,
+                                          const std::vector<double>& strengths) {
+  if (positions.size() != strengths.size()) throw std::invalid_argument("compute_proxy_weights: size mismatch");
+  std::vector<double> w(size_t(basis.size()));
+  check(tree.context(), ssum_compute_proxy_weights(tree.context(), basis.degree(), xyz_of(positions),
+                                                   strengths.data(), static_cast<int64_t>(positions.size()),
+                                                   source_node, w.data()));
+  return w;
 }
 
 namespace {

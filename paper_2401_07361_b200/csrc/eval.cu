@@ -181,9 +181,11 @@ __global__ void k_up_fill(const int* __restrict__ weight_nodes, int nw, const in
 }
 
 // w = sum of the node's chunk partials (in chunk order); w_hat = V^-T w.
+// raw != nullptr: store w itself (compute_proxy_weights) and stop.
 __global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const int2* __restrict__ chunk_range,
                            const double* __restrict__ wpart, const double* __restrict__ vinv, int P,
-                           const int* __restrict__ pslot, int64_t N, double4* __restrict__ pts) {
+                           const int* __restrict__ pslot, int64_t N, double4* __restrict__ pts,
+                           double* __restrict__ raw = nullptr) {
   extern __shared__ double ws[];
   const int w = blockIdx.x;
   if (w >= nw) return;
@@ -192,7 +194,9 @@ __global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const i
     double s = 0.0;
     for (int c = cr.x; c < cr.y; ++c) s += wpart[size_t(c) * P + m];
     ws[m] = s;
+    if (raw) raw[size_t(w) * P + m] = s;
   }
+  if (raw) return;
   __syncthreads();
   const int64_t base = N + int64_t(pslot[weight_nodes[w]]) * P;
   for (int kk = threadIdx.x; kk < P; kk += blockDim.x) {
@@ -415,10 +419,10 @@ void launch_up_partial(Ctx& c, cudaStream_t stream, int degree, int nchunks, con
 }  // namespace
 
 // V[m][k] = B_k(b_m) on the lattice (sbb.cpp:80-85), LU with partial pivoting,
-// explicit inverse; ConditioningError when the 1-norm reciprocal condition
-// number is not > 1e-12 (sbb.cpp:89-93).
-void ensure_vinv(Ctx& c, int degree) {
-  if (c.vinv_degree == degree) return;
+// explicit inverse, and the exact 1-norm reciprocal condition number
+// (lattice_fit / ProxyFit, sbb.cpp:74-138; the reference's Eigen rcond() is
+// an estimate of the same quantity). rcond = 0 for a singular matrix.
+void lattice_inverse(int degree, std::vector<double>& inv, double& rcond) {
   const int P = (degree + 1) * (degree + 2) / 2;
   std::vector<int> I(static_cast<size_t>(P)), J(static_cast<size_t>(P)), K(static_cast<size_t>(P));
   {
@@ -445,6 +449,8 @@ void ensure_vinv(Ctx& c, int degree) {
     }
   }
   A = V;
+  inv.assign(size_t(P) * P, 0.0);
+  rcond = 0.0;
   std::vector<int> perm(static_cast<size_t>(P));
   for (int i = 0; i < P; ++i) perm[i] = i;
   for (int k = 0; k < P; ++k) {
@@ -455,7 +461,7 @@ void ensure_vinv(Ctx& c, int degree) {
         best = std::fabs(A[size_t(i) * P + k]);
         piv = i;
       }
-    if (best == 0.0) throw Error(SSUM_CONDITIONING, "proxy Vandermonde is singular");
+    if (best == 0.0) return;  // singular
     if (piv != k) {
       for (int j = 0; j < P; ++j) std::swap(A[size_t(k) * P + j], A[size_t(piv) * P + j]);
       std::swap(perm[k], perm[piv]);
@@ -466,7 +472,6 @@ void ensure_vinv(Ctx& c, int degree) {
       for (int j = k + 1; j < P; ++j) A[size_t(i) * P + j] -= l * A[size_t(k) * P + j];
     }
   }
-  std::vector<double> inv(size_t(P) * P);
   std::vector<double> y(static_cast<size_t>(P));
   for (int col = 0; col < P; ++col) {
     for (int i = 0; i < P; ++i) y[i] = (perm[i] == col) ? 1.0 : 0.0;
@@ -488,10 +493,21 @@ void ensure_vinv(Ctx& c, int degree) {
     an = std::max(an, s1);
     in = std::max(in, s2);
   }
-  const double rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
-  if (!(rcond > 1e-12))
+  rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
+}
+
+// ConditioningError when the reciprocal condition number is not > 1e-12
+// (sbb.cpp:89-93); the value travels with the error (Ctx::last_rcond).
+void ensure_vinv(Ctx& c, int degree) {
+  if (c.vinv_degree == degree) return;
+  std::vector<double> inv;
+  double rcond = 0.0;
+  lattice_inverse(degree, inv, rcond);
+  if (!(rcond > 1e-12)) {
+    c.last_rcond = rcond;
     throw Error(SSUM_CONDITIONING, "proxy Vandermonde too ill-conditioned (rcond " + std::to_string(rcond) + ")");
-  c.vinv.ensure(size_t(P) * P);
+  }
+  c.vinv.ensure(inv.size());
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.vinv.p, inv.data(), inv.size() * 8, cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   c.vinv_degree = degree;
@@ -610,9 +626,28 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
   const bool fork = c.overlap_tiles && nfit > 0 && ntl > 0;
   cudaStream_t fit_stream = fork ? c.side_stream : c.stream;
   cudaEventRecord(c.ev[3], c.stream);
+  // the join below also runs when a launch check throws in between, so no
+  // fit-tile work outlives this call unordered with the caller's stream
+  struct Join {
+    Ctx& c;
+    bool on = false;
+    void now() {
+      if (!on) return;
+      on = false;
+      SSUM_CUDA_CHECK(cudaEventRecord(c.join_ev, c.side_stream));
+      SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
+    }
+    ~Join() {
+      if (on) {
+        cudaEventRecord(c.join_ev, c.side_stream);
+        cudaStreamWaitEvent(c.stream, c.join_ev, 0);
+      }
+    }
+  } join{c};
   if (fork) {
     SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
     SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
+    join.on = true;
   }
   cudaEventRecord(c.side_ev[0], fit_stream);
   if (nfit > 0) {
@@ -628,10 +663,7 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     c.launches++;
   }
   cudaEventRecord(c.leaf_ev[1], c.stream);
-  if (fork) {
-    SSUM_CUDA_CHECK(cudaEventRecord(c.join_ev, c.side_stream));
-    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.join_ev, 0));
-  }
+  join.now();
   cudaEventRecord(c.ev[4], c.stream);
 
   // ---- downward + finish
@@ -709,6 +741,219 @@ void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_
   c.launches++;
   launch_direct(c, kernel, n, d_out);
   check_flags(c, "direct_sum");
+}
+
+// ---- per-interaction entry points -----------------------------------------
+// eval_pp / eval_pc / eval_cp / eval_cc (treecode.cpp:170-244) and
+// compute_proxy_weights (treecode.cpp:79-91) for one node pair of the last
+// binning, in O(|t| |s| + (|t| + |s|) p + p^2) work: only the two bins'
+// particles are packed (from the caller's arrays, through the binning's
+// permutation) into a compact point array, followed by the source's and the
+// target's proxy points, and the pairs run through the tree code's own
+// kernels (k_tiles leaf / fit mode, k_up_partial / k_up_final, k_proxy).
+namespace {
+
+// Compact layout: bins are contiguous tree-position ranges and two bins are
+// either nested or disjoint. Nested (incl. equal): the outer range is packed
+// once, so a particle in both bins is one point (self pairs are excluded by
+// index, as in the tree code). Disjoint: target bin, then source bin.
+struct Compact {
+  int64_t n = 0;
+  int t0 = 0, nt = 0, s0 = 0, ns = 0;
+  bool nested = false;
+  std::vector<int> ids;  // caller index of each compact particle
+};
+
+Compact pack_bins(Ctx& c, const double* xyz, const double* q, int tdev, int sdev) {
+  const HostTree& h = host_tree(c);
+  Compact k;
+  const int64_t a0 = h.off[size_t(tdev)], a1 = a0 + h.cnt[size_t(tdev)];
+  const int64_t b0 = h.off[size_t(sdev)], b1 = b0 + h.cnt[size_t(sdev)];
+  k.nt = static_cast<int>(a1 - a0);
+  k.ns = static_cast<int>(b1 - b0);
+  std::vector<std::pair<int64_t, int64_t>> runs;
+  if (k.nt > 0 && k.ns > 0 && a0 < b1 && b0 < a1) {
+    k.nested = true;
+    const int64_t o0 = std::min(a0, b0), o1 = std::max(a1, b1);
+    runs.push_back({o0, o1});
+    k.t0 = static_cast<int>(a0 - o0);
+    k.s0 = static_cast<int>(b0 - o0);
+  } else {
+    runs.push_back({a0, a1});
+    runs.push_back({b0, b1});
+    k.t0 = 0;
+    k.s0 = k.nt;
+  }
+  for (const auto& r : runs) k.n += r.second - r.first;
+  k.ids.resize(size_t(k.n));
+  int64_t at = 0;
+  for (const auto& r : runs) {
+    if (r.second > r.first)
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(k.ids.data() + at, c.bins.perm.p + r.first, size_t(r.second - r.first) * 4,
+                                      cudaMemcpyDeviceToHost, c.stream));
+    at += r.second - r.first;
+  }
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  std::vector<double4> hp(size_t(k.n));
+  for (int64_t i = 0; i < k.n; ++i) {
+    const size_t id = size_t(k.ids[size_t(i)]);
+    hp[size_t(i)] = make_double4(xyz[3 * id], xyz[3 * id + 1], xyz[3 * id + 2], q[id]);
+  }
+  if (k.n) SSUM_CUDA_CHECK(cudaMemcpy(c.pts.p, hp.data(), hp.size() * sizeof(double4), cudaMemcpyHostToDevice));
+  return k;
+}
+
+// fitted value sum_m C[m, d] B_m(beta_t(x)) at the compact targets (add_fitted_value,
+// treecode.cpp:143-155); runtime degree (this is not the tree code's hot loop)
+__global__ void k_ix_down(const double4* __restrict__ pts, int t0, int nt, const double* __restrict__ cramer_t,
+                          const double* __restrict__ coeff, int degree, int D, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nt) return;
+  const int P = (degree + 1) * (degree + 2) / 2;
+  const double4 x = pts[t0 + k];
+  double b1, b2, b3;
+  bary(cramer_t, x.x, x.y, x.z, b1, b2, b3);
+  double p1[kMaxDegree + 1], p2[kMaxDegree + 1], p3[kMaxDegree + 1];
+  p1[0] = p2[0] = p3[0] = 1.0;
+  for (int e = 1; e <= degree; ++e) {
+    p1[e] = p1[e - 1] * b1;
+    p2[e] = p2[e - 1] * b2;
+    p3[e] = p3[e - 1] * b3;
+  }
+  double val[3] = {0.0, 0.0, 0.0};
+  int m = 0;
+  for (int kk = 0; kk <= degree; ++kk)
+    for (int jj = 0; jj <= degree - kk; ++jj, ++m) {
+      const double B = p1[degree - kk - jj] * p2[jj] * p3[kk];
+      for (int d = 0; d < D; ++d) val[d] = fma(coeff[d * P + m], B, val[d]);
+    }
+  for (int d = 0; d < D; ++d) out[size_t(k) * D + d] = val[d];
+}
+
+// raw PP / PC sums of the compact targets: x X S (Biot-Savart) or -S / (4 pi)
+__global__ void k_ix_raw(const double4* __restrict__ pts, int t0, int nt, const double* __restrict__ S, int D,
+                         double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nt) return;
+  const double* s = S + size_t(t0 + k) * D;
+  if (D == 3) {
+    const double4 x = pts[t0 + k];
+    out[3 * size_t(k)] = x.y * s[2] - x.z * s[1];
+    out[3 * size_t(k) + 1] = x.z * s[0] - x.x * s[2];
+    out[3 * size_t(k) + 2] = x.x * s[1] - x.y * s[0];
+  } else {
+    out[k] = -kInv4Pi * s[0];
+  }
+}
+
+// Upward pass of one node over compact [s0, s0 + ns): chunks, partial sums,
+// then w_hat into the proxy points at pts[base ..) or, with raw, w into raw.
+// ix_ints must hold [0] = 0 (weight node 0 -> slot 0).
+void ix_upward(Ctx& c, int degree, int sdev, int s0, int ns, int64_t base, double* raw) {
+  const int P = (degree + 1) * (degree + 2) / 2;
+  std::vector<int4> ch;
+  for (int b = 0; b < ns; b += kUpChunk) ch.push_back(make_int4(sdev, s0 + b, std::min(kUpChunk, ns - b), 0));
+  const int nch = static_cast<int>(ch.size());
+  c.wchunks.ensure(size_t(nch) + 2);
+  c.wpart.ensure(size_t(std::max(nch, 1)) * P);
+  // chunk table, then (count, (0, count)) for launch_up_partial / k_up_final
+  ch.push_back(make_int4(nch, 0, nch, 0));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.wchunks.p, ch.data(), ch.size() * sizeof(int4), cudaMemcpyHostToDevice, c.stream));
+  const int* d_cnt = reinterpret_cast<const int*>(c.wchunks.p + nch);
+  const int2* d_range = reinterpret_cast<const int2*>(reinterpret_cast<const int*>(c.wchunks.p + nch) + 1);
+  if (nch > 0) launch_up_partial(c, c.stream, degree, nch, d_cnt);
+  const int bt = ((P + 31) / 32) * 32;
+  k_up_final<<<1, bt, size_t(P) * 8, c.stream>>>(c.ix_ints.p, 1, d_range, c.wpart.p, c.vinv.p, P, c.ix_ints.p, base,
+                                                  c.pts.p, raw);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+}
+
+}  // namespace
+
+void eval_interaction(Ctx& c, int kernel, int degree, const double* xyz, const double* q, int target, int source,
+                      int kind, double* field) {
+  const int D = kernel == kBS ? 3 : 1;
+  const int P = (degree + 1) * (degree + 2) / 2;
+  if (kind != 0) ensure_vinv(c, degree);
+  c.pts.ensure(size_t(c.bins.n) + 2 * size_t(P) + 1);
+  const Compact k = pack_bins(c, xyz, q, target, source);
+  if (k.nt == 0 || k.ns == 0) return;  // an empty bin contributes nothing
+  const int64_t n = k.n;
+  c.S.ensure(size_t(n + 2 * P) * D);
+  c.coeff.ensure(size_t(D) * P);
+  c.ix_out.ensure(size_t(k.nt) * D);
+  c.ix_ints.ensure(8);
+  const int hi[8] = {0, source, target, 0, 0, 0, 0, 0};
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.ix_ints.p, hi, sizeof(hi), cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
+  const int bs = 128;
+  if (kind != 0) {  // proxy points of the source (slot 0) and the target (slot 1)
+    k_proxy<<<grid_for(2 * P, bs), bs, 0, c.stream>>>(c.ix_ints.p + 1, 2, degree, c.nodes.tri.p, n, c.pts.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  if (kind == 1 || kind == 3) ix_upward(c, degree, source, k.s0, k.ns, n, nullptr);  // w_hat at pts[n, n + P)
+  // one range per interaction: PP / CP read the source bin, PC / CC its proxies
+  const bool from_bin = kind == 0 || kind == 2;
+  const SrcRange r{from_bin ? k.s0 : static_cast<int>(n), from_bin ? k.ns : P, kind == 0 ? 1 : 0, 0};
+  c.ix_range.ensure(1);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.ix_range.p, &r, sizeof(r), cudaMemcpyHostToDevice, c.stream));
+  if (kind == 0 || kind == 1) {
+    const int ntile = (k.nt + kTileTargets - 1) / kTileTargets;
+    std::vector<Tile> tl(static_cast<size_t>(ntile));
+    for (int j = 0; j < ntile; ++j) {
+      Tile& t = tl[size_t(j)];
+      t.tgt_begin = k.t0 + j * kTileTargets;
+      t.tgt_count = std::min(kTileTargets, k.nt - j * kTileTargets);
+      t.list_begin = 0;
+      t.list_end = 1;
+      t.near_total = kind == 0 ? k.ns : 0;
+      t.self_shift = -k.s0;  // point j of the bin sits at flattened position j - s0
+      t.has_self = (kind == 0 && k.nested) ? 1 : 0;
+      t.total = r.count;
+    }
+    c.ix_tiles.ensure(tl.size());
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.ix_tiles.p, tl.data(), tl.size() * sizeof(Tile), cudaMemcpyHostToDevice,
+                                    c.stream));
+    launch_leaf_tiles(c, c.stream, kernel, c.ix_tiles.p, ntile, c.ix_range.p, c.S.p);
+    SSUM_LAUNCH_CHECK();
+    k_ix_raw<<<grid_for(k.nt, bs), bs, 0, c.stream>>>(c.pts.p, k.t0, k.nt, c.S.p, D, c.ix_out.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches += 2;
+  } else {
+    // phi at the target's proxy points (slot 1), C = V^-1 phi into coeff slot 0
+    Tile t{static_cast<int>(n + P), P, 0, 1, 0, 0, 0, r.count};
+    c.ix_tiles.ensure(1);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.ix_tiles.p, &t, sizeof(t), cudaMemcpyHostToDevice, c.stream));
+    launch_fit_tiles_on(c, c.stream, kernel, P, c.ix_tiles.p, 1, nullptr, c.ix_range.p, c.ix_ints.p, c.ix_ints.p,
+                        c.coeff.p);
+    SSUM_LAUNCH_CHECK();
+    k_ix_down<<<grid_for(k.nt, bs), bs, 0, c.stream>>>(c.pts.p, k.t0, k.nt, c.nodes.cramer.p + 12 * size_t(target),
+                                                        c.coeff.p, degree, D, c.ix_out.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches += 2;
+  }
+  check_flags(c, "eval_interaction");
+  std::vector<double> out(size_t(k.nt) * D);
+  SSUM_CUDA_CHECK(cudaMemcpy(out.data(), c.ix_out.p, out.size() * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < k.nt; ++i) {
+    double* f = field + size_t(k.ids[size_t(k.t0 + i)]) * D;
+    for (int d = 0; d < D; ++d) f[d] += out[size_t(i) * D + d];
+  }
+}
+
+void proxy_weights(Ctx& c, int degree, const double* xyz, const double* q, int node, double* w) {
+  const int P = (degree + 1) * (degree + 2) / 2;
+  c.pts.ensure(size_t(c.bins.n) + 1);
+  const Compact k = pack_bins(c, xyz, q, node, node);
+  c.ix_out.ensure(size_t(P));
+  c.ix_ints.ensure(8);
+  const int hi[8] = {0, node, node, 0, 0, 0, 0, 0};
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.ix_ints.p, hi, sizeof(hi), cudaMemcpyHostToDevice, c.stream));
+  ix_upward(c, degree, node, k.s0, k.ns, 0, c.ix_out.p);
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(w, c.ix_out.p, size_t(P) * 8, cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 
 }  // namespace ssum

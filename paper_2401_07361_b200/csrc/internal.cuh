@@ -227,9 +227,25 @@ struct TravScratch {
   long long* h_plan = nullptr;  // pinned read-back
 };
 
+// Host-made MAC decisions for node pairs inside the guard band around theta
+// (traversal.cu MacCtl / resolve_mac). Keys: t << 33 | s << 1 | well, sorted.
+// Valid for one theta; node ids persist with the geometry (reset: cleared).
+struct MacGuard {
+  static constexpr int kAmbCap = 4096;
+  double band = 1e-12;  // relative half-width (SSUM_MAC_BAND overrides, tests)
+  double theta = -1.0;
+  std::vector<unsigned long long> keys;
+  DBuf<unsigned long long> d_keys;
+  DBuf<int2> amb;
+  DBuf<int> amb_n;
+  DBuf<unsigned char> ctl;  // device copy of this traversal's MacCtl
+  int64_t resolved = 0;  // pairs decided on the host so far
+};
+
 struct Ctx {
   int device = 0;
   TravScratch trav;
+  MacGuard mac;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   std::string last_error;
@@ -269,6 +285,12 @@ struct Ctx {
   DBuf<Tile> direct_tiles;
   DBuf<SrcRange> direct_range;
   DBuf<double> rk_state;             // RK4 scratch
+  double last_rcond = 0.0;           // reciprocal condition of the last ConditioningError
+  // per-interaction scratch (eval_interaction / proxy_weights)
+  DBuf<Tile> ix_tiles;
+  DBuf<SrcRange> ix_range;
+  DBuf<int> ix_ints;
+  DBuf<double> ix_out;
   cudaEvent_t ev[8];
   // The fit tiles (CP/CC+fit) run on side_stream (highest priority)
   // concurrently with the leaf tiles (PP+PC): both only read pts and write
@@ -338,6 +360,17 @@ void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
 void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel);
+// k_tiles<fit> over explicit tiles / ranges (fit node k -> coeff slot pslot[fit_nodes[k]])
+void launch_fit_tiles_on(Ctx& c, cudaStream_t stream, int kernel, int P, const Tile* tiles, int nfit, const int* sel,
+                        const SrcRange* ranges, const int* fit_nodes, const int* pslot, double* coeff);
+// Per-interaction entry points (eval.cu): eval_pp/pc/cp/cc and
+// compute_proxy_weights on the bins of the last binning, O(|t| |s|).
+void eval_interaction(Ctx& c, int kernel, int degree, const double* xyz, const double* q, int target, int source,
+                      int kind, double* field);
+void proxy_weights(Ctx& c, int degree, const double* xyz, const double* q, int node, double* w);
+// V^-1 of the degree-d lattice Vandermonde (row-major, P x P) and its exact
+// 1-norm reciprocal condition number (no throw; eval.cu)
+void lattice_inverse(int degree, std::vector<double>& inv, double& rcond);
 void start_prep(Ctx& c);
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct = false);

@@ -1,6 +1,8 @@
 // Interaction tiles: the PP + PC (leaf) and CP + CC + fit (fit node) passes
 // and the direct sum, all on one kernel shape (k_tiles). Kept in its own
 // translation unit so tuning builds (make variants) recompile only this file.
+#include <atomic>
+
 #include "kernels.cuh"
 
 namespace ssum {
@@ -430,36 +432,45 @@ constexpr size_t tile_smem() {
   return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap + sizeof(double2) * kLogTabN;
 }
 
-// k_tiles instantiation with its dynamic shared-memory limit raised once
-// (per process; every context's device is an sm_100a part)
+// k_tiles instantiation with its dynamic shared-memory limit raised. The
+// attribute belongs to the device (context), not the process: a per-device
+// bit records where it is set, so a context on a second device raises it
+// there too before its first launch.
 template <int KER, int MODE, int NTH, int CHUNK, int MINB>
-auto tiles_kernel() {
-  static const bool ready = [] {
+auto tiles_kernel(int device) {
+  static std::atomic<unsigned long long> ready{0};
+  const unsigned long long bit = 1ull << (device & 63);
+  if (!(ready.load(std::memory_order_acquire) & bit)) {
     SSUM_CUDA_CHECK(cudaFuncSetAttribute(k_tiles<KER, MODE, NTH, CHUNK, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(tile_smem<CHUNK>())));
-    return true;
-  }();
-  (void)ready;
+    ready.fetch_or(bit, std::memory_order_acq_rel);
+  }
   return k_tiles<KER, MODE, NTH, CHUNK, MINB>;
 }
 
 }  // namespace
 
+void launch_fit_tiles_on(Ctx& c, cudaStream_t stream, int kernel, int P, const Tile* tiles, int nfit, const int* sel,
+                        const SrcRange* ranges, const int* fit_nodes, const int* pslot, double* coeff) {
+  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device)
+                          : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device);
+  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), stream>>>(tiles, nfit, sel, ranges, c.pts.p, nullptr, c.d_flags.p,
+                                                           fit_nodes, pslot, c.vinv.p, P, coeff);
+}
+
 void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel) {
   Lists& L = c.lists;
-  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>()
-                          : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>();
-  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), stream>>>(L.fit_tiles.p, nfit, sel, L.fit_ranges.p, c.pts.p, nullptr,
-                                                 c.d_flags.p, L.fit_nodes.p, L.pslot.p, c.vinv.p, P, c.coeff.p);
+  launch_fit_tiles_on(c, stream, kernel, P, L.fit_tiles.p, nfit, sel, L.fit_ranges.p, L.fit_nodes.p, L.pslot.p,
+                      c.coeff.p);
 }
 
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct) {
-  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>()
-                                   : tiles_kernel<kLOG, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>())
-                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>()
-                                   : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>());
+  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device)
+                                   : tiles_kernel<kLOG, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device))
+                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device)
+                                   : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device));
   k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
                                                 nullptr, nullptr, 0, nullptr);
 }

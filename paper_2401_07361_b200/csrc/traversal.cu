@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 
 #include "internal.cuh"
 
@@ -48,6 +49,41 @@ __device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_o
   return k;
 }
 
+// MAC decisions exact by construction. R and the radii come from CUDA's
+// atan2 (<= 2 ulp) where the reference uses glibc's (< 1 ulp), so the
+// quotient (r_t + r_s)/R may differ from the reference's by a few ulp
+// (<= ~1e-15 relative). A decision can therefore differ only when the quotient
+// lies that close to theta. Every pair whose device quotient falls in the
+// guard band theta (1 +- band) (band = 1e-12 by default, ~5000 ulp) is looked
+// up in a table of host-made decisions; a pair missing from it is recorded,
+// takes the device decision provisionally, and the traversal is redone once
+// the host (glibc atan2, the reference's expressions: great_circle_distance,
+// triangle_radius, mac_well_separated, treecode.cpp:22-25) has decided it
+// (resolve_mac below). Outside the band the device decision is the
+// reference's; inside it the host's is.
+struct MacCtl {
+  const unsigned long long* keys;  // sorted (t << 33 | s << 1 | well)
+  int n;
+  double lo, hi;                   // theta (1 - band), theta (1 + band)
+  int2* amb;                       // undecided pairs (first amb_cap)
+  int* amb_n;
+  int amb_cap;
+};
+
+__device__ __noinline__ bool mac_lookup(const MacCtl& m, int t, int s, bool provisional) {
+  const unsigned long long k = (static_cast<unsigned long long>(t) << 33) | (static_cast<unsigned long long>(s) << 1);
+  int lo = 0, hi = m.n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((m.keys[mid] | 1ull) < k) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < m.n && (m.keys[lo] >> 1) == (k >> 1)) return (m.keys[lo] & 1ull) != 0;
+  const int i = atomicAdd(m.amb_n, 1);
+  if (i < m.amb_cap) m.amb[i] = make_int2(t, s);
+  return provisional;
+}
+
 // action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
 // [rlo, rhi): the tree-position range whose targets this call evaluates
 // (restricted multi-part call; [0, INT_MAX) otherwise): a pair whose target
@@ -56,14 +92,20 @@ __device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__
                                            int rlo, int rhi, const double* __restrict__ center,
                                            const double* __restrict__ radius, const int* __restrict__ level,
                                            const int* __restrict__ child_base, double theta, int thr, int max_depth,
-                                           int pc_only) {
+                                           int pc_only, const MacCtl* __restrict__ mac) {
   const int ct = cnt[t], cs = cnt[s];
   int a = 0;
   if (ct > 0 && cs > 0 && off[t] < rhi && off[t] + ct > rlo) {
     const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
     const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
     const double R = arc_dist(a3, b3);
-    if (R > 0.0 && div_rn(add_rn(radius[t], radius[s]), R) < theta) {
+    bool well = false;
+    if (R > 0.0) {
+      const double qv = div_rn(add_rn(radius[t], radius[s]), R);
+      well = qv < theta;
+      if (qv > __ldg(&mac->lo) && qv < __ldg(&mac->hi)) well = mac_lookup(*mac, t, s, well);
+    }
+    if (well) {
       a = 4 | classify_kind(ct, cs, thr, pc_only);
     } else if (ct <= thr && cs <= thr) {
       a = 4;  // PP
@@ -113,7 +155,7 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
                             const int* __restrict__ off, int rlo, int rhi, const double* __restrict__ center,
                             const double* __restrict__ radius,
                             const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr,
-                            int max_depth, int pc_only, int* __restrict__ action,
+                            int max_depth, int pc_only, const MacCtl* mac, int* __restrict__ action,
                             unsigned long long* __restrict__ packed) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > m) return;
@@ -122,7 +164,7 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
     return;
   }
   const int a = pair_action(F[k].t, F[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
-                            max_depth, pc_only);
+                            max_depth, pc_only, mac);
   action[k] = a;
   packed[k] = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
 }
@@ -167,7 +209,7 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
     k_bfs(const int* __restrict__ cnt, const int* __restrict__ off, int rlo, int rhi,
           const double* __restrict__ center, const double* __restrict__ radius,
           const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr, int max_depth,
-          int pc_only, PairEntry* F0, PairEntry* F1, int fcap, int4* __restrict__ E,
+          int pc_only, const MacCtl* mac, PairEntry* F0, PairEntry* F1, int fcap, int4* __restrict__ E,
           unsigned long long* __restrict__ K, long long ecap, int* __restrict__ action,
           unsigned long long* __restrict__ loc, unsigned long long* btot, int* out, long long* ne_out,
           int* flags) {
@@ -193,7 +235,7 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
 #pragma unroll 4
     for (int k = lo + tid; k < hi; k += kBfsThreads)
       action[k] = pair_action(Fc[k].t, Fc[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
-                              max_depth, pc_only);
+                              max_depth, pc_only, mac);
     for (int base = lo; base < hi; base += kBfsThreads) {
       const int k = base + tid;
       unsigned long long v = 0;
@@ -618,6 +660,90 @@ void exclusive_scan(Ctx& c, const T* in, T* out, int64_t n) {
 
 static TravScratch& scratch(Ctx& c) { return c.trav; }
 
+// Guard-band control for this traversal (see MacCtl); the undecided-pair
+// counter is reset here, on the stream, before the traversal kernels.
+static const MacCtl* mac_ctl(Ctx& c) {
+  MacGuard& g = c.mac;
+  g.amb.ensure(size_t(MacGuard::kAmbCap));
+  g.amb_n.ensure(1);
+  g.ctl.ensure(sizeof(MacCtl));
+  if (!g.d_keys.p) g.d_keys.ensure(1);
+  MacCtl m;
+  m.keys = g.d_keys.p;
+  m.n = static_cast<int>(g.keys.size());
+  m.lo = g.theta * (1.0 - g.band);
+  m.hi = g.theta * (1.0 + g.band);
+  m.amb = g.amb.p;
+  m.amb_n = g.amb_n.p;
+  m.amb_cap = MacGuard::kAmbCap;
+  // pageable source: staged before the call returns, so m may go out of scope
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(g.ctl.p, &m, sizeof(m), cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaMemsetAsync(g.amb_n.p, 0, sizeof(int), c.stream));
+  return reinterpret_cast<const MacCtl*>(g.ctl.p);
+}
+
+// mac_well_separated (treecode.cpp:22-25) on the host, with the reference's
+// expressions and glibc's atan2: great_circle_distance (geometry.cpp:55-57),
+// radius = great_circle_distance(circumcenter, v1) (face_tree.hpp:23-24).
+// Node geometry (circumcentre, v1) is bit-identical to the reference's.
+static bool host_mac(const double* ct, const double* v1t, const double* cs, const double* v1s, double theta) {
+  auto gcd = [](const double* a, const double* b) {
+    const double cx = a[1] * b[2] - a[2] * b[1], cy = a[2] * b[0] - a[0] * b[2], cz = a[0] * b[1] - a[1] * b[0];
+    return std::atan2(std::sqrt(cx * cx + cy * cy + cz * cz), a[0] * b[0] + a[1] * b[1] + a[2] * b[2]);
+  };
+  const double r = gcd(ct, cs);
+  return r > 0.0 && (gcd(ct, v1t) + gcd(cs, v1s)) / r < theta;
+}
+
+// After a traversal: decide the pairs it met inside the guard band on the
+// host, add them to the table and report whether the traversal must be
+// redone (a provisional decision may have differed).
+static bool resolve_mac(Ctx& c) {
+  MacGuard& g = c.mac;
+  int namb = 0;
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(&namb, g.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  if (namb == 0) return false;
+  const int m = std::min(namb, static_cast<int>(MacGuard::kAmbCap));
+  std::vector<int2> pairs(static_cast<size_t>(m));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(pairs.data(), g.amb.p, size_t(m) * sizeof(int2), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  // node geometry: a few pairs fetch their nodes one by one, many fetch the table
+  std::vector<double> all_c, all_t;
+  if (m > 64) {
+    const size_t nn = size_t(c.nodes.count);
+    all_c.resize(3 * nn);
+    all_t.resize(9 * nn);
+    SSUM_CUDA_CHECK(cudaMemcpy(all_c.data(), c.nodes.center.p, all_c.size() * 8, cudaMemcpyDeviceToHost));
+    SSUM_CUDA_CHECK(cudaMemcpy(all_t.data(), c.nodes.tri.p, all_t.size() * 8, cudaMemcpyDeviceToHost));
+  }
+  auto geom = [&](int id, double* ctr, double* v1) {
+    if (!all_c.empty()) {
+      std::copy(all_c.begin() + 3 * size_t(id), all_c.begin() + 3 * size_t(id) + 3, ctr);
+      std::copy(all_t.begin() + 9 * size_t(id), all_t.begin() + 9 * size_t(id) + 3, v1);
+      return;
+    }
+    SSUM_CUDA_CHECK(cudaMemcpy(ctr, c.nodes.center.p + 3 * size_t(id), 24, cudaMemcpyDeviceToHost));
+    SSUM_CUDA_CHECK(cudaMemcpy(v1, c.nodes.tri.p + 9 * size_t(id), 24, cudaMemcpyDeviceToHost));
+  };
+  for (const int2 p : pairs) {
+    double ct[3], v1t[3], cs[3], v1s[3];
+    geom(p.x, ct, v1t);
+    geom(p.y, cs, v1s);
+    const bool well = host_mac(ct, v1t, cs, v1s, g.theta);
+    g.keys.push_back((static_cast<unsigned long long>(p.x) << 33) | (static_cast<unsigned long long>(p.y) << 1) |
+                     (well ? 1ull : 0ull));
+  }
+  std::sort(g.keys.begin(), g.keys.end());
+  g.keys.erase(std::unique(g.keys.begin(), g.keys.end(),
+                           [](unsigned long long a, unsigned long long b) { return (a >> 1) == (b >> 1); }),
+               g.keys.end());
+  g.d_keys.ensure(g.keys.size());
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(g.d_keys.p, g.keys.data(), g.keys.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  g.resolved += m;
+  return true;
+}
+
 // Breadth-first traversal with one host read per step (the frontier size
 // sizes the next step). Records the step sizes as the plan for the next call.
 static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
@@ -636,6 +762,7 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
   L.inter.ensure(1 << 16);
   L.key.ensure(1 << 16);
   S.plan_m.clear();
+  const MacCtl* mac = mac_ctl(c);
   while (m > 0) {
     S.plan_m.push_back(m);
     S.action.ensure(size_t(m) + 1);
@@ -644,8 +771,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
     k_trav_eval<<<grid_for(m + 1, bs), bs, 0, c.stream>>>(S.F0.p, m, B.cnt.p, B.off.p, rlo, rhi, c.nodes.center.p,
                                                            c.nodes.radius.p,
                                                            c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
-                                                           cfg.n_threshold, cfg.max_depth, cfg.pc_only, S.action.p,
-                                                           S.packed.p);
+                                                           cfg.n_threshold, cfg.max_depth, cfg.pc_only, mac,
+                                                           S.action.p, S.packed.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     exclusive_scan(c, S.packed.p, S.scan.p, m + 1);  // packed[m] = 0: totals at scan[m]
@@ -715,6 +842,7 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   const int *level = c.nodes.level.p, *child_base = c.nodes.child_base.p;
   double theta = cfg.theta;
   int thr = cfg.n_threshold, max_depth = cfg.max_depth, pc_only = cfg.pc_only;
+  const MacCtl* mac = mac_ctl(c);
   PairEntry *f0 = S.F0.p, *f1 = S.F1.p;
   int4* e = L.inter.p;
   unsigned long long* k = L.key.p;
@@ -724,7 +852,7 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   long long* ne = S.debase.p;
   int* flags = c.d_flags.p;
   void* args[] = {&cnt, &off, &rlo, &rhi, &center, &radius, &level, &child_base, &theta, &thr, &max_depth,
-                  &pc_only, &f0, &f1,
+                  &pc_only, &mac, &f0, &f1,
                   &fcap, &e, &k, &ecap, &action, &loc, &btot, &out, &ne, &flags};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs), dim3(nb), dim3(kBfsThreads), args, 0, c.stream) !=
       cudaSuccess) {
@@ -759,7 +887,16 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
   // ---- breadth-first traversal
   long long ne = 0;
   if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
-  if (!bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+  MacGuard& g = c.mac;
+  if (g.theta != cfg.theta) {  // host decisions are per theta (node ids persist with the geometry)
+    g.keys.clear();
+    g.theta = cfg.theta;
+  }
+  for (int round = 0;; ++round) {
+    if (!bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+    if (!resolve_mac(c)) break;
+    if (round > 64) throw Error(SSUM_INTERNAL, "dual traversal: MAC guard band did not settle");
+  }
   L.n_inter = ne;
   trace().mark("trav.bfs");
   build_lists(c, cfg);

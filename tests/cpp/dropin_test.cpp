@@ -66,6 +66,32 @@ int main(int argc, char** argv) {
     }
   put(fo, field.data()->data(), n * 3);
 
+  // compute_proxy_weights of root face 0 (degree 4) on the tree as binned by
+  // the calls above; the SBB API: lattice_fit rcond, constant reproduction by
+  // fit_coefficients / interpolant_eval, the degree-16 conditioning guard
+  {
+    const std::vector<double> w = compute_proxy_weights(tree, 0, SBBBasis(4), pts, q);
+    put(fo, w.data(), w.size());
+    const double rc8 = lattice_fit(8).rcond();
+    put(fo, &rc8, 1);
+    const TreeNode& nd = tree.node(0);
+    const SphericalTriangle tri(nd.triangle.v1, nd.triangle.v2, nd.triangle.v3);
+    const ProxyPointSet pp8 = proxy_points(tri, 8);
+    const SBBInterpolant f = fit_coefficients(pp8, std::vector<double>(pp8.points.size(), 2.5));
+    const double at = interpolant_eval(f, triangle_circumcenter(tri)) - 2.5;
+    put(fo, &at, 1);
+    double rc16 = -1.0;
+    try {
+      lattice_fit(16);
+    } catch (const ConditioningError& e) {
+      rc16 = e.rcond;
+    }
+    put(fo, &rc16, 1);
+    const double geo[3] = {double(triangle_contains(tri, triangle_circumcenter(tri))),
+                           triangle_radius(tri) - nd.radius, great_circle_distance(nd.circumcenter, tri.v1)};
+    put(fo, geo, 3);
+  }
+
   ParticleState st{pts, std::vector<double>(n), area};
   for (size_t i = 0; i < n; ++i) {  // RH4 vorticity from q = zeta * A
     st.zeta[i] = q[i] / area[i];

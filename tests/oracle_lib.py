@@ -195,6 +195,14 @@ class RefTree:
         _check(lib.ref_eval_interaction(self.h, kernel, _p(xyz), _p(q), xyz.shape[0], theta, nt, degree, max_depth,
                                         int(target), int(source), int(kind), _p(field)))
 
+    def proxy_weights(self, degree, xyz, q, node):
+        """compute_proxy_weights (treecode.cpp:79-91) of one node."""
+        lib = ref()
+        lib.ref_compute_proxy_weights.argtypes = [_P, ctypes.c_int, _P, _P, _I64, ctypes.c_int, _P]
+        w = np.zeros((degree + 1) * (degree + 2) // 2)
+        _check(lib.ref_compute_proxy_weights(self.h, degree, _p(xyz), _p(q), xyz.shape[0], int(node), _p(w)))
+        return w
+
     def treecode(self, kernel, xyz, q, theta, nt, degree, max_depth=10, workers=1):
         n = xyz.shape[0]
         d = 3 if kernel == 0 else 1

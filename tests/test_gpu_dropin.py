@@ -1,5 +1,6 @@
 """The C++ drop-in (include/spheresum_b200/spheresum.hpp, libspheresum_dropin.so)
 driven the way a reference caller drives spheresum:: — tests/cpp/dropin_test.cpp."""
+import ctypes
 import os
 import subprocess
 
@@ -42,9 +43,26 @@ def test_cpp_dropin_matches_reference(tmp_path):
     lst = take(3 * cnt).reshape(cnt, 3).astype(np.int32)
     sizes = take(20)
     pp = take(3 * n).reshape(n, 3)
+    w = take(15)
+    rc8 = take(1)[0]
+    const_err = take(1)[0]
+    rc16 = take(1)[0]
+    geo = take(3)
     x = take(3 * n).reshape(n, 3)
     z = take(n)
     assert o == v.size
+    # compute_proxy_weights vs the reference on its own tree of the same input
+    xyz, _ = ol.mesh(3)
+    t = ol.RefTree()
+    t.bin(xyz, 8, 10)
+    wr = t.proxy_weights(4, xyz, g["l3_q"], 0)
+    assert np.abs(w - wr).max() <= 1e-13 * np.abs(wr).max()
+    rcr = ctypes.c_double()
+    ol.ref().ref_lattice_fit_rcond(8, ctypes.byref(rcr))
+    assert abs(rc8 - rcr.value) <= 1e-8 * rcr.value  # exact 1-norm rcond, both
+    assert abs(const_err) < 1e-12
+    assert 0.0 <= rc16 <= 1e-12  # ConditioningError carries rcond (errors.hpp:22-27)
+    assert geo[0] == 1.0 and geo[1] == 0.0 and geo[2] > 0
     assert ol.rel_l2(u, g["l3_u_tree"]) < 1e-10
     assert ol.rel_l2(psi, g["l3_psi_tree"]) < 1e-10
     assert ol.rel_l2(ud, g["l3_u_direct"]) < 1e-13

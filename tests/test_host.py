@@ -123,3 +123,46 @@ def test_random_cap_policy_removes_duplicates(ss):
     if len(pairs):
         den = 1.0 - np.einsum("ij,ij->i", x[pairs[:, 0]], x[pairs[:, 1]])
         assert (den > 1e-12).all()
+
+
+# --------------------------------------------------- SBB host entry points
+@pytest.mark.parametrize("deg", [1, 4, 8, 12])
+def test_lattice_fit_matches_reference(ss, ol, deg):  # sbb.cpp:74-138
+    """V^-1 and rcond of the lattice Vandermonde (the matrix the tree code's
+    fit and V^-T transforms apply) against the reference's ProxyFit."""
+    import ctypes
+
+    inv, rc = ss.lattice_fit(deg)
+    p = ss.sbb_basis_size(deg)
+    ref = np.zeros(p * p)
+    assert ol.ref().ref_lattice_inverse(deg, ol._p(ref)) == 0
+    ref = ref.reshape(p, p).T  # column-major solve of I
+    assert np.abs(inv - ref).max() <= 1e-12 * np.abs(ref).max()
+    rcr = ctypes.c_double()
+    assert ol.ref().ref_lattice_fit_rcond(deg, ctypes.byref(rcr)) == 0
+    assert abs(rc - rcr.value) <= 1e-8 * rcr.value
+
+
+def test_lattice_fit_conditioning_error_carries_rcond(ss):  # sbb.cpp:89-93, errors.hpp:22-27
+    with pytest.raises(ss.ConditioningError) as e:
+        ss.lattice_fit(16)
+    assert 0.0 <= e.value.rcond <= 1e-12
+    with pytest.raises(ValueError):
+        ss.lattice_fit(21)
+
+
+@pytest.mark.parametrize("deg", [2, 4, 8])
+def test_proxy_points_bit_identical(ss, ol, deg):  # sbb.cpp:46-66
+    rng = np.random.default_rng(deg)
+    # vertices whose UnitVector3 renormalisation (inside the reference helper)
+    # is the identity, so both sides see the same bits
+    tri = np.array([[1.0, 0.0, 0.0], [0.6, 0.8, 0.0], [0.0, 0.6, 0.8]])
+    assert np.array_equal(np.sqrt(tri[:, 0] * tri[:, 0] + tri[:, 1] * tri[:, 1] + tri[:, 2] * tri[:, 2]), np.ones(3))
+    mine = ss.proxy_points(tri, deg)
+    ref = np.zeros((ss.sbb_basis_size(deg), 3))
+    assert ol.ref().ref_proxy_points(ol._p(np.ascontiguousarray(tri)), deg, ol._p(ref)) == 0
+    assert np.array_equal(mine, ref)
+    b = ss.SBBBasis(deg)
+    assert b.size() == ss.sbb_basis_size(deg)
+    vals = b.eval(rng.dirichlet([1, 1, 1]))
+    assert vals.shape == (b.size(),) and np.isfinite(vals).all()
