@@ -856,11 +856,11 @@ void ix_upward(Ctx& c, int degree, int sdev, int s0, int ns, int64_t base, doubl
   const int nch = static_cast<int>(ch.size());
   c.wchunks.ensure(size_t(nch) + 2);
   c.wpart.ensure(size_t(std::max(nch, 1)) * P);
-  // chunk table, then (count, (0, count)) for launch_up_partial / k_up_final
-  ch.push_back(make_int4(nch, 0, nch, 0));
+  // chunk table, then (count, pad, (0, count)) for launch_up_partial / k_up_final
+  ch.push_back(make_int4(nch, 0, 0, nch));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.wchunks.p, ch.data(), ch.size() * sizeof(int4), cudaMemcpyHostToDevice, c.stream));
   const int* d_cnt = reinterpret_cast<const int*>(c.wchunks.p + nch);
-  const int2* d_range = reinterpret_cast<const int2*>(reinterpret_cast<const int*>(c.wchunks.p + nch) + 1);
+  const int2* d_range = reinterpret_cast<const int2*>(reinterpret_cast<const int*>(c.wchunks.p + nch) + 2);
   if (nch > 0) launch_up_partial(c, c.stream, degree, nch, d_cnt);
   const int bt = ((P + 31) / 32) * 32;
   k_up_final<<<1, bt, size_t(P) * 8, c.stream>>>(c.ix_ints.p, 1, d_range, c.wpart.p, c.vinv.p, P, c.ix_ints.p, base,
