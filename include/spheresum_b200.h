@@ -176,6 +176,14 @@ int ssum_partition_range(ssum_ctx* ctx, int64_t* begin, int64_t* end);
 /* Copy the last binning's permutation (tree position -> caller's particle
  * index, N ints) into dst, a device pointer if on_device != 0. */
 int ssum_tree_perm(ssum_ctx* ctx, int* dst, int on_device);
+/* Every part's tree-position range in the last evaluation: nparts + 1
+ * positions (part r = [cuts[r], cuts[r+1])). The ranks bin identically, so
+ * every rank gets the same table without communicating. */
+int ssum_partition_cuts(ssum_ctx* ctx, int64_t* cuts);
+/* Device-pointer evaluations write this part's rows in tree order (position
+ * p0 + r to row r, rows past p1 - p0 untouched) instead of the caller's order
+ * over all N rows: the rows one all-gather exchanges (tree_order = 1). */
+int ssum_set_output_order(ssum_ctx* ctx, int tree_order);
 
 /* ---- Lagrangian RK4 (absent from the reference code) ---- */
 /* In place on host arrays: xyz (N x 3), zeta (N); area (N) fixed. Each stage
@@ -199,6 +207,14 @@ int ssum_rk4_stage_end(ssum_ctx* ctx, int stage, double omega, int64_t n, const 
                        double* d_k, double* d_kz, double* d_acc, double* d_accz);
 int ssum_rk4_step_end(ssum_ctx* ctx, double dt, int64_t n, double* d_x0, double* d_z0,
                       const double* d_acc, const double* d_accz);
+/* stage_end on the all-gathered rows of a partitioned evaluation (SURVEY.md
+ * §8(e)/(f) rank 2): d_rows holds nparts slots of `width` rows x 3, slot r =
+ * part r's rows in tree order (ssum_set_output_order(ctx, 1)), exactly what one
+ * ncclAllGather of equal slots leaves on every rank; the stage kernel reads
+ * them through the binning's permutation. Bitwise ssum_rk4_stage_end on the
+ * assembled field. */
+int ssum_rk4_stage_end_rows(ssum_ctx* ctx, int stage, double omega, int64_t n, const double* d_rows,
+                            int64_t width, double* d_k, double* d_kz, double* d_acc, double* d_accz);
 
 /* ---- measurement --------------------------------------------------------- */
 /* FP64 roofline denominator: DFMA-chain throughput of this device in TFLOP/s

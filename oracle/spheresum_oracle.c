@@ -749,3 +749,184 @@ int orc_build_lists(const double* xyz, int64_t n, double theta, int nt, int max_
   free(P);
   return g_status;
 }
+
+/* ------------------------------------------------------------------ fixtures
+ * The BASELINE.json inputs for bench.py's reference arm, which must not load
+ * the product library: the RH4 vorticity (config 1/2/4/5) and the config-3
+ * random cap generator, restated here from their definitions in BASELINE.json
+ * (the product's host generators, paper_2401_07361_b200/csrc/workloads.cpp,
+ * implement the same definitions; tests/test_host.py checks the two agree bit
+ * for bit). The mesh itself comes from the reference (ref_make_mesh). */
+
+/* zeta = 2 sin(lat) - 30 sin(lat) cos^4(lat) cos(4 lon); lat = asin(clamp z),
+ * lon = atan2(y, x) in [-pi, pi) (unit_to_latlon, geometry.cpp:46-53). */
+int orc_rh4_vorticity(const double* xyz, int64_t n, double* zeta) {
+  for (int64_t i = 0; i < n; ++i) {
+    double z = xyz[3 * i + 2];
+    if (z > 1.0) z = 1.0;
+    if (z < -1.0) z = -1.0;
+    const double lat = asin(z);
+    double lon = atan2(xyz[3 * i + 1], xyz[3 * i]);
+    if (lon >= M_PI) lon -= 2.0 * M_PI;
+    const double st = sin(lat), ct = cos(lat);
+    zeta[i] = 2.0 * st - 30.0 * st * ct * ct * ct * ct * cos(4.0 * lon);
+  }
+  return ORC_OK;
+}
+
+/* splitmix64 seeding of xoshiro256** (Vigna / Blackman, public domain);
+ * doubles from the top 53 bits. */
+typedef struct {
+  uint64_t s[4];
+} orc_rng;
+static uint64_t orc_splitmix(uint64_t* x) {
+  uint64_t z = (*x += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t orc_rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+static uint64_t orc_next(orc_rng* r) {
+  uint64_t* s = r->s;
+  const uint64_t out = orc_rotl(s[1] * 5, 7) * 9;
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = orc_rotl(s[3], 45);
+  return out;
+}
+static double orc_u01(orc_rng* r) { return (double)(orc_next(r) >> 11) * 0x1.0p-53; }
+static double orc_u01_open(orc_rng* r) { return ((double)(orc_next(r) >> 11) + 0.5) * 0x1.0p-53; }
+static double orc_normal(orc_rng* r) { /* Box-Muller, one value per call */
+  const double u1 = orc_u01_open(r), u2 = orc_u01(r);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+}
+
+/* half the points: normalised i.i.d. N(0,1)^3; the other half uniform in area
+ * on the 10-degree cap about x0 = (lat 40, lon 0): z' ~ U[cos 10, 1], azimuth
+ * ~ U[0, 2 pi) in the frame (north, east, x0) at x0 */
+static v3 orc_draw(orc_rng* r, int in_cap) {
+  if (!in_cap) {
+    for (;;) {
+      const double x = orc_normal(r), y = orc_normal(r), z = orc_normal(r);
+      if (x * x + y * y + z * z > 1e-20) return unitv(x, y, z);
+    }
+  }
+  const double c10 = cos(10.0 * M_PI / 180.0);
+  const double zp = c10 + (1.0 - c10) * orc_u01(r);
+  const double ph = 2.0 * M_PI * orc_u01(r);
+  const double q = 1.0 - zp * zp;
+  const double rp = sqrt(q > 0.0 ? q : 0.0);
+  const double lat0 = 40.0 * M_PI / 180.0;
+  const v3 e3 = latlon_unit(lat0, 0.0);
+  const v3 e1 = {-sin(lat0), 0.0, cos(lat0)};
+  const v3 e2 = {0.0, 1.0, 0.0};
+  const double a = rp * cos(ph), b = rp * sin(ph);
+  return unitv(a * e1.x + b * e2.x + zp * e3.x, a * e1.y + b * e2.y + zp * e3.y, a * e1.z + b * e2.z + zp * e3.z);
+}
+
+typedef struct {
+  int64_t key, idx;
+} orc_cell;
+static int orc_cell_cmp(const void* a, const void* b) {
+  const orc_cell* x = (const orc_cell*)a;
+  const orc_cell* y = (const orc_cell*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* near-duplicate policy: flag every j with 1 - x_i.x_j <= 1e-12 (reference
+ * rounding) against some i < j, found through a uniform grid of 2^-19 cells */
+static int64_t orc_near_dups(const v3* p, int64_t n, char* bad) {
+  const double h = 1.0 / (1 << 19);
+  orc_cell* ks = (orc_cell*)malloc((size_t)n * sizeof(orc_cell));
+  if (!ks) return -1;
+#define ORC_CELL(v) ((int64_t)floor(((v) + 1.0) / h))
+#define ORC_KEY(a, b, c) (((a) << 42) | ((b) << 21) | (c))
+  for (int64_t i = 0; i < n; ++i) {
+    ks[i].key = ORC_KEY(ORC_CELL(p[i].x), ORC_CELL(p[i].y), ORC_CELL(p[i].z));
+    ks[i].idx = i;
+  }
+  qsort(ks, (size_t)n, sizeof(orc_cell), orc_cell_cmp);
+  memset(bad, 0, (size_t)n);
+  int64_t nbad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const v3 x = p[i];
+    const int64_t cx = ORC_CELL(x.x), cy = ORC_CELL(x.y), cz = ORC_CELL(x.z);
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int64_t k = ORC_KEY(cx + dx, cy + dy, cz + dz);
+          int64_t lo = 0, hi = n;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (ks[mid].key < k) lo = mid + 1;
+            else hi = mid;
+          }
+          for (; lo < n && ks[lo].key == k; ++lo) {
+            const int64_t j = ks[lo].idx;
+            if (j <= i) continue;
+            const v3 y = p[j];
+            const double den = 1.0 - ((x.x * y.x + x.y * y.y) + x.z * y.z);
+            if (den <= 1e-12 && !bad[j]) {
+              bad[j] = 1;
+              ++nbad;
+            }
+          }
+        }
+  }
+#undef ORC_CELL
+#undef ORC_KEY
+  free(ks);
+  return nbad;
+}
+
+/* BASELINE config 3: xyz (n x 3), zeta = exp(-16 (1 - x.x0)) minus its
+ * weighted mean, area = 4 pi / n. */
+int orc_make_random_cap(int64_t n, uint64_t seed, double* xyz, double* zeta, double* area) {
+  if (n < 2) return ORC_CONFIG;
+  orc_rng r;
+  for (int k = 0; k < 4; ++k) r.s[k] = orc_splitmix(&seed);
+  const int64_t half = n / 2;
+  v3* p = (v3*)malloc((size_t)n * sizeof(v3));
+  char* bad = (char*)malloc((size_t)n);
+  if (!p || !bad) {
+    free(p);
+    free(bad);
+    return ORC_NOMEM;
+  }
+  for (int64_t i = 0; i < n; ++i) p[i] = orc_draw(&r, i >= half);
+  int rc = ORC_OK;
+  for (int round = 0; round < 64; ++round) {
+    const int64_t nb = orc_near_dups(p, n, bad);
+    if (nb < 0) {
+      rc = ORC_NOMEM;
+      break;
+    }
+    if (nb == 0) break;
+    for (int64_t j = 0; j < n; ++j)
+      if (bad[j]) p[j] = orc_draw(&r, j >= half);
+    if (round == 63) rc = ORC_GEOMETRY;
+  }
+  if (rc == ORC_OK) {
+    const v3 x0 = latlon_unit(40.0 * M_PI / 180.0, 0.0);
+    const double a = 4.0 * M_PI / (double)n;
+    double circ = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      xyz[3 * i] = p[i].x;
+      xyz[3 * i + 1] = p[i].y;
+      xyz[3 * i + 2] = p[i].z;
+      zeta[i] = exp(-16.0 * (1.0 - v3dot(p[i], x0)));
+      area[i] = a;
+      circ += zeta[i] * a;
+    }
+    const double mean = circ / (4.0 * M_PI);
+    for (int64_t i = 0; i < n; ++i) zeta[i] -= mean;
+  }
+  free(p);
+  free(bad);
+  return rc;
+}

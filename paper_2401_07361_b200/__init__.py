@@ -119,7 +119,7 @@ EXPORTED_SYMBOLS = (
     "ssum_make_random_cap", "ssum_fp64_peak", "ssum_probe_log_far", "ssum_set_partition", "ssum_partition_range",
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
     "ssum_rk4_step_end", "ssum_compute_proxy_weights", "ssum_last_rcond", "ssum_lattice_fit",
-    "ssum_proxy_points",
+    "ssum_proxy_points", "ssum_partition_cuts", "ssum_set_output_order", "ssum_rk4_stage_end_rows",
 )
 
 
@@ -170,6 +170,9 @@ def load_library():
         "ssum_last_rcond": (ctypes.c_double, [_P]),
         "ssum_lattice_fit": (ctypes.c_int, [ctypes.c_int, _P, _P]),
         "ssum_proxy_points": (ctypes.c_int, [_P, ctypes.c_int, _P]),
+        "ssum_partition_cuts": (ctypes.c_int, [_P, _P]),
+        "ssum_set_output_order": (ctypes.c_int, [_P, ctypes.c_int]),
+        "ssum_rk4_stage_end_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64, _P, _I64] + [_P] * 4),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -389,11 +392,32 @@ class FaceTree:
         """Compute only part `part` of `nparts` cost-balanced target ranges
         (multi-GPU strong scaling); see include/spheresum_b200.h."""
         self._check(self._lib.ssum_set_partition(self._h, int(part), int(nparts)))
+        self._nparts = int(nparts)
 
     def partition_range(self) -> Tuple[int, int]:
         b, e = _I64(), _I64()
         self._check(self._lib.ssum_partition_range(self._h, ctypes.byref(b), ctypes.byref(e)))
         return b.value, e.value
+
+    def partition_cuts(self) -> np.ndarray:
+        """Every part's tree-position range of the last evaluation (nparts + 1
+        positions); identical on every rank."""
+        out = np.zeros(getattr(self, "_nparts", 1) + 1, np.int64)
+        self._check(self._lib.ssum_partition_cuts(self._h, _ptr(out)))
+        return out
+
+    def set_output_order(self, tree_order: bool) -> None:
+        """Device evaluations write this part's rows in tree order (row r =
+        tree position p0 + r) instead of the caller's order."""
+        self._check(self._lib.ssum_set_output_order(self._h, 1 if tree_order else 0))
+
+    def rk4_stage_end_rows(self, stage: int, omega: float, n: int, rows: int, width: int, k: int, kz: int,
+                           acc: int, accz: int) -> None:
+        """rk4_stage_end with u read from the all-gathered tree-order slots of
+        every part (device pointers; see ssum_rk4_stage_end_rows)."""
+        v = ctypes.c_void_p
+        self._check(self._lib.ssum_rk4_stage_end_rows(self._h, int(stage), float(omega), int(n), v(rows),
+                                                      int(width), v(k), v(kz), v(acc), v(accz)))
 
     def perm(self, device_ptr: Optional[int] = None) -> Optional[np.ndarray]:
         """Tree position -> particle index of the last binning (host copy, or

@@ -255,6 +255,37 @@ __global__ void k_rk4_accum(int64_t n, int stage, double omega, const double* __
   accz[i] = stage == 0 ? kzv : add_rn(accz[i], mul_rn(w, kzv));
 }
 
+// k_rk4_accum with u read from the all-gathered tree-order rows of every
+// part (slot r of width W holds part r's positions [cuts[r], cuts[r+1]));
+// one thread per tree position j, particle perm[j]. Same arithmetic, so a
+// driver built on it reproduces ssum_rk4 bit for bit.
+__global__ void k_rk4_accum_rows(int64_t n, int stage, double omega, const double* __restrict__ rows, int64_t W,
+                                 const long long* __restrict__ cuts, int np, const int* __restrict__ perm,
+                                 double* __restrict__ k, double* __restrict__ kz, double* __restrict__ acc,
+                                 double* __restrict__ accz) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int lo = 0, hi = np - 1;  // the part holding j: last r with cuts[r] <= j
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cuts[mid] <= j)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const double* u = rows + 3 * (lo * W + (j - cuts[lo]));
+  const int64_t i = perm[j];
+  const double w = (stage == 1 || stage == 2) ? 2.0 : 1.0;
+  const double kzv = mul_rn(mul_rn(-2.0, omega), u[2]);
+  for (int d = 0; d < 3; ++d) {
+    const double v = u[d];
+    k[3 * i + d] = v;
+    acc[3 * i + d] = stage == 0 ? v : add_rn(acc[3 * i + d], mul_rn(w, v));
+  }
+  kz[i] = kzv;
+  accz[i] = stage == 0 ? kzv : add_rn(accz[i], mul_rn(w, kzv));
+}
+
 __global__ void k_rk4_final(int64_t n, double h6, double* __restrict__ x0, double* __restrict__ z0,
                             const double* __restrict__ acc, const double* __restrict__ accz, int* flags) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -711,6 +742,39 @@ int ssum_rk4_stage_end(ssum_ctx* h, int stage, double omega, int64_t n, const do
     if (stage < 0 || stage > 3) throw Error(SSUM_INVALID, "RK4 stage must be 0..3");
     if (n == 0) return;
     k_rk4_accum<<<grid_for(n, 256), 256, 0, c.stream>>>(n, stage, omega, d_u, d_k, d_kz, d_acc, d_accz);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  });
+}
+
+int ssum_set_output_order(ssum_ctx* h, int tree_order) {
+  return guarded(h, [&](Ctx& c) { c.out_tree_order = tree_order != 0; });
+}
+
+int ssum_partition_cuts(ssum_ctx* h, int64_t* cuts) {
+  return guarded(h, [&](Ctx& c) {
+    if (c.part_pos.empty()) throw Error(SSUM_INVALID, "partition_cuts: no evaluation yet");
+    for (size_t r = 0; r < c.part_pos.size(); ++r) cuts[r] = c.part_pos[r];
+  });
+}
+
+int ssum_rk4_stage_end_rows(ssum_ctx* h, int stage, double omega, int64_t n, const double* d_rows, int64_t width,
+                            double* d_k, double* d_kz, double* d_acc, double* d_accz) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (stage < 0 || stage > 3) throw Error(SSUM_INVALID, "RK4 stage must be 0..3");
+    if (n == 0) return;
+    if (n != c.bins.n || int64_t(c.part_pos.size()) != c.nparts + 1 || c.part_pos.back() != n)
+      throw Error(SSUM_INVALID, "rk4_stage_end_rows: no partitioned evaluation of these particles");
+    const int np = c.nparts;
+    for (int r = 0; r < np; ++r)
+      if (c.part_pos[size_t(r) + 1] - c.part_pos[size_t(r)] > width)
+        throw Error(SSUM_INVALID, "rk4_stage_end_rows: a part has more rows than the slot width");
+    c.cut_dev.ensure(size_t(np) + 1);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.cut_dev.p, c.part_pos.data(), (size_t(np) + 1) * 8, cudaMemcpyHostToDevice,
+                                    c.stream));
+    k_rk4_accum_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(n, stage, omega, d_rows, width, c.cut_dev.p, np,
+                                                             c.bins.perm.p, d_k, d_kz, d_acc, d_accz);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   });

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
     int64_t p0, int64_t p1, const double4* __restrict__ pts, const double* __restrict__ S,
     const int* __restrict__ pos_leaf, const int* __restrict__ parent, const int* __restrict__ pslot,
     const unsigned char* __restrict__ is_fit, const double* __restrict__ cramer, const double* __restrict__ coeff,
-    const int* __restrict__ perm, double* __restrict__ out) {
+    const int* __restrict__ perm, double* __restrict__ out, int64_t obase) {
   constexpr int D = KDim<KER>::D;
   constexpr int P = Sbb<DEG>::P;
   constexpr int DP = D == 3 ? 4 : 1;  // staged row: (c_0, c_1, c_2, pad) per basis function
@@ -330,7 +330,8 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
     a = a >= 0 ? parent[a] : -1;
   }
   if (!valid) return;
-  const int64_t o = perm ? perm[k] : k;  // no perm: tree order (in place over S is safe: own row only)
+  // no perm: tree order from obase (in place over S, obase 0, is safe: own row only)
+  const int64_t o = perm ? perm[k] : k - obase;
   if constexpr (KER == kBS) {
     const double s0 = S[3 * k], s1 = S[3 * k + 1], s2 = S[3 * k + 2];
     const double pref = -kInv4Pi;  // BiotSavartKernel::prefactor (kernels.hpp:54)
@@ -361,10 +362,10 @@ __global__ void k_inv_perm(const int* __restrict__ perm, int64_t n, int* __restr
 
 // inv: finish caller-order rows [i0, i1) (per-lane k_finish); otherwise the
 // part's tree positions with k_finish_tree, written to d_out in caller order
-// (perm) or, with tree_order, in tree order.
+// (perm) or, with tree_order, in tree order: position k to row k - obase.
 template <int KER>
 void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, int64_t i0 = 0, int64_t i1 = 0,
-                   bool tree_order = false) {
+                   bool tree_order = false, int64_t obase = 0) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   const int bs = 128;
@@ -380,7 +381,7 @@ void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, 
     else                                                                                                      \
       k_finish_tree<KER, DG><<<grid_for(n, 32 * kFinWarps), 32 * kFinWarps, 0, c.stream>>>(                   \
           L.p0, L.p1, c.pts.p, c.S.p, B.pos_leaf.p, c.nodes.parent.p, L.pslot.p, L.is_fit.p, c.nodes.cramer.p, \
-          c.coeff.p, tree_order ? nullptr : B.perm.p, d_out);                                                 \
+          c.coeff.p, tree_order ? nullptr : B.perm.p, d_out, obase);                                          \
     break;
   switch (degree) {
     SSUM_FINISH_CASE(1) SSUM_FINISH_CASE(2) SSUM_FINISH_CASE(3) SSUM_FINISH_CASE(4) SSUM_FINISH_CASE(5)
@@ -706,6 +707,13 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
                                         cudaMemcpyDeviceToHost, c.copy_stream));
     }
     SSUM_CUDA_CHECK(cudaEventRecord(c.io.t1, c.copy_stream));
+  } else if (c.out_tree_order) {
+    // this part's rows in tree order: position p0 + r -> row r (the rows
+    // one multi-GPU all-gather exchanges, dist.py)
+    if (kernel == kBS)
+      launch_finish<kBS>(c, degree, d_out, nullptr, 0, 0, true, L.p0);
+    else
+      launch_finish<kLOG>(c, degree, d_out, nullptr, 0, 0, true, L.p0);
   } else if (kernel == kBS) {
     launch_finish<kBS>(c, degree, d_out);
   } else {

@@ -260,6 +260,13 @@ struct Ctx {
     int nparts = 0;
     std::vector<int64_t> pos;  // nparts + 1 tree positions
   } cuts;
+  // every part's tree-position range in the last evaluation (nparts + 1
+  // positions; {0, N} unpartitioned) — identical on every rank, so each rank
+  // can place every other rank's rows without communication
+  std::vector<int64_t> part_pos;
+  DBuf<long long> snap;      // k_snap_cuts output
+  DBuf<long long> cut_dev;   // part_pos on the device (ssum_rk4_stage_end_rows)
+  bool out_tree_order = false;  // device results: this part's rows in tree order (ssum_set_output_order)
   bool restrict_on = false;
   int64_t rp0 = 0, rp1 = 0;
   int rl0 = 0, rl1 = 0;

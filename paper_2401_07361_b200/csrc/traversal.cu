@@ -1091,11 +1091,13 @@ void finalize_counts(Ctx& c) {
 }
 
 // First leaf (depth-first index) starting at or after tree position x, for
-// the two cut positions of this part: [0] p0, [1] p1, [2] l0, [3] l1.
+// every cut position x = pos[r] (r = 0 .. m-1): out[r] its tree position,
+// out[m + r] its leaf index.
 __global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* __restrict__ off, long long n,
-                            long long x0, long long x1, long long* out) {
-  if (threadIdx.x >= 2) return;
-  const long long x = threadIdx.x == 0 ? x0 : x1;
+                            const long long* __restrict__ pos, int m, long long* out) {
+  const int r = threadIdx.x;
+  if (r >= m) return;
+  const long long x = pos[r];
   int lo = 0, hi = nl;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
@@ -1104,8 +1106,8 @@ __global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* _
     else
       hi = mid;
   }
-  out[threadIdx.x] = lo < nl ? off[leaves[lo]] : n;
-  out[2 + threadIdx.x] = lo;
+  out[r] = lo < nl ? off[leaves[lo]] : n;
+  out[m + r] = lo;
 }
 
 // Restricted multi-part call: once a full multi-part call has placed the
@@ -1114,23 +1116,30 @@ __global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* _
 // traverse / build lists for this part's targets only. The lists of a target
 // are the same pairs in the same order as in the full traversal (dropping
 // pairs keeps the relative emission order), so the union of the parts stays
-// bitwise the single-part result.
+// bitwise the single-part result. Every part's snapped range is kept
+// (Ctx::part_pos): all ranks bin identically, so all agree on it.
 bool plan_restriction(Ctx& c) {
   c.restrict_on = false;
   const Binned& B = c.bins;
+  c.part_pos.assign({0, B.n});
   if (c.nparts <= 1 || c.cuts.n != B.n || c.cuts.nparts != c.nparts || B.n_leaves == 0) return false;
-  long long* d_out = reinterpret_cast<long long*>(c.d_flags.p + 40);  // ints [40, 48)
-  k_snap_cuts<<<1, 32, 0, c.stream>>>(B.d_leaves.p, B.n_leaves, B.off.p, B.n, c.cuts.pos[size_t(c.part)],
-                                      c.cuts.pos[size_t(c.part) + 1], d_out);
+  const int m = c.nparts + 1;
+  c.snap.ensure(size_t(3 * m));
+  std::vector<long long> h(size_t(2 * m));
+  for (int r = 0; r < m; ++r) h[size_t(r)] = c.cuts.pos[size_t(r)];
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.snap.p + 2 * m, h.data(), size_t(m) * 8, cudaMemcpyHostToDevice, c.stream));
+  k_snap_cuts<<<1, ((m + 31) / 32) * 32, 0, c.stream>>>(B.d_leaves.p, B.n_leaves, B.off.p, B.n, c.snap.p + 2 * m, m,
+                                                        c.snap.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
-  long long h[4];
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h.data(), c.snap.p, size_t(2 * m) * 8, cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-  c.rp0 = h[0];
-  c.rp1 = h[1];
-  c.rl0 = static_cast<int>(h[2]);
-  c.rl1 = static_cast<int>(h[3]);
+  c.part_pos.assign(h.begin(), h.begin() + m);
+  c.part_pos.front() = 0;
+  c.rp0 = h[size_t(c.part)];
+  c.rp1 = h[size_t(c.part) + 1];
+  c.rl0 = static_cast<int>(h[size_t(m + c.part)]);
+  c.rl1 = static_cast<int>(h[size_t(m + c.part) + 1]);
   c.restrict_on = true;
   return true;
 }
@@ -1209,6 +1218,8 @@ void partition_targets(Ctx& c) {
     const int ct = std::min(cut(r), nt);
     c.cuts.pos[size_t(r)] = ct < nt ? tiles[size_t(ct)].tgt_begin : N;
   }
+  c.cuts.pos.front() = 0;
+  c.part_pos = c.cuts.pos;
   std::vector<int> fit_nodes(static_cast<size_t>(L.n_fit_tiles));
   if (L.n_fit_tiles > 0) {
     SSUM_CUDA_CHECK(cudaMemcpyAsync(fit_nodes.data(), L.fit_nodes.p, fit_nodes.size() * 4, cudaMemcpyDeviceToHost, c.stream));

@@ -3,10 +3,19 @@
 The tree code shards by TARGETS: every rank bins and
 traverses the full (replicated) particle set, then evaluates only its
 cost-balanced contiguous range of target leaves (FaceTree.set_partition).
-The one exchange step is this all-gather of the rows each rank computed, so
-every rank holds the full velocity field (e.g. before the next RK4 stage).
-Rows travel in tree order (contiguous per rank); each rank scatters them back
-to the caller's particle order with the shared permutation.
+Every rank bins identically, so every rank knows every part's tree-position
+range without communicating (FaceTree.partition_cuts).
+
+The one exchange per RK4 stage (§8(f) rank 2) is fused into the stage
+update: each rank's evaluation writes its rows in TREE order straight into
+a slot (FaceTree.set_output_order), ONE all-gather of equal-width slots
+(ncclAllGather under NCCL) leaves every part's rows on every rank, and the
+stage kernel (ssum_rk4_stage_end_rows) reads them there through the
+binning's permutation — no scatter, no index tensors, no per-rank sizes on
+the wire.
+
+`gather_partitioned_rows` / `gather_rows` remain for single evaluations in
+the caller's order (bench.py's non-RK4 configs).
 """
 from __future__ import annotations
 
@@ -16,12 +25,48 @@ import torch
 import torch.distributed as dist
 
 
+def _ws(group=None) -> int:
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
+def slot_width(cuts) -> int:
+    """Equal slot width for the row all-gather: the widest part."""
+    return max(int(cuts[r + 1]) - int(cuts[r]) for r in range(len(cuts) - 1))
+
+
+def exchange_rows(slot: torch.Tensor, rows: torch.Tensor, width: int,
+                  group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
+    """All-gather equal slots: slot[:width] (this rank's rows, tree order) to
+    rows[r * width:(r + 1) * width] for every rank r. One collective."""
+    ws = _ws(group)
+    if ws == 1:
+        return slot
+    out = rows[: ws * width]
+    if out.is_cuda:
+        dist.all_gather_into_tensor(out, slot[:width], group=group)
+    else:  # gloo
+        parts = [torch.empty_like(slot[:width]) for _ in range(ws)]
+        dist.all_gather(parts, slot[:width].contiguous(), group=group)
+        out.copy_(torch.cat(parts))
+    return out
+
+
+def assemble_rows(rows: torch.Tensor, width: int, cuts, perm: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out[perm[j]] = the row of tree position j in the all-gathered slots —
+    what ssum_rk4_stage_end_rows reads on the device (tests and CPU drivers)."""
+    for r in range(len(cuts) - 1):
+        a, b = int(cuts[r]), int(cuts[r + 1])
+        if b > a:
+            out[perm[a:b].long()] = rows[r * width:r * width + (b - a)]
+    return out
+
+
 def gather_partitioned_rows(out: torch.Tensor, perm: torch.Tensor, p0: int, p1: int,
                             group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
-    """out: (N, D) with valid rows perm[p0:p1] on this rank; returns `out`
-    with every rank's rows filled in. Works for NCCL (CUDA tensors) and gloo
-    (CPU tensors)."""
-    ws = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    """out: (N, D) in the caller's order with valid rows perm[p0:p1] on this
+    rank; returns `out` with every rank's rows filled in (single evaluations
+    in the caller's order). Works for NCCL (CUDA tensors) and gloo (CPU)."""
+    ws = _ws(group)
     if ws == 1:
         return out
     dev = out.device
@@ -59,7 +104,7 @@ def allgather_inputs(h_xyz: torch.Tensor, h_q: torch.Tensor, d_xyz: torch.Tensor
     and d_q (>= ws*m,) with m = ceil(N / ws): rows [0, N) receive the
     inputs; rows past N are padding."""
     n = h_xyz.shape[0]
-    ws = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    ws = _ws(group)
     if ws == 1:
         d_xyz[:n].copy_(h_xyz, non_blocking=True)
         d_q[:n].copy_(h_q, non_blocking=True)
@@ -87,7 +132,8 @@ def _all_gather_slots(buf: torch.Tensor, slot: torch.Tensor, ws: int, group) -> 
 
 
 def gather_rows(tree, out: torch.Tensor, group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
-    """All-gather the last partitioned evaluation of `tree` into `out` (device)."""
+    """All-gather the last partitioned evaluation of `tree` into `out` (device,
+    caller's order)."""
     p0, p1 = tree.partition_range()
     n = out.shape[0]
     perm = torch.empty(n, dtype=torch.int32, device=out.device)
@@ -97,53 +143,67 @@ def gather_rows(tree, out: torch.Tensor, group: Optional[dist.ProcessGroup] = No
 
 # ------------------------------------------------------------------ RK4
 class TreecodeRK4Ops:
-    """Stage operations of the multi-GPU RK4 on one FaceTree (this rank's
-    GPU): the RK4 arithmetic runs through ssum_rk4_stage_* (the kernels of
-    ssum_rk4), the stage velocity is this rank's partitioned tree-code
-    evaluation followed by the row all-gather (one exchange
-    per stage)."""
+    """Stage operations of the (multi-GPU) RK4 on one FaceTree (this rank's
+    GPU, on torch's current stream): ssum_rk4_stage_begin, this rank's
+    partitioned tree-code evaluation written in tree order into its slot,
+    one all-gather of the slots, ssum_rk4_stage_end_rows on the gathered
+    rows, and ssum_rk4_step_end — the kernels of ssum_rk4, so one rank
+    reproduces it bit for bit and G ranks reproduce one rank bit for bit.
+    `stats`: a list that receives each evaluation's TreecodeStats."""
 
-    def __init__(self, tree, cfg, group: Optional[dist.ProcessGroup] = None):
-        from . import BiotSavartKernel, treecode_sum_device
+    def __init__(self, tree, cfg, group: Optional[dist.ProcessGroup] = None, stats: Optional[list] = None):
+        from . import BiotSavartKernel, TreecodeStats, treecode_sum_device
 
-        self.tree, self.cfg, self.group = tree, cfg, group
-        self._k, self._eval = BiotSavartKernel, treecode_sum_device
+        self.tree, self.cfg, self.group, self.stats = tree, cfg, group, stats
+        self._k, self._eval, self._stats = BiotSavartKernel, treecode_sum_device, TreecodeStats
+        self.ws = _ws(group)
+        tree.set_stream(torch.cuda.current_stream().cuda_stream)
+        tree.set_output_order(True)
+        if self.ws > 1:
+            tree.set_partition(dist.get_rank(group), self.ws)
 
-    def stage_begin(self, s: int, dt: float, st: dict) -> None:
+    def state(self, x: torch.Tensor, zeta: torch.Tensor, area: torch.Tensor) -> dict:
+        n = x.shape[0]
+        st = {"n": n, "x0": x, "z0": zeta, "area": area, "xs": torch.empty_like(x), "q": torch.empty_like(zeta),
+              "k": torch.zeros_like(x), "kz": torch.zeros_like(zeta), "acc": torch.zeros_like(x),
+              "accz": torch.zeros_like(zeta), "slot": torch.zeros_like(x)}
+        st["rows"] = torch.zeros((self.ws * n, 3), dtype=x.dtype, device=x.device) if self.ws > 1 else st["slot"]
+        return st
+
+    def stage(self, s: int, dt: float, omega: float, st: dict) -> int:
         n = st["n"]
-        self.tree.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
-                                  st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
+        t = self.tree
+        t.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
+                          st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
+        stats = self._stats()
+        self._eval(t, self._k, self.cfg, st["xs"].data_ptr(), st["q"].data_ptr(), n, st["slot"].data_ptr(),
+                   stats=stats)
+        if self.stats is not None:
+            self.stats.append(stats)
+        cuts = t.partition_cuts()
+        width = slot_width(cuts) if self.ws > 1 else n
+        rows = exchange_rows(st["slot"], st["rows"], width, self.group)
+        t.rk4_stage_end_rows(s, omega, n, rows.data_ptr(), width, st["k"].data_ptr(), st["kz"].data_ptr(),
+                             st["acc"].data_ptr(), st["accz"].data_ptr())
+        return stats.gpu_launches + 2
 
-    def velocity(self, st: dict) -> None:
-        n = st["n"]
-        st["u"].zero_()
-        self._eval(self.tree, self._k, self.cfg, st["xs"].data_ptr(), st["q"].data_ptr(), n, st["u"].data_ptr())
-        gather_rows(self.tree, st["u"], self.group)
-
-    def stage_end(self, s: int, omega: float, st: dict) -> None:
-        self.tree.rk4_stage_end(s, omega, st["n"], st["u"].data_ptr(), st["k"].data_ptr(), st["kz"].data_ptr(),
-                                st["acc"].data_ptr(), st["accz"].data_ptr())
-
-    def step_end(self, dt: float, st: dict) -> None:
+    def step(self, dt: float, st: dict, omega: float = 2.0 * 3.141592653589793) -> int:
+        """One RK4 step in place on st["x0"], st["z0"]; returns our kernel launches."""
+        launches = 0
+        for s in range(4):
+            launches += self.stage(s, dt, omega, st)
         self.tree.rk4_step_end(dt, st["n"], st["x0"].data_ptr(), st["z0"].data_ptr(), st["acc"].data_ptr(),
                                st["accz"].data_ptr())
+        return launches + 1
 
 
 def rk4_distributed(x: torch.Tensor, zeta: torch.Tensor, area: torch.Tensor, dt: float, steps: int, ops,
                     omega: float = 2.0 * 3.141592653589793):
-    """Lagrangian RK4 of the BVE with the stage velocities
-    from `ops.velocity` (every rank ends each stage holding all N rows). x
-    (N, 3), zeta (N), area (N) are replicated on every rank and advanced in
-    place; returns (x, zeta). With TreecodeRK4Ops on one rank this is
-    ssum_rk4 bit for bit."""
-    n = x.shape[0]
-    st = {"n": n, "x0": x, "z0": zeta, "area": area, "xs": torch.empty_like(x), "q": torch.empty_like(zeta),
-          "u": torch.zeros_like(x), "k": torch.zeros_like(x), "kz": torch.zeros_like(zeta),
-          "acc": torch.zeros_like(x), "accz": torch.zeros_like(zeta)}
+    """Lagrangian RK4 of the BVE with `ops` (TreecodeRK4Ops
+    or a CPU stand-in with the same protocol). x (N, 3), zeta (N), area (N)
+    are replicated on every rank and advanced in place; returns (x, zeta).
+    With TreecodeRK4Ops on one rank this is ssum_rk4 bit for bit."""
+    st = ops.state(x, zeta, area)
     for _ in range(steps):
-        for s in range(4):
-            ops.stage_begin(s, dt, st)
-            ops.velocity(st)
-            ops.stage_end(s, omega, st)
-        ops.step_end(dt, st)
+        ops.step(dt, st, omega)
     return x, zeta

@@ -120,6 +120,26 @@ def ref_direct(kernel: int, xyz, q):
     return out
 
 
+def orc_rh4(xyz):
+    """BASELINE RH4 vorticity (oracle C restatement; glibc)."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    z = np.zeros(xyz.shape[0])
+    orc().orc_rh4_vorticity.argtypes = [_P, _I64, _P]
+    orc().orc_rh4_vorticity(_p(xyz), xyz.shape[0], _p(z))
+    return z
+
+
+def orc_random_cap(n: int, seed: int):
+    """BASELINE config-3 point set (xyz, zeta, area), oracle restatement."""
+    lib = orc()
+    lib.orc_make_random_cap.argtypes = [_I64, ctypes.c_uint64, _P, _P, _P]
+    xyz, z, a = np.zeros((n, 3)), np.zeros(n), np.zeros(n)
+    code = lib.orc_make_random_cap(n, seed, _p(xyz), _p(z), _p(a))
+    if code:
+        raise OracleError(code, "orc_make_random_cap failed")
+    return xyz, z, a
+
+
 def orc_treecode(kernel: int, xyz, q, theta, nt, degree, max_depth=10, pc_only=False):
     n = xyz.shape[0]
     d = 3 if kernel == 0 else 1

@@ -477,6 +477,51 @@ def test_rk4_distributed_driver_matches_rk4(ss, mesh_fixture):
     assert np.array_equal(z.cpu().numpy(), z_ref)
 
 
+@pytest.mark.parametrize("G,level", [(2, 6), (3, 6), (8, 7)])
+def test_rk4_fused_row_exchange_emulated_parts(ss, mesh_fixture, G, level):
+    """The multi-GPU stage exchange on one GPU: per stage, every part r of G
+    evaluates its targets into slot r of one buffer in tree order (as the
+    one all-gather of the ranks' slots leaves it on every rank), and
+    ssum_rk4_stage_end_rows reads the field from there. After two steps the
+    state must be ssum_rk4's bit for bit (a rank never needs another rank's
+    sizes: the cut table is computed identically everywhere)."""
+    import torch
+
+    xyz, _, a = mesh_fixture(level)
+    n = xyz.shape[0]
+    z0 = ss.rh4_vorticity(xyz)
+    c = cfg(ss, deg=6)
+    x_ref, z_ref = ss.rk4(xyz, z0, a, c, dt=0.01, steps=2, tree=ss.FaceTree())
+    dev = torch.device("cuda", 0)
+    t = ss.FaceTree(0)
+    t.set_stream(torch.cuda.current_stream().cuda_stream)
+    t.set_output_order(True)
+    f = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev)  # noqa: E731
+    x, z, ar = f(xyz.copy()), f(z0.copy()), f(a)
+    xs, q = torch.empty_like(x), torch.empty_like(z)
+    k, kz, acc, accz = torch.zeros_like(x), torch.zeros_like(z), torch.zeros_like(x), torch.zeros_like(z)
+    rows = torch.full((G * n, 3), float("nan"), dtype=torch.float64, device=dev)
+    cut_tables = []
+    for _ in range(2):
+        for s in range(4):
+            t.rk4_stage_begin(s, 0.01, n, x.data_ptr(), z.data_ptr(), ar.data_ptr(), k.data_ptr(), kz.data_ptr(),
+                              xs.data_ptr(), q.data_ptr())
+            for r in range(G):
+                t.set_partition(r, G)
+                ss.treecode_sum_device(t, ss.BiotSavartKernel, c, xs.data_ptr(), q.data_ptr(), n,
+                                       rows[r * n:].data_ptr())
+                cut_tables.append(t.partition_cuts())
+            assert all(np.array_equal(cut_tables[-1], ct) for ct in cut_tables[-G:])
+            t.rk4_stage_end_rows(s, 2 * np.pi, n, rows.data_ptr(), n, k.data_ptr(), kz.data_ptr(), acc.data_ptr(),
+                                 accz.data_ptr())
+        t.rk4_step_end(0.01, n, x.data_ptr(), z.data_ptr(), acc.data_ptr(), accz.data_ptr())
+    torch.cuda.synchronize()
+    cuts = cut_tables[-1]
+    assert cuts[0] == 0 and cuts[-1] == n and (np.diff(cuts) >= 0).all() and (np.diff(cuts) > 0).sum() >= G - 1
+    assert np.array_equal(x.cpu().numpy(), x_ref)
+    assert np.array_equal(z.cpu().numpy(), z_ref)
+
+
 def test_rk4_direct_matches_reference(ss, ol, mesh_fixture):
     xyz, _, a = mesh_fixture(3)
     z0 = ss.rh4_vorticity(xyz)

@@ -166,3 +166,16 @@ def test_proxy_points_bit_identical(ss, ol, deg):  # sbb.cpp:46-66
     assert b.size() == ss.sbb_basis_size(deg)
     vals = b.eval(rng.dirichlet([1, 1, 1]))
     assert vals.shape == (b.size(),) and np.isfinite(vals).all()
+
+
+def test_oracle_fixtures_bit_identical_to_product(ss):
+    """bench.py's reference arm builds its inputs without the product library
+    (reference mesh + the oracle's RH4 / random-cap restatements); they must
+    be the product's inputs bit for bit."""
+    xyz, _ = ol.mesh(5)
+    assert np.array_equal(ol.orc_rh4(xyz), ss.rh4_vorticity(xyz))
+    for n, seed in ((1 << 14, 5), (1 << 17, 3)):
+        a = ol.orc_random_cap(n, seed)
+        b = ss.make_random_cap(n, seed)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)

@@ -53,38 +53,41 @@ def test_gather_partitioned_rows_gloo(cuts, cols):
 
 
 class _CpuRK4Ops:
-    """CPU stand-in for dist.TreecodeRK4Ops: the same stage protocol, the
-    velocity by direct summation over this rank's slice of a fixed
-    permutation, then the row all-gather. Exercises the multi-GPU RK4 driver's
-    control flow and exchange under gloo."""
+    """CPU stand-in for dist.TreecodeRK4Ops with the same protocol: each rank
+    evaluates its contiguous range of tree positions (a fixed permutation
+    plays the binning's), writes those rows in tree order into its slot, ONE
+    all-gather of equal slots (dist.exchange_rows), then the stage update
+    reads the gathered rows through the permutation (dist.assemble_rows =
+    what ssum_rk4_stage_end_rows does on the device)."""
 
-    def __init__(self, rank, ws, perm):
-        self.rank, self.ws, self.perm = rank, ws, perm
+    def __init__(self, rank, ws, perm, cuts):
+        self.rank, self.ws, self.perm, self.cuts = rank, ws, perm, cuts
 
-    def stage_begin(self, s, dt, st):
+    def state(self, x, z, a):
+        n = x.shape[0]
+        return {"n": n, "x0": x, "z0": z, "area": a, "xs": torch.empty_like(x), "q": torch.empty_like(z),
+                "k": torch.zeros_like(x), "kz": torch.zeros_like(z), "acc": torch.zeros_like(x),
+                "accz": torch.zeros_like(z), "slot": torch.zeros_like(x), "rows": torch.zeros((self.ws * n, 3),
+                                                                                              dtype=x.dtype),
+                "u": torch.zeros_like(x)}
+
+    def stage(self, s, dt, omega, st):
+        from paper_2401_07361_b200.dist import assemble_rows, exchange_rows, slot_width
+
         cs = (0.0, 0.5 * dt, 0.5 * dt, dt)[s]
         v = st["x0"] + cs * st["k"]
         st["xs"].copy_(v / v.norm(dim=1, keepdim=True) if s else st["x0"])
         st["q"].copy_((st["z0"] + cs * st["kz"]) * st["area"])
-
-    def velocity(self, st):
-        from paper_2401_07361_b200.dist import gather_partitioned_rows
-
-        n = st["n"]
-        cuts = [n * r // self.ws for r in range(self.ws + 1)]
-        p0, p1 = cuts[self.rank], cuts[self.rank + 1]
-        st["u"].zero_()
-        rows = self.perm[p0:p1].long()
+        p0, p1 = self.cuts[self.rank], self.cuts[self.rank + 1]
+        ids = self.perm[p0:p1].long()  # this rank's targets, tree order
         x, q = st["xs"], st["q"]
-        xi = x[rows]
+        xi = x[ids]
         den = 1.0 - xi @ x.T
-        den[torch.arange(len(rows)), rows] = float("inf")  # no self pairs
-        w = q / den
-        st["u"][rows] = -torch.cross(xi, w @ x, dim=1) / (4 * torch.pi)
-        gather_partitioned_rows(st["u"], self.perm, p0, p1)
-
-    def stage_end(self, s, omega, st):
-        u = st["u"]
+        den[torch.arange(len(ids)), ids] = float("inf")  # no self pairs
+        st["slot"][: p1 - p0] = -torch.cross(xi, (q / den) @ x, dim=1) / (4 * torch.pi)
+        w = slot_width(self.cuts) if self.ws > 1 else st["n"]
+        rows = exchange_rows(st["slot"], st["rows"], w)
+        u = assemble_rows(rows, w, self.cuts, self.perm, st["u"])
         wgt = 2.0 if s in (1, 2) else 1.0
         st["k"].copy_(u)
         st["kz"].copy_(-2.0 * omega * u[:, 2])
@@ -95,13 +98,15 @@ class _CpuRK4Ops:
             st["acc"].add_(wgt * u)
             st["accz"].add_(wgt * st["kz"])
 
-    def step_end(self, dt, st):
+    def step(self, dt, st, omega):
+        for s in range(4):
+            self.stage(s, dt, omega, st)
         v = st["x0"] + dt / 6.0 * st["acc"]
         st["x0"].copy_(v / v.norm(dim=1, keepdim=True))
         st["z0"].add_(dt / 6.0 * st["accz"])
 
 
-def _rk4_worker(rank, ws, port, q):
+def _rk4_worker(rank, ws, port, q, cuts):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=ws)
@@ -114,21 +119,23 @@ def _rk4_worker(rank, ws, port, q):
         z = torch.randn(60, generator=g, dtype=torch.float64)
         a = torch.full((60,), 4 * torch.pi / 60, dtype=torch.float64)
         perm = torch.randperm(60, generator=g).to(torch.int32)
-        rk4_distributed(x, z, a, 0.01, 2, _CpuRK4Ops(rank, ws, perm))
+        rk4_distributed(x, z, a, 0.01, 2, _CpuRK4Ops(rank, ws, perm, cuts))
         q.put((rank, x.numpy().tobytes(), z.numpy().tobytes()))
     finally:
         dist.destroy_process_group()
 
 
-def test_rk4_distributed_gloo():
-    """Two ranks, each evaluating half the rows per stage and all-gathering,
-    end with the same state as one rank evaluating everything."""
+@pytest.mark.parametrize("cuts2", [[0, 23, 60], [0, 0, 60], [0, 60, 60]])
+def test_rk4_distributed_gloo(cuts2):
+    """Two ranks, each evaluating its (unequal, possibly empty) range of tree
+    positions per stage and exchanging tree-order slots, end with the same
+    state as one rank evaluating everything."""
     ctx = mp.get_context("spawn")
     outs = {}
-    for ws in (1, 2):
+    for ws, cuts in ((1, [0, 60]), (2, cuts2)):
         q = ctx.Queue()
         port = _free_port()
-        procs = [ctx.Process(target=_rk4_worker, args=(r, ws, port, q)) for r in range(ws)]
+        procs = [ctx.Process(target=_rk4_worker, args=(r, ws, port, q, cuts)) for r in range(ws)]
         for p in procs:
             p.start()
         for p in procs:
