@@ -748,14 +748,20 @@ def direct_sum_device(tree: FaceTree, kernel, xyz_ptr: int, q_ptr: int, n: int, 
 
 def rk4(positions, zeta, area, cfg: TraversalConfig, dt: float = 0.01, steps: int = 1,
         omega: float = 2.0 * np.pi, direct: bool = False, tree: Optional[FaceTree] = None,
-        stats: Optional[TreecodeStats] = None) -> Tuple[np.ndarray, np.ndarray]:
+        stats: Optional[TreecodeStats] = None, inplace: bool = False) -> Tuple[np.ndarray, np.ndarray]:
     """Lagrangian RK4 of the BVE: returns (positions, zeta)
     after `steps` steps. dzeta/dt = -2 omega u_z; positions renormalised after
-    every stage; one (reused) tree across all stages."""
+    every stage; one (reused) tree across all stages. inplace=True advances
+    the given (C-contiguous float64, e.g. pinned) arrays themselves."""
     cfg.validate()
-    p = _as_positions(positions).copy()
+    p = _as_positions(positions)
     n = p.shape[0]
-    z = _as_vector(zeta, n, "zeta").copy()
+    z = _as_vector(zeta, n, "zeta")
+    if inplace:
+        if p is not positions or z is not zeta:
+            raise ValueError("inplace rk4 needs C-contiguous float64 positions (N, 3) and zeta (N,)")
+    else:
+        p, z = p.copy(), z.copy()
     a = _as_vector(area, n, "area")
     t = tree or _default_tree()
     c = cfg._c()
