@@ -758,7 +758,8 @@ def rk4(positions, zeta, area, cfg: TraversalConfig, dt: float = 0.01, steps: in
     n = p.shape[0]
     z = _as_vector(zeta, n, "zeta")
     if inplace:
-        if p is not positions or z is not zeta:
+        same = lambda a, b: isinstance(b, np.ndarray) and a.ctypes.data == b.ctypes.data  # noqa: E731
+        if not (same(p, positions) and same(z, zeta)):
             raise ValueError("inplace rk4 needs C-contiguous float64 positions (N, 3) and zeta (N,)")
     else:
         p, z = p.copy(), z.copy()

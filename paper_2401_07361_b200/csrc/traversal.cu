@@ -1181,9 +1181,46 @@ void partition_targets(Ctx& c) {
   std::vector<ulonglong2> fcost(static_cast<size_t>(std::max(L.n_fit_tiles, 0)));
   if (L.n_fit_tiles > 0)
     SSUM_CUDA_CHECK(cudaMemcpyAsync(fcost.data(), L.fit_cost.p, fcost.size() * sizeof(ulonglong2), cudaMemcpyDeviceToHost, c.stream));
+  std::vector<int> fit_nodes(static_cast<size_t>(L.n_fit_tiles));
+  if (L.n_fit_tiles > 0)
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(fit_nodes.data(), L.fit_nodes.p, fit_nodes.size() * 4, cudaMemcpyDeviceToHost,
+                                    c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  // Cost per tile, in pair evaluations (13 flop): its own PP + PC pairs, plus
+  // a per-target share of every fit ancestor's work — the
+  // node's CP + CC pairs and its 2 D P^2 fit epilogue spread evenly over its
+  // bin, and the downward evaluation of its interpolant at each target
+  // (~402 flop at d = 8, §8(d)) — through a difference array over tree
+  // positions.
+  const HostTree& ht = host_tree(c);
+  const int D = c.early.dim > 0 ? c.early.dim : 3;
+  const int deg = c.early.degree > 0 ? c.early.degree : 8;
+  const int P = (deg + 1) * (deg + 2) / 2;
+  const double down_pairs = (21.0 + 3.0 * (deg - 1) + (2.0 + 2.0 * D) * P) / 13.0;
+  std::vector<double> dens(size_t(N) + 1, 0.0);
+  for (int k = 0; k < L.n_fit_tiles; ++k) {
+    const int id = fit_nodes[size_t(k)];
+    const int64_t o = ht.off[size_t(id)], cn = ht.cnt[size_t(id)];
+    if (cn <= 0) continue;
+    const double node = double(fcost[size_t(k)].x + fcost[size_t(k)].y) + 2.0 * D * P * P / 13.0;
+    const double per = node / double(cn) + down_pairs;
+    dens[size_t(o)] += per;
+    dens[size_t(o + cn)] -= per;
+  }
   std::vector<double> pre(static_cast<size_t>(nt) + 1, 0.0);
-  for (int t = 0; t < nt; ++t) pre[size_t(t) + 1] = pre[size_t(t)] + double(cost[size_t(t)].x + cost[size_t(t)].y) + 1.0;
+  {
+    double run = 0.0;  // density at position `at`
+    int64_t at = 0;
+    for (int t = 0; t < nt; ++t) {
+      const int64_t b = tiles[size_t(t)].tgt_begin, e = b + tiles[size_t(t)].tgt_count;
+      double share = 0.0;
+      for (; at < e; ++at) {
+        run += dens[size_t(at)];
+        if (at >= b) share += run;
+      }
+      pre[size_t(t) + 1] = pre[size_t(t)] + double(cost[size_t(t)].x + cost[size_t(t)].y) + share + 1.0;
+    }
+  }
   const double total = pre[size_t(nt)];
   // cut before the first tile at or after the cost goal that starts a leaf
   // (a leaf's tiles share list_begin): parts never split a leaf, so the
@@ -1220,15 +1257,9 @@ void partition_targets(Ctx& c) {
   }
   c.cuts.pos.front() = 0;
   c.part_pos = c.cuts.pos;
-  std::vector<int> fit_nodes(static_cast<size_t>(L.n_fit_tiles));
-  if (L.n_fit_tiles > 0) {
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(fit_nodes.data(), L.fit_nodes.p, fit_nodes.size() * 4, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-  }
   std::vector<int> sel;
   for (int k = 0; k < L.n_fit_tiles; ++k) {
     const int id = fit_nodes[size_t(k)];
-    const HostTree& ht = host_tree(c);
     const int64_t o = ht.off[size_t(id)], e = o + ht.cnt[size_t(id)];
     if (o < L.p1 && e > L.p0) {
       sel.push_back(k);
