@@ -88,7 +88,12 @@ typedef struct {
 
 /* ---- context ------------------------------------------------------------ */
 int ssum_create(int device, ssum_ctx** out);
+/* Device buffers come from the device's stream-ordered memory pool; blocks a
+ * destroyed context released stay cached there for the next context (a fresh
+ * FaceTree then allocates nothing from the driver). ssum_trim_memory returns
+ * the cached, unused blocks of `device` to the driver. */
 void ssum_destroy(ssum_ctx* ctx);
+int ssum_trim_memory(int device);
 const char* ssum_last_error(const ssum_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the
  * context's own (non-blocking) stream. The legacy default stream has handle 0,

@@ -120,6 +120,7 @@ EXPORTED_SYMBOLS = (
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
     "ssum_rk4_step_end", "ssum_compute_proxy_weights", "ssum_last_rcond", "ssum_lattice_fit",
     "ssum_proxy_points", "ssum_partition_cuts", "ssum_set_output_order", "ssum_rk4_stage_end_rows",
+    "ssum_trim_memory",
 )
 
 
@@ -171,6 +172,7 @@ def load_library():
         "ssum_lattice_fit": (ctypes.c_int, [ctypes.c_int, _P, _P]),
         "ssum_proxy_points": (ctypes.c_int, [_P, ctypes.c_int, _P]),
         "ssum_partition_cuts": (ctypes.c_int, [_P, _P]),
+        "ssum_trim_memory": (ctypes.c_int, [ctypes.c_int]),
         "ssum_set_output_order": (ctypes.c_int, [_P, ctypes.c_int]),
         "ssum_rk4_stage_end_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64, _P, _I64] + [_P] * 4),
     }
@@ -591,6 +593,12 @@ def eval_cc(kernel, tree: FaceTree, it: Interaction, positions, strengths, cfg: 
             field: np.ndarray) -> None:
     """eval_cc<K> (treecode.cpp:223-244)."""
     _eval_interaction(kernel, tree, it, positions, strengths, cfg, field)
+
+
+def trim_memory(device: int = 0) -> None:
+    """Return the device-pool blocks destroyed FaceTrees left cached to the
+    driver (ssum_trim_memory)."""
+    _raise(load_library().ssum_trim_memory(int(device)), "ssum_trim_memory failed")
 
 
 def sbb_basis_size(degree: int) -> int:

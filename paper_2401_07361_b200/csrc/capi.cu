@@ -15,6 +15,11 @@ namespace ssum {
 
 void sorted_interactions(Ctx& c, std::vector<int4>& out);
 
+cudaStream_t& dbuf_stream() {
+  thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
 double Trace::now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -65,6 +70,7 @@ int guarded(ssum_ctx* h, F&& f) {
   if (!c) return SSUM_INVALID;
   try {
     cudaSetDevice(c->device);
+    dbuf_stream() = c->stream;
     f(*c);
     return SSUM_OK;
   } catch (const Error& e) {
@@ -328,6 +334,13 @@ int ssum_create(int device, ssum_ctx** out) {
     SSUM_CUDA_CHECK(cudaSetDevice(device));
     SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
+    dbuf_stream() = c->stream;
+    {  // keep freed blocks in the device's pool between calls (ssum_destroy trims it)
+      cudaMemPool_t pool;
+      SSUM_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = ~0ull;
+      SSUM_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     for (auto& e : c->ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
     SSUM_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     int prio_lo = 0, prio_hi = 0;
@@ -363,7 +376,8 @@ int ssum_create(int device, ssum_ctx** out) {
 void ssum_destroy(ssum_ctx* h) {
   Ctx* c = reinterpret_cast<Ctx*>(h);
   if (!c) return;
-  cudaSetDevice(c->device);
+  const int dev = c->device;
+  cudaSetDevice(dev);
   cudaDeviceSynchronize();
   // device buffers (DBuf) free themselves when the context is deleted below
   for (auto& e : c->ev) cudaEventDestroy(e);
@@ -382,8 +396,19 @@ void ssum_destroy(ssum_ctx* h) {
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);
-  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  dbuf_stream() = nullptr;  // the buffers go back to the pool in legacy-stream order
+  cudaStream_t own = c->own_stream;
   delete c;
+  cudaDeviceSynchronize();
+  if (own) cudaStreamDestroy(own);
+  (void)dev;  // the blocks stay cached in the device pool for the next context (ssum_trim_memory)
+}
+
+int ssum_trim_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaSetDevice(device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return SSUM_CUDA;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return SSUM_CUDA;
+  return cudaMemPoolTrimTo(pool, 0) == cudaSuccess ? SSUM_OK : SSUM_CUDA;
 }
 
 const char* ssum_last_error(const ssum_ctx* h) {

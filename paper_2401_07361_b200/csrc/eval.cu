@@ -538,21 +538,21 @@ void launch_prep(Ctx& c, cudaStream_t s, DBuf<unsigned char>& tmp, int degree, c
   // chunks) built on the device
   if (L.n_weight > 0) {
     const int nw = L.n_weight;
-    c.wcount.ensure(size_t(nw) + 1);
-    c.wcount_off.ensure(size_t(nw) + 1);
+    c.wcount.ensure(size_t(nw) + 1, false, s);
+    c.wcount_off.ensure(size_t(nw) + 1, false, s);
     k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.cnt.p, c.wcount.p);
     SSUM_LAUNCH_CHECK();
     size_t tb = 0;
     SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, s));
-    tmp.ensure(tb);
+    tmp.ensure(tb, false, s);
     SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, c.wcount.p, c.wcount_off.p, nw + 1, s));
     // chunk count without a read-back: a particle lies in at most one node
     // per level, so sum_w ceil(cnt_w / kUpChunk) <= nw + N (levels) / kUpChunk
     const int64_t nch_bound =
         int64_t(nw) + (int64_t(n) * (c.nodes.max_level + 1) + kUpChunk - 1) / kUpChunk;
     const int nch = static_cast<int>(nch_bound);
-    c.wchunks.ensure(size_t(nch) + size_t(nw));
-    c.wpart.ensure(size_t(nch) * P);
+    c.wchunks.ensure(size_t(nch) + size_t(nw), false, s);
+    c.wpart.ensure(size_t(nch) * P, false, s);
     int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
     k_up_fill<<<grid_for(nw, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.off.p, B.cnt.p, c.wcount_off.p,
                                                  c.wchunks.p, d_crange);

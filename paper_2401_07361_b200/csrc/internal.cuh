@@ -40,6 +40,14 @@ constexpr double kSingularTol = 1e-14;  // kernels.hpp:13
 // Device error flags (bitmask in ctx.d_flags[0]).
 enum : int { kFlagGeometry = 1, kFlagSingular = 2 };
 
+// Stream the device allocations of the current C-ABI call are ordered on
+// (the context's stream, set by the entry point): DBuf memory comes from the
+// device's stream-ordered pool (cudaMallocAsync / cudaFreeAsync), so growing
+// a buffer neither synchronises the device nor returns memory to the driver
+// between calls, and a fresh context reuses what earlier ones released.
+// Code that fills a buffer on another stream passes that stream explicitly.
+cudaStream_t& dbuf_stream();
+
 // Growable device array. Contents are NOT preserved on growth unless keep.
 template <class T>
 struct DBuf {
@@ -58,22 +66,20 @@ struct DBuf {
     return *this;
   }
   ~DBuf() { release(); }
-  void ensure(size_t n, bool keep = false, cudaStream_t s = 0) {
+  void ensure(size_t n, bool keep = false, cudaStream_t s = nullptr) {
     if (n <= cap) return;
+    if (!s) s = dbuf_stream();
     size_t nc = cap ? cap : 1024;
     while (nc < n) nc *= 2;
     T* q = nullptr;
-    SSUM_CUDA_CHECK(cudaMalloc(&q, nc * sizeof(T)));
+    SSUM_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&q), nc * sizeof(T), s));
     if (keep && p && cap) SSUM_CUDA_CHECK(cudaMemcpyAsync(q, p, cap * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    if (p) {
-      if (keep) SSUM_CUDA_CHECK(cudaStreamSynchronize(s));
-      cudaFree(p);
-    }
+    if (p) SSUM_CUDA_CHECK(cudaFreeAsync(p, s));  // after every earlier use on s (callers join other streams first)
     p = q;
     cap = nc;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, dbuf_stream());
     p = nullptr;
     cap = 0;
   }

@@ -806,7 +806,6 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   TravScratch& S = c.trav;
-  if (!S.plan_valid || S.plan_m.empty()) return false;
   if (S.bfs_blocks == 0) {
     int per_sm = 0, sms = 0;
     SSUM_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs, kBfsThreads, 0));
@@ -819,9 +818,17 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   }
   if (S.bfs_blocks < 0) return false;
   const int nb = S.bfs_blocks;
-  const int fplan = *std::max_element(S.plan_m.begin(), S.plan_m.end());
-  int fcap = fplan + fplan / 8 + 1024;
-  long long ecap = S.plan_ne + S.plan_ne / 8 + 4096;
+  int fcap;
+  long long ecap;
+  if (S.plan_valid && !S.plan_m.empty()) {  // sized from the previous call
+    const int fplan = *std::max_element(S.plan_m.begin(), S.plan_m.end());
+    fcap = fplan + fplan / 8 + 1024;
+    ecap = S.plan_ne + S.plan_ne / 8 + 4096;
+  } else {  // first call: generous estimates from N (configs 1-5 emit 1.6-2.0 N pairs)
+    const int64_t N = B.n;
+    fcap = static_cast<int>(std::min<int64_t>(2 * N + 65536, 0x3fffffff));
+    ecap = 3 * N + 65536;
+  }
   S.F0.ensure(size_t(fcap));
   S.F1.ensure(size_t(fcap));
   S.action.ensure(size_t(fcap));

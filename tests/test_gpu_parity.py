@@ -578,6 +578,9 @@ def test_context_destroy_frees_device_memory(ss, mesh_fixture):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info(0)[0]
     assert free0 - free1 < 8 << 20, (free0, free1)
+    ss.trim_memory(0)  # the cached pool blocks go back to the driver
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info(0)[0] >= free1
 
 
 def test_log_far_accuracy(ss):

@@ -4,9 +4,11 @@ placed the cost-balanced cuts, each part bins, traverses and lists its own
 targets only). The max over parts approximates one G-GPU step before the row
 all-gather; nothing here waits on another rank.
 
-    python tools/part_bench.py [G ...] [--phases]
+    python tools/part_bench.py [G ...] [--phases] [--config c4|c5]
 
---phases adds each part's phase split (TreecodeStats of its last call).
+--phases adds each part's phase split (TreecodeStats of its last call);
+--config c5: BASELINE config 5 (L10 mesh, N = 10,485,762, theta = 0.8), the
+scaling sweep's own config (default c4: L9, theta = 0.7).
 """
 import json
 import sys
@@ -17,15 +19,17 @@ sys.path.insert(0, ".")
 import paper_2401_07361_b200 as ss  # noqa: E402
 
 phases = "--phases" in sys.argv
-parts = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [1, 2, 4, 8]
-xyz, area = ss.make_icosa_mesh(9)
+config = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "c4"
+level, theta = {"c4": (9, 0.7), "c5": (10, 0.8)}[config]
+parts = [int(a) for a in sys.argv[1:] if not a.startswith("--") and a not in ("c4", "c5")] or [1, 2, 4, 8]
+xyz, area = ss.make_icosa_mesh(level)
 q = ss.rh4_vorticity(xyz) * area
 n = xyz.shape[0]
 dev = torch.device("cuda", 0)
 d_xyz = torch.from_numpy(xyz).to(dev)
 d_q = torch.from_numpy(q).to(dev)
 d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
-cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+cfg = ss.TraversalConfig(theta=theta, n_threshold=64, degree=8, max_depth=10)
 res = {}
 for G in parts:
     tree = ss.FaceTree(0)
@@ -51,4 +55,4 @@ for G in parts:
     res[G] = {"max_part_ms": max(per), "min_part_ms": min(per), "parts_ms": per}
     if phases:
         res[G]["phases_of_max_part"] = split[per.index(max(per))]
-    print(json.dumps({"G": G, **res[G]}), flush=True)
+    print(json.dumps({"config": config, "n": n, "G": G, **res[G]}), flush=True)
