@@ -363,12 +363,21 @@ def run_gpu(args):
         torch.distributed.all_reduce(t, op=getattr(torch.distributed.ReduceOp, op.upper()))
         return float(t.item())
 
-    # cold: the first evaluation on a fresh FaceTree (tree built from scratch)
-    cold = ss.FaceTree(local)
-    cold.set_stream(stream.cuda_stream)
+    # cold: the first evaluation on a fresh FaceTree (tree built from scratch,
+    # every buffer allocated), in a warm process: a throw-away tree first
+    # loads the kernels (lazy module loading) and leaves its device blocks
+    # cached in the pool, as any earlier FaceTree of the process would
     d_x = torch.from_numpy(xyz).to(dev)
     d_q = torch.from_numpy(q).to(dev)
     d_o = torch.zeros((n, C["dim"]), dtype=torch.float64, device=dev)
+    w = ss.FaceTree(local)
+    w.set_stream(stream.cuda_stream)
+    for _ in range(2):
+        ss.treecode_sum_device(w, kernel_class(ss), ss.TraversalConfig(**C["cfg"]), d_x.data_ptr(), d_q.data_ptr(),
+                               n, d_o.data_ptr())
+    w.close()
+    cold = ss.FaceTree(local)
+    cold.set_stream(stream.cuda_stream)
     barrier()
     t0 = time.perf_counter()
     ss.treecode_sum_device(cold, kernel_class(ss), ss.TraversalConfig(**C["cfg"]), d_x.data_ptr(), d_q.data_ptr(),

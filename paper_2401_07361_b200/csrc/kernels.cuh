@@ -248,6 +248,91 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
   }
 }
 
+// One step of a near-possible range, decided per warp by a vote (the
+// default near handling of leaf / direct tiles): the NT x NS denominators
+// first, exactly as far_block forms them; when no lane of the warp met a near
+// pair (den < 2^-20) or one of its self pairs (known by list position), the
+// step finishes on far_block's arithmetic, otherwise the whole warp takes the
+// reference-rounded exact_step for it. Near pairs are rare outside dense
+// inputs (none on the icosahedral meshes) and a leaf's self pairs fill only
+// the steps over its own bin, so nearly every step stays on the fast path
+// with no per-pair mask, count or repair walk.
+template <int KER, int NT, int NS>
+__device__ __forceinline__ void exact_step(const double4* x, const double4* y, int G, Acc<KER>* a, int f0,
+                                           const int* selfpos, int* flags) {
+#pragma unroll
+  for (int c = 0; c < NT * NS; ++c) {
+    const double4& xx = x[c % NT];
+    const double4& yy = y[c / NT];
+    const double den = __dsub_rn(1.0, __dadd_rn(__dadd_rn(__dmul_rn(xx.x, yy.x), __dmul_rn(xx.y, yy.y)),
+                                                __dmul_rn(xx.z, yy.z)));
+    const bool self = f0 + (c / NT) * G == selfpos[c % NT];  // treecode.cpp:388, :257
+    const bool sing = den <= kSingularTol;                   // kernels.hpp:19,27-29
+    if (sing && !self) atomicOr(flags, kFlagSingular);
+    if constexpr (KER == kBS) {
+      const double r = (self || sing) ? 0.0 : q_over(yy.w, den);
+      a[c % NT].s[0] = fma(r, __dsub_rn(yy.x, xx.x), a[c % NT].s[0]);
+      a[c % NT].s[1] = fma(r, __dsub_rn(yy.y, xx.y), a[c % NT].s[1]);
+      a[c % NT].s[2] = fma(r, __dsub_rn(yy.z, xx.z), a[c % NT].s[2]);
+    } else {
+      a[c % NT].s[0] += (self || sing) ? 0.0 : yy.w * log(den);
+    }
+  }
+}
+
+template <int KER, int NT, int NS, bool CUBIC = false>
+__device__ __forceinline__ void near_vote_block(const double4* x, const double4* __restrict__ B, int G,
+                                                Acc<KER>* a, int f0, const int* selfpos, int* flags,
+                                                const double2* __restrict__ ltab) {
+  constexpr int C = NT * NS;
+  double4 y[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) y[s] = B[s * G];
+  double den[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].x, y[c / NT].x, 1.0);
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].y, y[c / NT].y, den[c]);
+#pragma unroll
+  for (int c = 0; c < C; ++c) den[c] = fma(-x[c % NT].z, y[c / NT].z, den[c]);
+  bool slow = false;
+#pragma unroll
+  for (int c = 0; c < C; ++c) slow |= __double2hiint(den[c]) < kNearHi;
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int s = 0; s < NS; ++s) slow |= f0 + s * G == selfpos[t];
+  if (__any_sync(0xffffffffu, slow)) {
+    exact_step<KER, NT, NS>(x, y, G, a, f0, selfpos, flags);
+    return;
+  }
+  if constexpr (KER == kBS) {
+    double r[C], e[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = rcp_approx(den[c]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) e[c] = fma(-den[c], r[c], 1.0);
+    if constexpr (CUBIC) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) e[c] = fma(e[c], e[c], e[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = y[c / NT].w * r[c];
+#pragma unroll
+    for (int c = 0; c < C; ++c) r[c] = fma(r[c], e[c], r[c]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[0] = fma(r[c], y[c / NT].x, a[c % NT].s[0]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[1] = fma(r[c], y[c / NT].y, a[c % NT].s[1]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) a[c % NT].s[2] = fma(r[c], y[c / NT].z, a[c % NT].s[2]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      a[c % NT].s[0] = fma(y[c / NT].w, CUBIC ? log(den[c]) : log_tab(den[c], ltab), a[c % NT].s[0]);
+  }
+}
+
 // Near-possible block of a dense leaf tile (Biot-Savart): every pair with
 // the reference's rounding (den = 1 - ((x.x y.x + x.y y.y) + x.z y.z),
 // separately rounded; singular guard on that value, kernels.hpp:19,27-29),

@@ -294,6 +294,20 @@ __global__ void __launch_bounds__(NTH, MINB)
         for (; it < near_steps; ++it) near_exact_block<kTpt, kNs>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos, flags);
       }
     }
+#ifdef SSUM_NEAR_VOTE
+    // tuning variant: per-step warp vote (kernels.cuh near_vote_block) —
+    // measured slower at C4 (leaf tiles 5.24 vs 5.16 ms with the mask below)
+    if (it < near_steps) {
+      int selfpos[kTpt];
+#pragma unroll
+      for (int q = 0; q < kTpt; ++q) selfpos[q] = (T.has_self & 1) ? ti[q] + T.self_shift : -1;
+      const int f0 = c * kChunk + g;
+#pragma unroll kNearUnroll
+      for (; it < near_steps; ++it)
+        near_vote_block<KER, kTpt, kNs, MODE == kDirectMode>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos,
+                                                              flags, ltab);
+    }
+#else
     if (it < near_steps) {
       // bit `it` of hit: step `it` met a masked pair (self or near); steps
       // past 64 are all re-walked when a repair is needed
@@ -332,6 +346,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         }
       }
     }
+#endif
     // well-separated sources only: branch-free, kNs sources x kTpt targets
     // of independent chains per step (zero-padded tail contributes 0)
     const double4* Bp = B + it * kStep;
