@@ -86,9 +86,13 @@ SSUM_HD d3 unit_rn(d3 v, int* bad) {
 
 // great_circle_distance = atan2(|a x b|, a.b) (geometry.cpp:55-57). The
 // device atan2 is CUDA's (<= 2 ulp), not glibc's: node radii and MAC distances
-// may differ from the reference in the last bits. A MAC decision flips only if
-// (r_t + r_s)/R lies within a few ulp of theta; tests/test_gpu_tree.py checks
-// the full interaction lists against the reference on every config.
+// may differ from the reference in the last bits. A MAC decision could flip
+// only if (r_t + r_s)/R lay within a few ulp of theta, so the traversal sends
+// every pair within a 1e-12 relative band of theta to the host, which decides
+// it with glibc and the reference's expressions (traversal.cu MacCtl /
+// resolve_mac): decisions are the reference's by construction. Tests:
+// tests/test_gpu_boundary.py (forced wide band), tests/test_gpu_parity.py and
+// tests/test_gpu_fullsize.py (bit-identical lists up to C5).
 SSUM_HD double arc_dist(d3 a, d3 b) {
   const d3 c = cross_rn(a, b);
   return atan2(sqrt_rn(dot_rn(c, c)), dot_rn(a, b));
