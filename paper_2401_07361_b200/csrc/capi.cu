@@ -245,6 +245,13 @@ __global__ void k_rk4_stage(int64_t n, int stage, double cs, const double* __res
   q[i] = mul_rn(zs, area[i]);
 }
 
+// stage-0 strengths q = zeta A (k_rk4_stage's product) for the host-pointer RK4
+__global__ void k_rk4_q(int64_t n, const double* __restrict__ z0, const double* __restrict__ area,
+                        double* __restrict__ q) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) q[i] = mul_rn(z0[i], area[i]);
+}
+
 // k_s = u, kz_s = -2 Omega u_z; acc = ((k1 + 2 k2) + 2 k3) + k4 in that order.
 __global__ void k_rk4_accum(int64_t n, int stage, double omega, const double* __restrict__ u, double* __restrict__ k,
                             double* __restrict__ kz, double* __restrict__ acc, double* __restrict__ accz) {
@@ -292,10 +299,11 @@ __global__ void k_rk4_accum_rows(int64_t n, int stage, double omega, const doubl
   accz[i] = stage == 0 ? kzv : add_rn(accz[i], mul_rn(w, kzv));
 }
 
-__global__ void k_rk4_final(int64_t n, double h6, double* __restrict__ x0, double* __restrict__ z0,
+// particles [i0, i1)
+__global__ void k_rk4_final(int64_t i0, int64_t i1, double h6, double* __restrict__ x0, double* __restrict__ z0,
                             const double* __restrict__ acc, const double* __restrict__ accz, int* flags) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= i1) return;
   int bad = 0;
   const d3 v{add_rn(x0[3 * i], mul_rn(h6, acc[3 * i])), add_rn(x0[3 * i + 1], mul_rn(h6, acc[3 * i + 1])),
              add_rn(x0[3 * i + 2], mul_rn(h6, acc[3 * i + 2]))};
@@ -713,32 +721,93 @@ int ssum_rk4(ssum_ctx* h, const ssum_config* cfg, double* xyz, double* zeta, con
     double* kz = k + 3 * N;
     double* acc = kz + N;
     double* accz = acc + 3 * N;
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(x0, xyz, 3 * N * 8, cudaMemcpyHostToDevice, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(z0, zeta, N * 8, cudaMemcpyHostToDevice, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(ar, area, N * 8, cudaMemcpyHostToDevice, c.stream));
     const double cs[4] = {0.0, 0.5 * dt, 0.5 * dt, dt};
     const int bs = 256;
+    // Inputs on the copy stream, overlapped with the first evaluation as in
+    // ssum_treecode_sum: x in kIoChunks pieces (the first stage's tree walk
+    // starts on each as it lands), then zeta and A and, still on the copy
+    // stream, the first stage's q = zeta A (waited for at the gather). The
+    // first stage evaluates at x0 itself (its stage positions are x0 bit for
+    // bit). The direct-sum driver takes the plain path.
+    Ctx::HostIo& io = c.io;
+    struct Reset {
+      Ctx& c;
+      ~Reset() {
+        cudaStreamSynchronize(c.copy_stream);
+        c.io.active = false, c.io.h_out = nullptr;
+      }
+    } reset{c};
+    SSUM_CUDA_CHECK(cudaEventRecord(io.t0, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, io.t0, 0));
+    for (int j = 0; j <= Ctx::kIoChunks; ++j) io.bounds[j] = n * j / Ctx::kIoChunks;
+    for (int j = 0; j < Ctx::kIoChunks; ++j) {
+      const int64_t a = io.bounds[j], b = io.bounds[j + 1];
+      if (b > a)
+        SSUM_CUDA_CHECK(cudaMemcpyAsync(x0 + 3 * a, xyz + 3 * a, size_t(b - a) * 24, cudaMemcpyHostToDevice,
+                                        c.copy_stream));
+      SSUM_CUDA_CHECK(cudaEventRecord(io.xyz[j], c.copy_stream));
+    }
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(z0, zeta, N * 8, cudaMemcpyHostToDevice, c.copy_stream));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(ar, area, N * 8, cudaMemcpyHostToDevice, c.copy_stream));
+    k_rk4_q<<<grid_for(n, bs), bs, 0, c.copy_stream>>>(n, z0, ar, q);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+    SSUM_CUDA_CHECK(cudaEventRecord(io.q, c.copy_stream));
+    if (direct) {
+      SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, io.q, 0));  // everything landed
+    } else {
+      io.active = true;
+      io.h_out = nullptr;
+      io.dim = 3;
+    }
     for (int step = 0; step < steps; ++step) {
       for (int s = 0; s < 4; ++s) {
         SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
-        k_rk4_stage<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, cs[s], x0, z0, ar, k, kz, xs, q, c.d_flags.p);
-        SSUM_LAUNCH_CHECK();
-        if (direct)
-          direct_sum_device(c, SSUM_BIOT_SAVART, xs, q, n, u);
-        else
-          treecode_device(c, SSUM_BIOT_SAVART, *cfg, xs, q, n, u, st);
+        if (io.active) {  // first stage of the call: x0 and q as they land
+          treecode_device(c, SSUM_BIOT_SAVART, *cfg, x0, q, n, u, st);
+          SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, io.q, 0));  // zeta and A for the next stages
+          io.active = false;
+        } else {
+          k_rk4_stage<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, cs[s], x0, z0, ar, k, kz, xs, q, c.d_flags.p);
+          SSUM_LAUNCH_CHECK();
+          c.launches++;
+          if (direct)
+            direct_sum_device(c, SSUM_BIOT_SAVART, xs, q, n, u);
+          else
+            treecode_device(c, SSUM_BIOT_SAVART, *cfg, xs, q, n, u, st);
+        }
         k_rk4_accum<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, omega, u, k, kz, acc, accz);
         SSUM_LAUNCH_CHECK();
-        c.launches += 2;
+        c.launches++;
       }
-      k_rk4_final<<<grid_for(n, bs), bs, 0, c.stream>>>(n, dt / 6.0, x0, z0, acc, accz, c.d_flags.p);
-      SSUM_LAUNCH_CHECK();
-      c.launches++;
+      if (step + 1 < steps) {
+        k_rk4_final<<<grid_for(n, bs), bs, 0, c.stream>>>(0, n, dt / 6.0, x0, z0, acc, accz, c.d_flags.p);
+        SSUM_LAUNCH_CHECK();
+        c.launches++;
+        check_flags(c, "rk4");
+        continue;
+      }
+      // last step: the final update in pieces, each piece's copy to the host
+      // overlapping the next piece's update
+      for (int j = 0; j < Ctx::kIoChunks; ++j) {
+        const int64_t a = io.bounds[j], b = io.bounds[j + 1];
+        if (b > a) {
+          k_rk4_final<<<grid_for(b - a, bs), bs, 0, c.stream>>>(a, b, dt / 6.0, x0, z0, acc, accz, c.d_flags.p);
+          SSUM_LAUNCH_CHECK();
+          c.launches++;
+        }
+        SSUM_CUDA_CHECK(cudaEventRecord(io.out[j], c.stream));
+        SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.copy_stream, io.out[j], 0));
+        if (b > a) {
+          SSUM_CUDA_CHECK(cudaMemcpyAsync(xyz + 3 * a, x0 + 3 * a, size_t(b - a) * 24, cudaMemcpyDeviceToHost,
+                                          c.copy_stream));
+          SSUM_CUDA_CHECK(cudaMemcpyAsync(zeta + a, z0 + a, size_t(b - a) * 8, cudaMemcpyDeviceToHost,
+                                          c.copy_stream));
+        }
+      }
       check_flags(c, "rk4");
     }
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(xyz, x0, 3 * N * 8, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaMemcpyAsync(zeta, z0, N * 8, cudaMemcpyDeviceToHost, c.stream));
-    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.copy_stream));
   });
 }
 
@@ -810,7 +879,7 @@ int ssum_rk4_step_end(ssum_ctx* h, double dt, int64_t n, double* d_x0, double* d
   return guarded(h, [&](Ctx& c) {
     check_n(n);
     if (n == 0) return;
-    k_rk4_final<<<grid_for(n, 256), 256, 0, c.stream>>>(n, dt / 6.0, d_x0, d_z0, d_acc, d_accz, c.d_flags.p);
+    k_rk4_final<<<grid_for(n, 256), 256, 0, c.stream>>>(0, n, dt / 6.0, d_x0, d_z0, d_acc, d_accz, c.d_flags.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
     check_flags(c, "rk4");
