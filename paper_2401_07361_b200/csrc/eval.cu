@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
     while (pend) {
       const int an = __shfl_sync(full, a, __ffs(pend) - 1);
       const bool mine = fit && a == an;
+      SSUM_DCHECK(pslot[an] >= 0);
       const double* c = coeff + size_t(pslot[an]) * D * P;
       for (int i = lane; i < D * P; i += 32) cs[w][(i % P) * DP + i / P] = c[i];
       if (lane < 12) cr[w][lane] = cramer[12 * an + lane];
@@ -574,6 +575,7 @@ void size_eval_buffers(Ctx& c, int degree, int D, int64_t n) {
   const int64_t npts = n + int64_t(c.lists.n_proxy) * P;
   if (npts > 0x7fffffff) throw Error(SSUM_INVALID, "point count exceeds int32 indexing");
   c.pts.ensure(size_t(npts));
+  c.npts = npts;
   c.S.ensure(size_t(n) * D);
   c.coeff.ensure(std::max<size_t>(size_t(c.lists.n_proxy) * D * P, 1));
 }
@@ -888,6 +890,7 @@ void eval_interaction(Ctx& c, int kernel, int degree, const double* xyz, const d
   const Compact k = pack_bins(c, xyz, q, target, source);
   if (k.nt == 0 || k.ns == 0) return;  // an empty bin contributes nothing
   const int64_t n = k.n;
+  c.npts = n + 2 * P;
   c.S.ensure(size_t(n + 2 * P) * D);
   c.coeff.ensure(size_t(D) * P);
   c.ix_out.ensure(size_t(k.nt) * D);

@@ -33,6 +33,27 @@ struct Error : std::runtime_error {
 
 #define SSUM_LAUNCH_CHECK() SSUM_CUDA_CHECK(cudaGetLastError())
 
+// Device-side bounds checks of the index arithmetic (the checked build,
+// `make -C paper_2401_07361_b200/csrc checked`, compiles with
+// -DSSUM_DEVICE_CHECKS): a violated check prints its site and traps, so the
+// test run fails at the first bad access. compute-sanitizer is not available
+// on the GPU pool; this is the stand-in (tests run against the checked
+// library with SSUM_LIBRARY=.../lib/checked/libspheresum_b200.so).
+#ifdef SSUM_DEVICE_CHECKS
+#define SSUM_DCHECK(cond)                                                                      \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("SSUM_DCHECK failed %s:%d (block %d thread %d): %s\n", __FILE__, __LINE__,       \
+             int(blockIdx.x), int(threadIdx.x), #cond);                                        \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define SSUM_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 constexpr int kMaxDegree = 20;  // kMaxSbbDegree (sbb.hpp:12)
 constexpr int kWarp = 32;
 constexpr double kSingularTol = 1e-14;  // kernels.hpp:13
@@ -287,6 +308,7 @@ struct Ctx {
   int* h_pinned = nullptr;           // small pinned host scratch (64 ints)
   DBuf<unsigned char> cub_tmp;
   DBuf<double4> pts;                 // unified points: N particles (tree order) + proxies
+  int64_t npts = 0;                  // valid entries of pts (bounds checks)
   DBuf<double> S;                    // per tree position accumulated kernel sums (D doubles)
   DBuf<double> coeff;                // per proxy slot: D x P fit coefficients
   DBuf<double> wpart;                // upward partial sums

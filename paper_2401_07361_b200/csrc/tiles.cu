@@ -126,9 +126,10 @@ __global__ void __launch_bounds__(NTH, MINB)
     k_tiles(const Tile* __restrict__ tiles, int ntiles, const int* __restrict__ sel,
             const SrcRange* __restrict__ ranges, const double4* __restrict__ pts, double* __restrict__ S,
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
-            const double* __restrict__ vinv, int P, double* __restrict__ coeff) {
+            const double* __restrict__ vinv, int P, double* __restrict__ coeff, int64_t npts) {
   constexpr int D = KDim<KER>::D;
   constexpr int kFU = MODE == kFitMode ? 2 : kFastUnroll;
+  (void)npts;  // valid points in pts (bounds checks of the checked build)
   // dynamic shared memory (kTileSmem bytes): two source stages and the range
   // table; two mbarriers (one per stage)
   extern __shared__ __align__(16) unsigned char smem[];
@@ -146,6 +147,8 @@ __global__ void __launch_bounds__(NTH, MINB)
   const int tix = sel ? sel[blockIdx.x] : static_cast<int>(blockIdx.x);
   const Tile T = tiles[tix];
   const int tc = T.tgt_count;
+  SSUM_DCHECK(tc >= 1 && tc <= kTileTargets && T.tgt_begin >= 0 && T.tgt_begin + tc <= npts);
+  SSUM_DCHECK(T.list_begin >= 0 && T.list_end >= T.list_begin && T.near_total <= T.total);
   const int th = (tc + kTpt - 1) / kTpt;  // thread-targets; thread slot u holds targets u, u + th, ...
   const int G = min(32, NTH / th);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -233,6 +236,7 @@ __global__ void __launch_bounds__(NTH, MINB)
         if (pad < c0 + cn) {
           more_r = true;
           const int lo = max(pad, c0), hi = min(end, c0 + cn);
+          SSUM_DCHECK(hi <= lo || (beg + (lo - pad) >= 0 && beg + (hi - pad) <= npts && hi - c0 <= kChunk));
           if (hi > lo)
             bulk_g2s(dst + (lo - c0), pts + beg + (lo - pad), static_cast<unsigned>(hi - lo) * sizeof(double4),
                      &full[st]);
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     }
     __syncthreads();
     const int slot = pslot[fit_nodes[tix]];
+    SSUM_DCHECK(slot >= 0);
     for (int kk = tid; kk < P; kk += NTH) {
 #pragma unroll
       for (int d = 0; d < D; ++d) {
@@ -471,7 +476,7 @@ void launch_fit_tiles_on(Ctx& c, cudaStream_t stream, int kernel, int P, const T
   auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device)
                           : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device);
   k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), stream>>>(tiles, nfit, sel, ranges, c.pts.p, nullptr, c.d_flags.p,
-                                                           fit_nodes, pslot, c.vinv.p, P, coeff);
+                                                           fit_nodes, pslot, c.vinv.p, P, coeff, c.npts);
 }
 
 void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel) {
@@ -487,7 +492,7 @@ void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tile
                   : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device)
                                    : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device));
   k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
-                                                nullptr, nullptr, 0, nullptr);
+                                                nullptr, nullptr, 0, nullptr, c.npts);
 }
 
 // Direct sum (treecode.cpp:246-264): every target against one range [0, n)
@@ -498,6 +503,7 @@ void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out) {
   c.direct_range.ensure(1);
   const int bs = 256;
   k_direct_tiles<<<grid_for(nt, bs), bs, 0, c.stream>>>(n, c.direct_tiles.p, c.direct_range.p);
+  c.npts = n;
   SSUM_LAUNCH_CHECK();
   launch_leaf_tiles(c, c.stream, kernel, c.direct_tiles.p, static_cast<int>(nt), c.direct_range.p, c.S.p, true);
   SSUM_LAUNCH_CHECK();

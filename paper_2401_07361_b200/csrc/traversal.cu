@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(32 * kFillWarps)
     const int w = cur.w;
     const int c = cnt[leaf];
     const int nt = (c + kTileTargets - 1) / kTileTargets;
+    SSUM_DCHECK(w0 + w <= range_off[k + 1]);  // within the ranges k_leaf_count sized
     for (int j = lane; j < nt; j += 32) {
       Tile t;
       t.tgt_begin = offl + j * kTileTargets;
