@@ -369,6 +369,7 @@ int ssum_create(int device, ssum_ctx** out) {
     SSUM_CUDA_CHECK(cudaEventCreate(&c->io.t1));
     c->d_flags.ensure(64);
     SSUM_CUDA_CHECK(cudaMemset(c->d_flags.p, 0, 64 * sizeof(int)));
+    ensure_log_table(*c);
     tree_init_roots(*c);
   } catch (const Error& e) {
     delete c;

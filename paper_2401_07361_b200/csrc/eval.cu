@@ -498,6 +498,24 @@ void lattice_inverse(int degree, std::vector<double>& inv, double& rcond) {
   rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
 }
 
+// The far-pair log table (kernels.cuh log_tab): (1 / c_j, log c_j) for the
+// 512 bucket centres, each correctly rounded from 80-bit precision.
+void log_table(double2* tab) {
+  for (int j = 0; j < kLogTabN; ++j) {
+    const long double c = static_cast<long double>(log_tab_node(j));
+    tab[j] = make_double2(static_cast<double>(1.0L / c), static_cast<double>(logl(c)));
+  }
+}
+
+void ensure_log_table(Ctx& c) {
+  if (c.logtab.p) return;
+  std::vector<double2> h(static_cast<size_t>(kLogTabN));
+  log_table(h.data());
+  c.logtab.ensure(h.size());
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.logtab.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+
 // ConditioningError when the reciprocal condition number is not > 1e-12
 // (sbb.cpp:89-93); the value travels with the error (Ctx::last_rcond).
 void ensure_vinv(Ctx& c, int degree) {

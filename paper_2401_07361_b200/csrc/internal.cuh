@@ -315,6 +315,7 @@ struct Ctx {
   DBuf<int4> wchunks;                // upward chunks (node, begin, count, 0) + per-node chunk ranges
   DBuf<int> wcount, wcount_off;      // chunks per weight node, and their prefix
   DBuf<double> vinv;                 // P x P inverse Vandermonde (row-major), per degree
+  DBuf<double2> logtab;              // far-pair log table (kernels.cuh log_tab)
   int vinv_degree = -1;
   DBuf<double> in_xyz, in_q, out_buf;  // staging for host-pointer entry points
   DBuf<Tile> direct_tiles;
@@ -394,6 +395,7 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
 void direct_sum_device(Ctx& c, int kernel, const double* d_xyz, const double* d_q, int64_t n,
                        double* d_out);
 void ensure_vinv(Ctx& c, int degree);
+void ensure_log_table(Ctx& c);
 void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel);
 // k_tiles<fit> over explicit tiles / ranges (fit node k -> coeff slot pslot[fit_nodes[k]])
 void launch_fit_tiles_on(Ctx& c, cudaStream_t stream, int kernel, int P, const Tile* tiles, int nfit, const int* sel,

@@ -62,71 +62,49 @@ __device__ __forceinline__ double q_over(double q, double den) {
 
 // log(x) for a far pair's denominator (x >= 2^-20, positive and normal;
 // anything else only reaches it in a near-masked step, whose term is
-// discarded), table-driven: x = 2^k m, m in [1, 2) from the bits; c_j =
-// 1 + j/64 the nearest of 65 nodes (j from the top 7 mantissa bits), so
-// t = (m - c_j) / c_j is within 2^-7 (m - c_j exact by Sterbenz; c_j = 1 and 2
-// give t exactly, so x near 1 keeps full relative accuracy); log(m) =
-// log(c_j) + log1p(t), log1p through t^8 (truncation < 2^-66 relative).
-// Nodes c_j >= sqrt(2) (j >= 27) are taken as c_j / 2 with k + 1, so the
-// k ln 2 term and log(c) never cancel catastrophically. ln 2 is split into
-// a 21-bit head (k ln2_hi exact) and a tail. <= 1.6 ulp (CPU emulation over
-// [2^-20, 4]; the GPU test bounds it by 2 ulp); 13 FP64 instructions and one
-// LDS.128 of the shared-memory copy of kLogTab, against 24 for the
-// atanh-series version it replaced and ~85 for the generic log.
-// kLogTab[j] = (1 / c_j, log c_j or log(c_j / 2) for j >= 27), both
-// correctly rounded (computed in 80-bit precision).
-constexpr int kLogTabN = 65;
-static __constant__ double2 kLogTab[kLogTabN] = {
-    {0x1p+0, 0x0p+0},    {0x1.f81f81f81f82p-1, 0x1.fc0a8b0fc03e4p-7},
-    {0x1.f07c1f07c1f08p-1, 0x1.f829b0e7833p-6},    {0x1.e9131abf0b767p-1, 0x1.77458f632dcfcp-5},
-    {0x1.e1e1e1e1e1e1ep-1, 0x1.f0a30c01162a6p-5},    {0x1.dae6076b981dbp-1, 0x1.341d7961bd1d1p-4},
-    {0x1.d41d41d41d41dp-1, 0x1.6f0d28ae56b4cp-4},    {0x1.cd85689039b0bp-1, 0x1.a926d3a4ad563p-4},
-    {0x1.c71c71c71c71cp-1, 0x1.e27076e2af2e6p-4},    {0x1.c0e070381c0ep-1, 0x1.0d77e7cd08e59p-3},
-    {0x1.bacf914c1badp-1, 0x1.29552f81ff523p-3},    {0x1.b4e81b4e81b4fp-1, 0x1.44d2b6ccb7d1ep-3},
-    {0x1.af286bca1af28p-1, 0x1.5ff3070a793d4p-3},    {0x1.a98ef606a63bep-1, 0x1.7ab890210d909p-3},
-    {0x1.a41a41a41a41ap-1, 0x1.9525a9cf456b4p-3},    {0x1.9ec8e951033d9p-1, 0x1.af3c94e80bff3p-3},
-    {0x1.999999999999ap-1, 0x1.c8ff7c79a9a22p-3},    {0x1.948b0fcd6e9ep-1, 0x1.e27076e2af2e6p-3},
-    {0x1.8f9c18f9c18fap-1, 0x1.fb9186d5e3e2bp-3},    {0x1.8acb90f6bf3aap-1, 0x1.0a324e27390e3p-2},
-    {0x1.8618618618618p-1, 0x1.1675cababa60ep-2},    {0x1.8181818181818p-1, 0x1.22941fbcf7966p-2},
-    {0x1.7d05f417d05f4p-1, 0x1.2e8e2bae11d31p-2},    {0x1.78a4c8178a4c8p-1, 0x1.3a64c556945eap-2},
-    {0x1.745d1745d1746p-1, 0x1.4618bc21c5ec2p-2},    {0x1.702e05c0b817p-1, 0x1.51aad872df82dp-2},
-    {0x1.6c16c16c16c17p-1, 0x1.5d1bdbf5809cap-2},    {0x1.6816816816817p-1, -0x1.5d5bddf595f3p-2},
-    {0x1.642c8590b2164p-1, -0x1.522ae0738a3d8p-2},    {0x1.6058160581606p-1, -0x1.4718dc271c41bp-2},
-    {0x1.5c9882b931057p-1, -0x1.3c25277333184p-2},    {0x1.58ed2308158edp-1, -0x1.314f1e1d35ce4p-2},
-    {0x1.5555555555555p-1, -0x1.269621134db92p-2},    {0x1.51d07eae2f815p-1, -0x1.1bf99635a6b95p-2},
-    {0x1.4e5e0a72f0539p-1, -0x1.1178e8227e47cp-2},    {0x1.4afd6a052bf5bp-1, -0x1.07138604d5862p-2},
-    {0x1.47ae147ae147bp-1, -0x1.f991c6cb3b379p-3},    {0x1.446f86562d9fbp-1, -0x1.e530effe71012p-3},
-    {0x1.4141414141414p-1, -0x1.d1037f2655e7bp-3},    {0x1.3e22cbce4a902p-1, -0x1.bd087383bd8adp-3},
-    {0x1.3b13b13b13b14p-1, -0x1.a93ed3c8ad9e3p-3},    {0x1.3813813813814p-1, -0x1.95a5adcf7017fp-3},
-    {0x1.3521cfb2b78c1p-1, -0x1.823c16551a3c2p-3},    {0x1.323e34a2b10bfp-1, -0x1.6f0128b756abcp-3},
-    {0x1.2f684bda12f68p-1, -0x1.5bf406b543db2p-3},    {0x1.2c9fb4d812cap-1, -0x1.4913d8333b561p-3},
-    {0x1.29e4129e4129ep-1, -0x1.365fcb0159016p-3},    {0x1.27350b8812735p-1, -0x1.23d712a49c202p-3},
-    {0x1.2492492492492p-1, -0x1.1178e8227e47cp-3},    {0x1.21fb78121fb78p-1, -0x1.fe89139dbd566p-4},
-    {0x1.1f7047dc11f7p-1, -0x1.da727638446a2p-4},    {0x1.1cf06ada2811dp-1, -0x1.b6ac88dad5b1cp-4},
-    {0x1.1a7b9611a7b96p-1, -0x1.9335e5d594989p-4},    {0x1.1811811811812p-1, -0x1.700d30aeac0e1p-4},
-    {0x1.15b1e5f75270dp-1, -0x1.4d3115d207eacp-4},    {0x1.135c81135c811p-1, -0x1.2aa04a44717a5p-4},
-    {0x1.1111111111111p-1, -0x1.08598b59e3a07p-4},    {0x1.0ecf56be69c9p-1, -0x1.ccb73cdddb2ccp-5},
-    {0x1.0c9714fbcda3bp-1, -0x1.894aa149fb343p-5},    {0x1.0a6810a6810a7p-1, -0x1.466aed42de3eap-5},
-    {0x1.0842108421084p-1, -0x1.0415d89e74444p-5},    {0x1.0624dd2f1a9fcp-1, -0x1.8492528c8cabfp-6},
-    {0x1.041041041041p-1, -0x1.0205658935847p-6},    {0x1.0204081020408p-1, -0x1.010157588de71p-7},
-    {0x1p-1, 0x0p+0}
-};
+// discarded), table-driven with the reduction centred on 1:
+//   t1 = hi(x) - kLogTabK (kLogTabK = hi word just above sqrt(2)/2), so
+//   k = t1 >> 20 is the exponent with x = 2^k m, m in [0.7072, 1.4143), and
+//   hi(m) = hi(x) - (t1 & 0xfff00000) (integer ops only);
+//   j = the next 9 bits of t1: 512 buckets of m, bucket j centred on
+//   c_j = (hi word kLogTabK + 2048 j + 1024, low word 0) — the bucket of m = 1
+//   has c = 1 exactly, so x near 1 keeps full relative accuracy;
+//   t = (m - c_j) / c_j with |t| <= 2^-10 (m - c_j exact by Sterbenz);
+//   log m = log c_j + log1p(t), log1p through t^6 (truncation < 2^-60 t);
+//   log x = k ln2_hi + (log c_j + (k ln2_lo + log1p t)), ln 2 split into a
+//   21-bit head (k ln2_hi exact) and a tail; |log x| >= ~0.35 whenever k != 0,
+//   so the sum never cancels. (1 / c_j, log c_j) come from a 512-entry table
+//   (log_table, correctly rounded from 80-bit precision) staged in shared
+//   memory. 15 FP64 and ~9 integer instructions per pair including the
+//   denominator and the accumulation, against 17 + ~14 for the 65-entry,
+//   degree-8 version before it; <= 1.5 ulp (tests/test_gpu_parity.py
+//   test_log_far_accuracy bounds it by 2 ulp over [2^-20, 4]).
+constexpr int kLogTabN = 512;
+constexpr int kLogTabK = 0x3FE6A400;  // (0x3FF00000 - kLogTabK) % 2048 == 1024: c = 1 is a bucket centre
+void log_table(double2* tab);         // host: kLogTabN entries (1 / c_j, log c_j)
+__host__ __device__ __forceinline__ double log_tab_node(int j) {
+#if defined(__CUDA_ARCH__)
+  return __hiloint2double(kLogTabK + (j << 11) + 1024, 0);
+#else
+  const unsigned long long bits = static_cast<unsigned long long>(static_cast<unsigned>(kLogTabK + (j << 11) + 1024))
+                                  << 32;
+  double d;
+  __builtin_memcpy(&d, &bits, 8);
+  return d;
+#endif
+}
 
 __device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab) {
   constexpr double kLn2Hi = 0x1.62e42p-1;           // ln 2, low 32 mantissa bits cleared
   constexpr double kLn2Lo = 0x1.fdf473de6af28p-22;  // ln 2 - kLn2Hi
   const int hi = __double2hiint(x);
-  const int mant = hi & 0xfffff;
-  const int j = (mant + 0x2000) >> 14;  // nearest node c_j = 1 + j / 64, j in [0, 64]
-  const int kk = (hi >> 20) - 1023 + (j >= 27 ? 1 : 0);
-  const double m = __hiloint2double(mant | 0x3ff00000, __double2loint(x));
-  const double c = __hiloint2double(0x3ff00000 + (j << 14), 0);
+  const int t1 = hi - kLogTabK;
+  const int kk = t1 >> 20;  // arithmetic shift: the exponent of x relative to m
+  const int j = (t1 >> 11) & (kLogTabN - 1);
+  const double m = __hiloint2double(hi - (t1 & static_cast<int>(0xfff00000u)), __double2loint(x));
   const double2 e = tab[j];
-  const double t = (m - c) * e.x;
-  double p = -1.0 / 8.0;
-  p = fma(t, p, 1.0 / 7.0);
-  p = fma(t, p, -1.0 / 6.0);
-  p = fma(t, p, 1.0 / 5.0);
+  const double t = (m - log_tab_node(j)) * e.x;
+  double p = fma(t, -1.0 / 6.0, 1.0 / 5.0);
   p = fma(t, p, -0.25);
   p = fma(t, p, 1.0 / 3.0);
   p = fma(t, p, -0.5);

@@ -29,9 +29,10 @@ __global__ void k_dfma_chain(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
 }
 
-__global__ void k_log_far(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+__global__ void k_log_far(const double* __restrict__ x, int64_t n, const double2* __restrict__ tab_g,
+                          double* __restrict__ out) {
   __shared__ double2 tab[kLogTabN];  // as the log tiles stage it
-  for (int j = threadIdx.x; j < kLogTabN; j += blockDim.x) tab[j] = kLogTab[j];
+  for (int j = threadIdx.x; j < kLogTabN; j += blockDim.x) tab[j] = tab_g[j];
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = log_tab(x[i], tab);
@@ -52,7 +53,7 @@ extern "C" int ssum_probe_log_far(ssum_ctx* h, const double* x, int64_t n, doubl
     DBuf<double> buf;
     buf.ensure(size_t(2 * n));
     SSUM_CUDA_CHECK(cudaMemcpyAsync(buf.p, x, size_t(n) * 8, cudaMemcpyHostToDevice, c->stream));
-    k_log_far<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(buf.p, n, buf.p + n);
+    k_log_far<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(buf.p, n, c->logtab.p, buf.p + n);
     SSUM_LAUNCH_CHECK();
     SSUM_CUDA_CHECK(cudaMemcpyAsync(out, buf.p + n, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
     SSUM_CUDA_CHECK(cudaStreamSynchronize(c->stream));

@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(NTH, MINB)
     k_tiles(const Tile* __restrict__ tiles, int ntiles, const int* __restrict__ sel,
             const SrcRange* __restrict__ ranges, const double4* __restrict__ pts, double* __restrict__ S,
             int* __restrict__ flags, const int* __restrict__ fit_nodes, const int* __restrict__ pslot,
-            const double* __restrict__ vinv, int P, double* __restrict__ coeff, int64_t npts) {
+            const double* __restrict__ vinv, int P, double* __restrict__ coeff, int64_t npts,
+            const double2* __restrict__ ltab_g) {
   constexpr int D = KDim<KER>::D;
   constexpr int kFU = MODE == kFitMode ? 2 : kFastUnroll;
   (void)npts;  // valid points in pts (bounds checks of the checked build)
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   constexpr int kChunk = CHUNK;
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
   int2* rtab = reinterpret_cast<int2*>(smem + kStages * sizeof(double4) * (kChunk + kPad));
-  double2* ltab = reinterpret_cast<double2*>(rtab + kRangeCap);  // log kernel: kLogTab staged
+  double2* ltab = reinterpret_cast<double2*>(rtab + kRangeCap);  // log kernel: log_table staged
   static_assert(sizeof(double) * NTH * D * kTpt <= kStages * sizeof(double4) * (kChunk + kPad), "red alias");
   static_assert(kPad <= NTH, "zero tail");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     for (int st = 0; st < kStages; ++st) buf[st][kChunk + tid] = zero4;
   }
   if constexpr (KER == kLOG)
-    for (int j = tid; j < kLogTabN; j += NTH) ltab[j] = kLogTab[j];
+    for (int j = tid; j < kLogTabN; j += NTH) ltab[j] = ltab_g[j];
   if (tid == 0) {
 #pragma unroll
     for (int st = 0; st < kStages; ++st) {
@@ -447,10 +448,17 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
                   static_cast<int>(n), 0, 1, static_cast<int>(n)};
 }
 
-template <int CHUNK>
+template <int KER, int CHUNK>
 constexpr size_t tile_smem() {
-  return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap + sizeof(double2) * kLogTabN;
+  return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap +
+         (KER == kLOG ? sizeof(double2) * kLogTabN : 0);
 }
+// the log tiles stream smaller chunks so that the 8 KB log table still fits
+// four blocks per SM
+#ifndef SSUM_LOG_CHUNK
+#define SSUM_LOG_CHUNK 640
+#endif
+constexpr int kLogChunk = SSUM_LOG_CHUNK;
 
 // k_tiles instantiation with its dynamic shared-memory limit raised. The
 // attribute belongs to the device (context), not the process: a per-device
@@ -463,7 +471,7 @@ auto tiles_kernel(int device) {
   if (!(ready.load(std::memory_order_acquire) & bit)) {
     SSUM_CUDA_CHECK(cudaFuncSetAttribute(k_tiles<KER, MODE, NTH, CHUNK, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(tile_smem<CHUNK>())));
+                                         static_cast<int>(tile_smem<KER, CHUNK>())));
     ready.fetch_or(bit, std::memory_order_acq_rel);
   }
   return k_tiles<KER, MODE, NTH, CHUNK, MINB>;
@@ -473,10 +481,16 @@ auto tiles_kernel(int device) {
 
 void launch_fit_tiles_on(Ctx& c, cudaStream_t stream, int kernel, int P, const Tile* tiles, int nfit, const int* sel,
                         const SrcRange* ranges, const int* fit_nodes, const int* pslot, double* coeff) {
-  auto k = kernel == kBS ? tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device)
-                          : tiles_kernel<kLOG, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device);
-  k<<<nfit, kFitThreads, tile_smem<kFitChunk>(), stream>>>(tiles, nfit, sel, ranges, c.pts.p, nullptr, c.d_flags.p,
-                                                           fit_nodes, pslot, c.vinv.p, P, coeff, c.npts);
+  if (kernel == kBS)
+    tiles_kernel<kBS, kFitMode, kFitThreads, kFitChunk, kFitMinB>(c.device)
+        <<<nfit, kFitThreads, tile_smem<kBS, kFitChunk>(), stream>>>(tiles, nfit, sel, ranges, c.pts.p, nullptr,
+                                                                   c.d_flags.p, fit_nodes, pslot, c.vinv.p, P, coeff,
+                                                                   c.npts, nullptr);
+  else
+    tiles_kernel<kLOG, kFitMode, kFitThreads, kLogChunk, kFitMinB>(c.device)
+        <<<nfit, kFitThreads, tile_smem<kLOG, kLogChunk>(), stream>>>(tiles, nfit, sel, ranges, c.pts.p, nullptr,
+                                                                    c.d_flags.p, fit_nodes, pslot, c.vinv.p, P, coeff,
+                                                                    c.npts, c.logtab.p);
 }
 
 void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, const int* sel) {
@@ -487,12 +501,21 @@ void launch_fit_tiles(Ctx& c, cudaStream_t stream, int kernel, int P, int nfit, 
 
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct) {
-  auto k = direct ? (kernel == kBS ? tiles_kernel<kBS, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device)
-                                   : tiles_kernel<kLOG, kDirectMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device))
-                  : (kernel == kBS ? tiles_kernel<kBS, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device)
-                                   : tiles_kernel<kLOG, kLeafMode, kLeafThreads, kLeafChunk, kLeafMinB>(c.device));
-  k<<<ntl, kLeafThreads, tile_smem<kLeafChunk>(), stream>>>(tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr,
-                                                nullptr, nullptr, 0, nullptr, c.npts);
+#define SSUM_LEAF_LAUNCH(K, M, CH, TAB)                                                                       \
+  tiles_kernel<K, M, kLeafThreads, CH, kLeafMinB>(c.device)<<<ntl, kLeafThreads, tile_smem<K, CH>(), stream>>>( \
+      tiles, ntl, nullptr, ranges, c.pts.p, S, c.d_flags.p, nullptr, nullptr, nullptr, 0, nullptr, c.npts, TAB)
+  if (kernel == kBS) {
+    if (direct)
+      SSUM_LEAF_LAUNCH(kBS, kDirectMode, kLeafChunk, nullptr);
+    else
+      SSUM_LEAF_LAUNCH(kBS, kLeafMode, kLeafChunk, nullptr);
+  } else {
+    if (direct)
+      SSUM_LEAF_LAUNCH(kLOG, kDirectMode, kLogChunk, c.logtab.p);
+    else
+      SSUM_LEAF_LAUNCH(kLOG, kLeafMode, kLogChunk, c.logtab.p);
+  }
+#undef SSUM_LEAF_LAUNCH
 }
 
 // Direct sum (treecode.cpp:246-264): every target against one range [0, n)

@@ -592,7 +592,11 @@ def test_log_far_accuracy(ss):
     edges = [2.0 ** -20, 0.25, 0.5, 1.0, 2.0, 4.0, np.sqrt(0.5), np.sqrt(2.0), np.nextafter(1.0, 0.0),
              np.nextafter(1.0, 2.0), 1 - 1e-9, 1 + 1e-9, np.nextafter(np.sqrt(0.5), 0.0),
              np.nextafter(np.sqrt(2.0), 4.0), 0.70710676, 1.4142135]
-    x = np.concatenate([x, edges])
+    # the table's reduction boundary (hi word 0x3FE6A400) and its bucket
+    # edges, densely around 1
+    bits = np.array([0x3FE6A400, 0x3FE6A3FF, 0x3FF6A400, 0x3FF6A3FF, 0x3FEFFC00, 0x3FF00400], np.uint64) << 32
+    near1 = rng.uniform(0.7, 1.42, 100_000)
+    x = np.concatenate([x, edges, bits.view(np.float64), np.nextafter(bits.view(np.float64), 0.0), near1])
     tree = ss.FaceTree(0)
     got = tree.probe_log_far(x)
     ref = np.log(x)
