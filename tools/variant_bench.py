@@ -1,7 +1,7 @@
 """Time the config-4 evaluation passes for each tuning build of the library
 (make -C paper_2401_07361_b200/csrc variants). One subprocess per library.
 
-    python tools/variant_bench.py [level]
+    python tools/variant_bench.py [level | c3 | c5]
 """
 import glob
 import json
@@ -14,15 +14,22 @@ CHILD = r"""
 import sys, json, statistics, torch
 sys.path.insert(0, '.')
 import paper_2401_07361_b200 as ss
-lvl = int(sys.argv[1])
-xyz, area = ss.make_icosa_mesh(lvl)
-q = ss.rh4_vorticity(xyz) * area
+arg = sys.argv[1]
+theta = 0.7
+if arg == 'c3':
+    xyz, zeta, area = ss.make_random_cap(1 << 22, 5)
+    q = zeta * area
+else:
+    if arg == 'c5':
+        arg, theta = '10', 0.8
+    xyz, area = ss.make_icosa_mesh(int(arg))
+    q = ss.rh4_vorticity(xyz) * area
 dev = torch.device('cuda', 0)
 dx, dq = torch.from_numpy(xyz).to(dev), torch.from_numpy(q).to(dev)
 out = torch.zeros((xyz.shape[0], 3), dtype=torch.float64, device=dev)
 tree = ss.FaceTree(0)
 tree.set_stream(torch.cuda.current_stream().cuda_stream)
-cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+cfg = ss.TraversalConfig(theta=theta, n_threshold=64, degree=8, max_depth=10)
 rows = []
 for k in range(8):
     st = ss.TreecodeStats()
