@@ -110,5 +110,8 @@ def test_config4_rk4_golden(ss, steps):
     print(f"\nc4 RK4 {steps} steps: sampled rel_l2 x {ex:.3e} zeta {ez:.3e}; "
           f"|x|-1 max {np.abs(np.linalg.norm(x, axis=1) - 1).max():.1e}")
     assert ex < REL_TOL and ez < REL_TOL
-    assert np.abs(x.sum(axis=0) - g["x_sum"]).max() <= 1e-9 * np.abs(g["x_sum"]).max() + 1e-9
+    # whole-field sums: the positions cancel to ~1e-4 over N unit vectors, so
+    # per-particle differences at the parity level (<= 1e-10) move the sum by
+    # up to ~1e-10 sqrt(N) (random signs)
+    assert np.abs(x.sum(axis=0) - g["x_sum"]).max() <= 1e-10 * np.sqrt(x.shape[0])
     assert abs(np.linalg.norm(z) - float(g["z_norm"])) <= 1e-10 * float(g["z_norm"])
