@@ -185,6 +185,17 @@ int ssum_tree_perm(ssum_ctx* ctx, int* dst, int on_device);
  * positions (part r = [cuts[r], cuts[r+1])). The ranks bin identically, so
  * every rank gets the same table without communicating. */
 int ssum_partition_cuts(ssum_ctx* ctx, int64_t* cuts);
+/* Sharded binning walk (multi-GPU): walks particles [i0, i1) of the caller's
+ * order (device xyz, all n rows) through the context's existing tree and
+ * returns device pointers to its per-particle leaf keys (uint64, n rows) and
+ * leaves (int32, n rows), each with room for `slots` >= n rows. The caller
+ * fills the other ranks' rows (one all-gather of equal slots per array); the
+ * next binning of these n particles (e.g. ssum_treecode_sum_device) then
+ * skips its walk and is bitwise the unsharded binning. *walked = 0 when the
+ * tree cannot be walked yet (first call on a tree): nothing to exchange, the
+ * next binning builds the tree itself. */
+int ssum_bin_walk_shard(ssum_ctx* ctx, const double* d_xyz, int64_t n, int64_t i0, int64_t i1, int64_t slots,
+                        void** keys, void** leaf_of, int* walked);
 /* Device-pointer evaluations write this part's rows in tree order (position
  * p0 + r to row r, rows past p1 - p0 untouched) instead of the caller's order
  * over all N rows: the rows one all-gather exchanges (tree_order = 1). */

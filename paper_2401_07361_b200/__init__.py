@@ -120,7 +120,7 @@ EXPORTED_SYMBOLS = (
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
     "ssum_rk4_step_end", "ssum_compute_proxy_weights", "ssum_last_rcond", "ssum_lattice_fit",
     "ssum_proxy_points", "ssum_partition_cuts", "ssum_set_output_order", "ssum_rk4_stage_end_rows",
-    "ssum_trim_memory",
+    "ssum_trim_memory", "ssum_bin_walk_shard",
 )
 
 
@@ -173,6 +173,8 @@ def load_library():
         "ssum_proxy_points": (ctypes.c_int, [_P, ctypes.c_int, _P]),
         "ssum_partition_cuts": (ctypes.c_int, [_P, _P]),
         "ssum_trim_memory": (ctypes.c_int, [ctypes.c_int]),
+        "ssum_bin_walk_shard": (ctypes.c_int, [_P, _P, _I64, _I64, _I64, _I64, ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                               ctypes.POINTER(ctypes.c_int)]),
         "ssum_set_output_order": (ctypes.c_int, [_P, ctypes.c_int]),
         "ssum_rk4_stage_end_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64, _P, _I64] + [_P] * 4),
     }
@@ -407,6 +409,17 @@ class FaceTree:
         out = np.zeros(getattr(self, "_nparts", 1) + 1, np.int64)
         self._check(self._lib.ssum_partition_cuts(self._h, _ptr(out)))
         return out
+
+    def bin_walk_shard(self, xyz_ptr: int, n: int, i0: int, i1: int, slots: int) -> Tuple[int, int, bool]:
+        """Walk particles [i0, i1) of the device positions through the
+        existing tree (multi-GPU sharded binning). Returns device pointers to
+        the context's per-particle leaf keys (uint64) and leaves (int32), each
+        with room for `slots` rows, and whether the walk ran; the caller fills
+        the other shards' rows before the next evaluation (dist.sharded_walk)."""
+        kp, lp, w = _P(), _P(), ctypes.c_int()
+        self._check(self._lib.ssum_bin_walk_shard(self._h, ctypes.c_void_p(xyz_ptr), int(n), int(i0), int(i1),
+                                                  int(slots), ctypes.byref(kp), ctypes.byref(lp), ctypes.byref(w)))
+        return kp.value or 0, lp.value or 0, bool(w.value)
 
     def set_output_order(self, tree_order: bool) -> None:
         """Device evaluations write this part's rows in tree order (row r =

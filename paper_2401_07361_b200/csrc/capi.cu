@@ -842,6 +842,26 @@ int ssum_rk4_stage_end(ssum_ctx* h, int stage, double omega, int64_t n, const do
   });
 }
 
+int ssum_bin_walk_shard(ssum_ctx* h, const double* d_xyz, int64_t n, int64_t i0, int64_t i1, int64_t slots,
+                        void** keys, void** leaf_of, int* walked) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (i0 < 0 || i1 < i0 || i1 > n || slots < n) throw Error(SSUM_INVALID, "bin_walk_shard: bad shard");
+    *walked = tree_walk_shard(c, d_xyz, n, i0, i1, slots) ? 1 : 0;
+    *keys = c.bins.wkey.p;
+    *leaf_of = c.bins.leaf_of.p;
+    if (*walked) {
+      int f = 0;  // a particle in no root face: the same GeometryError as the binning
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      if (f & kFlagGeometry) {
+        c.bins.walked_n = -1;
+        throw Error(SSUM_GEOMETRY, "bin_particles: particle contained in no root face");
+      }
+    }
+  });
+}
+
 int ssum_set_output_order(ssum_ctx* h, int tree_order) {
   return guarded(h, [&](Ctx& c) { c.out_tree_order = tree_order != 0; });
 }

@@ -146,6 +146,9 @@ struct Binned {
   DBuf<int> perm;           // tree position -> original particle id
   int64_t perm_n = -1;      // particle count perm is complete for (-1: none)
   bool input_coherent = true;  // last reuse binning: most consecutive inputs in one leaf
+  int64_t walked_n = -1;    // wkey / leaf_of of all walked_n particles filled by sharded walks
+                            // (ssum_bin_walk_shard + the caller's all-gather): the next binning
+                            // of walked_n particles skips its own walk
   DBuf<int> pos_leaf;       // tree position -> leaf node
   DBuf<int> sort_keys, sort_keys2, sort_vals;
   // level-synchronous descent: candidates of the current level, their split
@@ -383,6 +386,9 @@ Trace& trace();
 // ---- passes (tree.cu / traversal.cu / eval.cu) ------------------------------
 void tree_init_roots(Ctx& c);
 void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth);
+// One rank's share [i0, i1) of the binning walk (multi-GPU); false when the
+// tree cannot be walked yet (the next binning then builds it, replicated).
+bool tree_walk_shard(Ctx& c, const double* d_xyz, int64_t n, int64_t i0, int64_t i1, int64_t slots);
 void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_keys);
 void partition_targets(Ctx& c);
 bool plan_restriction(Ctx& c);  // multi-part: restrict this call's lists to the part's targets

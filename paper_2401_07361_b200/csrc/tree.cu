@@ -278,6 +278,11 @@ __device__ __forceinline__ bool deep_inside(const d3& p, const double* __restric
   return true;
 }
 
+__global__ void k_iota(int* __restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<int>(i);
+}
+
 __global__ void k_walk(const double* __restrict__ xyz, int64_t i0, int64_t i1, const int* __restrict__ order,
                        const double* __restrict__ tri,
                        const double* __restrict__ cramer, const double* __restrict__ center,
@@ -556,8 +561,15 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   // the previous call's leaf of each particle is the walk's first guess
   // (verified per particle, so any stale guess only costs the full walk)
   const int guess_nodes = prev_perm_n == n ? nn : 0;
+  const bool walked = B.walked_n == n;  // every rank walked its shard, the keys were all-gathered
+  B.walked_n = -1;
+  if (walked) {
+    k_iota<<<grid_for(n, bs), bs, 0, c.stream>>>(B.sort_vals.p, n);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
   if (c.io.active && pieces == 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[Ctx::kIoChunks - 1], 0));
-  for (int j = 0; j < pieces; ++j) {
+  for (int j = 0; j < (walked ? 0 : pieces); ++j) {
     const int64_t a = pieces > 1 ? c.io.bounds[j] : 0, b = pieces > 1 ? c.io.bounds[j + 1] : n;
     if (pieces > 1) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.xyz[j], 0));
     if (b <= a) continue;
@@ -602,6 +614,34 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   B.n_leaves = B.h_small[2];
   B.input_coherent = 2 * int64_t(B.h_small[3]) > n;
   B.perm_n = n;
+  return true;
+}
+
+// Multi-GPU binning: rank r walks only particles
+// [i0, i1) of the caller's order through the existing tree (the same k_walk,
+// previous leaves as guesses); the caller all-gathers the keys and leaves of
+// the other shards into this context's wkey / leaf_of (ssum_bin_walk_shard
+// hands out the pointers, slots >= n rows each), and the next binning of the
+// same n particles starts at the sort — bitwise the unsharded binning, with
+// the walk (the binning's largest part) divided by the rank count.
+bool tree_walk_shard(Ctx& c, const double* d_xyz, int64_t n, int64_t i0, int64_t i1, int64_t slots) {
+  NodeTable& T = c.nodes;
+  Binned& B = c.bins;
+  B.walked_n = -1;
+  if (T.count <= 20 || T.max_level > kKeyMaxLevel || n > 0x3fffffff || n <= 0) return false;
+  B.wkey.ensure(size_t(std::max(slots, n)));
+  B.leaf_of.ensure(size_t(std::max(slots, n)), true, c.stream);  // previous leaves: the guesses
+  B.sort_vals.ensure(std::max<size_t>(size_t(n), size_t(T.count)));
+  const int guess_nodes = B.perm_n == n ? T.count : 0;
+  SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, sizeof(int), c.stream));
+  if (i1 > i0) {
+    k_walk<<<grid_for(i1 - i0, 256), 256, 0, c.stream>>>(d_xyz, i0, i1, nullptr, T.tri.p, T.cramer.p, T.center.p,
+                                                          T.child_base.p, T.parent.p, T.key.p, B.wkey.p, B.sort_vals.p,
+                                                          B.leaf_of.p, guess_nodes, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches++;
+  }
+  B.walked_n = n;
   return true;
 }
 

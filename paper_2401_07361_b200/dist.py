@@ -6,6 +6,10 @@ cost-balanced contiguous range of target leaves (FaceTree.set_partition).
 Every rank bins identically, so every rank knows every part's tree-position
 range without communicating (FaceTree.partition_cuts).
 
+The binning's particle walk is sharded too (sharded_walk): each rank walks
+1/ws of the particles and one all-gather of the per-particle leaf keys
+completes every rank's binning.
+
 The one exchange per RK4 stage (§8(f) rank 2) is fused into the stage
 update: each rank's evaluation writes its rows in TREE order straight into
 a slot (FaceTree.set_output_order), ONE all-gather of equal-width slots
@@ -59,6 +63,42 @@ def assemble_rows(rows: torch.Tensor, width: int, cuts, perm: torch.Tensor, out:
         if b > a:
             out[perm[a:b].long()] = rows[r * width:r * width + (b - a)]
     return out
+
+
+class _DeviceArray:
+    """A raw device allocation of the library as a torch tensor view
+    (__cuda_array_interface__, no copy)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def slot_bounds(n: int, ws: int, rank: int) -> tuple:
+    """Rank `rank`'s equal slot [a, b) of n rows (m = ceil(n / ws) per slot)."""
+    m = -(-n // ws)
+    return min(n, rank * m), min(n, (rank + 1) * m), m
+
+
+def sharded_walk(tree, xyz_ptr: int, n: int, group: Optional[dist.ProcessGroup] = None,
+                 device: Optional[torch.device] = None) -> bool:
+    """Multi-GPU binning: this rank walks only its slot of
+    the particles through the tree (ssum_bin_walk_shard), then ONE all-gather
+    per array (leaf keys, leaves) completes every rank's copy; the next
+    evaluation of these n particles starts its binning at the sort, bitwise
+    the unsharded binning. Returns False when the tree could not be walked
+    yet (first call on a tree: every rank builds it)."""
+    ws = _ws(group)
+    r = dist.get_rank(group) if ws > 1 else 0
+    a, b, m = slot_bounds(n, ws, r)
+    kp, lp, walked = tree.bin_walk_shard(xyz_ptr, n, a, b, ws * m)
+    if not walked or ws == 1:
+        return walked
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    keys = torch.as_tensor(_DeviceArray(kp, ws * m, "<i8"), device=dev)
+    leaf = torch.as_tensor(_DeviceArray(lp, ws * m, "<i4"), device=dev)
+    for buf in (keys, leaf):
+        _all_gather_slots(buf, buf[r * m:(r + 1) * m], ws, group)
+    return True
 
 
 def gather_partitioned_rows(out: torch.Tensor, perm: torch.Tensor, p0: int, p1: int,
@@ -151,12 +191,14 @@ class TreecodeRK4Ops:
     reproduces it bit for bit and G ranks reproduce one rank bit for bit.
     `stats`: a list that receives each evaluation's TreecodeStats."""
 
-    def __init__(self, tree, cfg, group: Optional[dist.ProcessGroup] = None, stats: Optional[list] = None):
+    def __init__(self, tree, cfg, group: Optional[dist.ProcessGroup] = None, stats: Optional[list] = None,
+                 shard_binning: bool = True):
         from . import BiotSavartKernel, TreecodeStats, treecode_sum_device
 
         self.tree, self.cfg, self.group, self.stats = tree, cfg, group, stats
         self._k, self._eval, self._stats = BiotSavartKernel, treecode_sum_device, TreecodeStats
         self.ws = _ws(group)
+        self.shard_binning = shard_binning and self.ws > 1
         tree.set_stream(torch.cuda.current_stream().cuda_stream)
         tree.set_output_order(True)
         if self.ws > 1:
@@ -176,6 +218,8 @@ class TreecodeRK4Ops:
         t.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
                           st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
         stats = self._stats()
+        if self.shard_binning:  # each rank walks 1/ws of the particles, one all-gather of the keys
+            sharded_walk(t, st["xs"].data_ptr(), n, self.group, st["xs"].device)
         self._eval(t, self._k, self.cfg, st["xs"].data_ptr(), st["q"].data_ptr(), n, st["slot"].data_ptr(),
                    stats=stats)
         if self.stats is not None:

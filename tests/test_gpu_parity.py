@@ -603,3 +603,40 @@ def test_log_far_accuracy(ss):
     ulps = np.abs(got - ref) / np.spacing(np.abs(ref) + np.finfo(float).tiny)
     assert ulps.max() <= 2.0, (ulps.max(), x[np.argmax(ulps)])
     assert got[np.where(x == 1.0)[0][0]] == 0.0
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_sharded_walk_is_bitwise_the_full_binning(ss, mesh_fixture, G):
+    """Multi-GPU binning: each of G shards walks its slot of the particles
+    (ssum_bin_walk_shard) into one context — what the all-gather of the leaf
+    keys leaves on every rank — and the evaluation that follows must be the
+    unsharded one bit for bit (moving particles: previous leaves as guesses)."""
+    import torch
+    from paper_2401_07361_b200.dist import slot_bounds
+
+    xyz, q, _ = mesh_fixture(7)
+    n = xyz.shape[0]
+    rng = np.random.default_rng(G)
+    moved = xyz + 2e-3 * rng.standard_normal(xyz.shape)
+    moved /= np.linalg.norm(moved, axis=1, keepdims=True)
+    c = cfg(ss, deg=6)
+    dev = torch.device("cuda", 0)
+    out = {}
+    for mode in ("full", "sharded"):
+        t = ss.FaceTree(0)
+        t.set_stream(torch.cuda.current_stream().cuda_stream)
+        o = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+        for k, pos in enumerate((xyz, moved)):
+            x = torch.from_numpy(np.ascontiguousarray(pos)).to(dev)
+            qq = torch.from_numpy(q).to(dev)
+            if mode == "sharded":
+                for r in range(G):
+                    a, b, m = slot_bounds(n, G, r)
+                    kp, lp, walked = t.bin_walk_shard(x.data_ptr(), n, a, b, G * m)
+                    assert walked == (k > 0)  # the first call builds the tree
+            ss.treecode_sum_device(t, ss.BiotSavartKernel, c, x.data_ptr(), qq.data_ptr(), n, o.data_ptr())
+        torch.cuda.synchronize()
+        out[mode] = (o.cpu().numpy(), t.export())
+    assert np.array_equal(out["full"][0], out["sharded"][0])
+    for key in ("bin_offsets", "bin_ids", "leaf_of"):
+        assert np.array_equal(out["full"][1][key], out["sharded"][1][key])
