@@ -131,3 +131,23 @@ def test_default_stream_is_ordered(ss, mesh_fixture):
                                out.data_ptr())
         torch.cuda.synchronize()
         assert ol.rel_l2(out.cpu().numpy(), ref) < 1e-13
+
+
+def test_partitioned_host_call_keeps_other_rows(ss, mesh_fixture):
+    """A partitioned host-pointer call computes only its part's rows; every
+    other row of the caller's buffer must come back as it was."""
+    xyz, q, _ = mesh_fixture(6)
+    n = xyz.shape[0]
+    c = cfg(ss, deg=4)
+    full = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=ss.FaceTree())
+    t = ss.FaceTree()
+    t.set_partition(1, 3)
+    sentinel = np.full((n, 3), 7.25)
+    out = ss.treecode_sum(ss.BiotSavartKernel, xyz, q, c, tree=t, out=sentinel.copy())
+    p0, p1 = t.partition_range()
+    perm = t.perm()
+    mine = np.zeros(n, bool)
+    mine[perm[p0:p1]] = True
+    assert 0 < mine.sum() < n
+    assert np.array_equal(out[mine], full[mine])
+    assert np.all(out[~mine] == 7.25)
