@@ -96,6 +96,13 @@ __device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__
   const int ct = cnt[t], cs = cnt[s];
   int a = 0;
   if (ct > 0 && cs > 0 && off[t] < rhi && off[t] + ct > rlo) {
+    // two small bins interact directly whatever the MAC says: a
+    // well-separated pair is emitted with classify()'s kind, which is PP for
+    // two small bins (and stays PP in PC-only mode), the other case is the
+    // both-small PP rule (treecode.cpp:43-50) — so the MAC (an atan2, a
+    // square root, a division) is evaluated only where it can change the
+    // outcome (at C4 the last BFS step alone holds 3.6M leaf pairs)
+    if (ct <= thr && cs <= thr) return 4;
     const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
     const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
     const double R = arc_dist(a3, b3);
@@ -107,8 +114,6 @@ __device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__
     }
     if (well) {
       a = 4 | classify_kind(ct, cs, thr, pc_only);
-    } else if (ct <= thr && cs <= thr) {
-      a = 4;  // PP
     } else {
       const bool rt = ct > cs;
       const int r = rt ? t : s;
@@ -901,7 +906,16 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     g.theta = cfg.theta;
   }
   for (int round = 0;; ++round) {
-    if (!bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+    static const bool stepwise = [] {  // SSUM_BFS_STEPWISE=1: step by step, frontier sizes traced
+      const char* e = std::getenv("SSUM_BFS_STEPWISE");
+      return e && *e == '1';
+    }();
+    if (stepwise || !bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+    if (stepwise && trace().on) {
+      std::fprintf(stderr, "[ssum bfs] %zu steps, frontier:", S.plan_m.size());
+      for (const int m : S.plan_m) std::fprintf(stderr, " %d", m);
+      std::fprintf(stderr, " emissions %lld\n", ne);
+    }
     if (!resolve_mac(c)) break;
     if (round > 64) throw Error(SSUM_INTERNAL, "dual traversal: MAC guard band did not settle");
   }
