@@ -280,8 +280,12 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
     const int* __restrict__ perm, double* __restrict__ out, int64_t obase) {
   constexpr int D = KDim<KER>::D;
   constexpr int P = Sbb<DEG>::P;
-  constexpr int DP = D == 3 ? 4 : 1;  // staged row: (c_0, c_1, c_2, pad) per basis function
-  __shared__ __align__(16) double cs[kFinWarps][P * DP];
+  // staged coefficients, packed (c_0, c_1, c_2) per basis function: a pair
+  // of basis functions (m even, m + 1) is three LDS.128 (1.5 per function
+  // instead of an LDS.128 + LDS.64 each — the kernel is LSU-bound)
+  constexpr int DP = D == 3 ? 3 : 1;
+  constexpr int kRow = (P * DP + 1) & ~1;  // even: every warp's row starts 16-byte aligned
+  __shared__ __align__(16) double cs[kFinWarps][kRow];
   __shared__ __align__(16) double cr[kFinWarps][12];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
@@ -309,16 +313,28 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
         double q1[DEG + 1], q2[DEG + 1], q3[DEG + 1];
         powers<DEG>(b1, b2, b3, q1, q2, q3);
         int m = 0;
+        double n0 = 0.0, n1 = 0.0, n2 = 0.0;  // basis m + 1's coefficients, loaded with m's
 #pragma unroll
         for (int kk = 0; kk <= DEG; ++kk) {
 #pragma unroll
           for (int jj = 0; jj <= DEG - kk; ++jj, ++m) {
             const double B = q1[DEG - kk - jj] * q2[jj] * q3[kk];
             if constexpr (D == 3) {
-              const double2 c01 = *reinterpret_cast<const double2*>(&cs[w][m * 4]);
-              val[0] = fma(c01.x, B, val[0]);
-              val[1] = fma(c01.y, B, val[1]);
-              val[2] = fma(cs[w][m * 4 + 2], B, val[2]);
+              double c0, c1, c2;
+              if ((m & 1) == 0) {
+                const double2* r = reinterpret_cast<const double2*>(&cs[w][m * 3]);
+                const double2 a = r[0], b = r[1];
+                c0 = a.x, c1 = a.y, c2 = b.x;
+                if (m + 1 < P) {
+                  const double2 e = r[2];
+                  n0 = b.y, n1 = e.x, n2 = e.y;
+                }
+              } else {
+                c0 = n0, c1 = n1, c2 = n2;
+              }
+              val[0] = fma(c0, B, val[0]);
+              val[1] = fma(c1, B, val[1]);
+              val[2] = fma(c2, B, val[2]);
             } else {
               val[0] = fma(cs[w][m], B, val[0]);
             }
