@@ -37,6 +37,7 @@ void check_flags(Ctx& c, const char* where) {
   int f = 0;
   SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  c.last_flags = f;
   if (f & kFlagGeometry) throw Error(SSUM_GEOMETRY, std::string(where) + ": degenerate geometry");
   if (f & kFlagSingular)
     throw Error(SSUM_SINGULAR, std::string(where) + ": kernel evaluated at its singularity (1 - x.y <= 1e-14)");
@@ -112,12 +113,24 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
       c.prep_started = false;
     }
   } early{c};
-  c.early = Ctx::Early{d_xyz, d_q, cfg.degree, kernel == SSUM_BIOT_SAVART ? 3 : 1};
-  traverse_and_build_lists(c, cfg, false);
-  c.early = Ctx::Early{};
-  tr.mark("lists.done");
-  const auto t2 = clk::now();
-  evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
+  // Lists per target subtree (sublists.cu) when the binning made a plan;
+  // if they came out incomplete (a buffer outgrew, undecided MAC pairs) the
+  // evaluation is redone on the global traversal path (traversal.cu).
+  const bool sub = sub_lists_usable(c, cfg);
+  auto t2 = clk::now();
+  for (int attempt = 0;; ++attempt) {
+    c.early = Ctx::Early{d_xyz, d_q, cfg.degree, kernel == SSUM_BIOT_SAVART ? 3 : 1};
+    if (sub && attempt == 0)
+      build_lists_subtree(c, cfg);
+    else
+      traverse_and_build_lists(c, cfg, false);
+    c.early = Ctx::Early{};
+    tr.mark("lists.done");
+    t2 = clk::now();
+    evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
+    if (!sub_lists_redo(c, c.last_flags)) break;
+    SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, sizeof(int), c.stream));
+  }
   finalize_counts(c);
   tr.mark("eval.done");
   const auto t3 = clk::now();
@@ -354,6 +367,12 @@ int ssum_create(int device, ssum_ctx** out) {
     int prio_lo = 0, prio_hi = 0;
     SSUM_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SSUM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, prio_hi));
+    {  // the upward pass (start_prep): lowest priority by default, so the list
+       // builder's blocks are dispatched first and the FP64 work fills in
+      const char* v = std::getenv("SSUM_PREP_PRIO");
+      const int pr = (v && *v == 'h') ? prio_hi : prio_lo;
+      SSUM_CUDA_CHECK(cudaStreamCreateWithPriority(&c->prep_stream, cudaStreamNonBlocking, pr));
+    }
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     for (auto& e : c->side_ev) SSUM_CUDA_CHECK(cudaEventCreate(&e));
@@ -397,6 +416,7 @@ void ssum_destroy(ssum_ctx* h) {
   if (c->io.t1) cudaEventDestroy(c->io.t1);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->prep_stream) cudaStreamDestroy(c->prep_stream);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
   for (auto& e : c->side_ev) if (e) cudaEventDestroy(e);

@@ -619,15 +619,17 @@ void size_eval_buffers(Ctx& c, int degree, int D, int64_t n) {
 // so they run on side_stream while the main stream builds the range lists
 // and tiles (k_leaf_fill / k_fit_fill are latency-bound; the upward pass is
 // FP64 work). evaluate() joins on prep_ev.
-void start_prep(Ctx& c) {
+void start_prep(Ctx& c, bool forked) {
   if (!c.early.xyz || !c.early_prep || c.bins.n == 0) return;
   const int64_t n = c.bins.n;
   size_eval_buffers(c, c.early.degree, c.early.dim, n);
-  SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
-  SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.fork_ev, 0));
-  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.side_stream, c.io.q, 0));  // q of a host-pointer call
-  launch_prep(c, c.side_stream, c.cub_tmp_side, c.early.degree, c.early.xyz, c.early.q, n);
-  SSUM_CUDA_CHECK(cudaEventRecord(c.prep_ev, c.side_stream));
+  // forked: the caller recorded fork_ev (after sizing the buffers) before
+  // launching work the prep stream need not wait for
+  if (!forked) SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+  SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.prep_stream, c.fork_ev, 0));
+  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.prep_stream, c.io.q, 0));  // q of a host-pointer call
+  launch_prep(c, c.prep_stream, c.cub_tmp_side, c.early.degree, c.early.xyz, c.early.q, n);
+  SSUM_CUDA_CHECK(cudaEventRecord(c.prep_ev, c.prep_stream));
   c.prep_started = true;
 }
 

@@ -57,9 +57,12 @@ struct Error : std::runtime_error {
 constexpr int kMaxDegree = 20;  // kMaxSbbDegree (sbb.hpp:12)
 constexpr int kWarp = 32;
 constexpr double kSingularTol = 1e-14;  // kernels.hpp:13
+constexpr double kPi = 3.141592653589793;
 
 // Device error flags (bitmask in ctx.d_flags[0]).
-enum : int { kFlagGeometry = 1, kFlagSingular = 2 };
+// kFlagListsRedo: the subtree list builder (sublists.cu) ran out of room or
+// met undecided MAC pairs; the evaluation is redone on the global path.
+enum : int { kFlagGeometry = 1, kFlagSingular = 2, kFlagListsRedo = 8 };
 
 // Stream the device allocations of the current C-ABI call are ordered on
 // (the context's stream, set by the entry point): DBuf memory comes from the
@@ -236,7 +239,19 @@ struct PairEntry {
   int step, pad;
 };
 
+// Everything a pair decision reads about one node, packed per call (bin
+// counts change, and sh / ch depend on theta): circumcentre, radius,
+// sin / cos of radius / (2 theta) (the MAC screen, travdev.cuh), bin, level,
+// first child. 64 bytes: one node is two aligned 32-byte sectors.
+struct __align__(16) NodeRec {
+  double cx, cy, cz, r, sh, ch;
+  int cnt, off, level, child_base;
+};
+static_assert(sizeof(NodeRec) == 64, "NodeRec layout");
+
 struct TravScratch {
+  DBuf<NodeRec> rec;         // per call (build_node_records)
+  double rec_theta = -1.0;
   DBuf<PairEntry> F0, F1;
   DBuf<int> action;
   DBuf<unsigned long long> packed, scan;
@@ -272,8 +287,30 @@ struct MacGuard {
   int64_t resolved = 0;  // pairs decided on the host so far
 };
 
+// Subtree list plan (sublists.cu): made by each reuse binning (tree.cu),
+// consumed by build_lists_subtree.
+struct SubPlan {
+  bool valid = false;   // the last binning made the plan
+  bool used = false;    // this call's lists came from the subtree builder
+  int disabled = 0;     // SSUM_SUB_LISTS=0: global path only
+  int forced = 0;       // SSUM_SUB_LISTS=1: whenever the plan applies (else by size / restriction)
+  int thr = -1;         // N_T the big nodes were flagged with
+  int cmax = 0;         // largest cut-node bin (0: not set yet)
+  int n_big = 0, n_cut = 0, n_leaf_tiles = 0;
+  int smem = 0;
+  DBuf<unsigned char> big_flag, cut_flag;
+  DBuf<int> cut, tpl, tile_off;
+  DBuf<unsigned long long> up_visits, cursor;
+  int64_t leaf_cap = 0, fit_cap = 0;  // range buffer sizes
+  int64_t max_emit = 0, max_front = 0;  // last call's largest block emission count / frontier
+  int64_t redos = 0;
+};
+
 struct Ctx {
   int device = 0;
+  SubPlan sub;
+  int last_flags = 0;  // device error flags read by the last check_flags
+  int rt0 = 0, rt1 = 0;  // restricted call: this part's leaf tile range (subtree plan)
   TravScratch trav;
   MacGuard mac;
   cudaStream_t own_stream = nullptr;
@@ -336,6 +373,7 @@ struct Ctx {
   // disjoint buffers, and the leaf blocks fill the SMs the fit kernel's
   // tail leaves idle (eval.cu).
   cudaStream_t side_stream = nullptr;
+  cudaStream_t prep_stream = nullptr;  // gather + proxies + upward pass (start_prep)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, side_ev[2] = {}, leaf_ev[2] = {};
   bool overlap_tiles = true;
   // The gather + proxy points + upward pass start on side_stream from
@@ -394,6 +432,18 @@ void partition_targets(Ctx& c);
 bool plan_restriction(Ctx& c);  // multi-part: restrict this call's lists to the part's targets
 void build_lists(Ctx& c, const ssum_config& cfg);
 void finalize_counts(Ctx& c);
+// subtree list builder (sublists.cu)
+void plan_subtrees(Ctx& c, int thr, const int* d_nl, int* d_out);
+void plan_subtrees_done(Ctx& c, const int* h);
+bool sub_lists_usable(const Ctx& c, const ssum_config& cfg);
+void build_lists_subtree(Ctx& c, const ssum_config& cfg);
+bool sub_lists_redo(Ctx& c, int flags);
+// MAC guard band (traversal.cu): the device control block for a traversal
+// (resets the undecided-pair count), and the host decision of undecided pairs
+const void* mac_ctl_device(Ctx& c);
+// NodeRec of every node for this call's bins and theta (c.trav.rec)
+void build_node_records(Ctx& c, double theta);
+bool resolve_mac_host(Ctx& c);
 std::vector<int> reference_ids(const HostTree& h);
 const HostTree& host_tree(Ctx& c);  // downloads the node structure when stale
 void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, const double* d_q,
@@ -414,7 +464,8 @@ void proxy_weights(Ctx& c, int degree, const double* xyz, const double* q, int n
 // V^-1 of the degree-d lattice Vandermonde (row-major, P x P) and its exact
 // 1-norm reciprocal condition number (no throw; eval.cu)
 void lattice_inverse(int degree, std::vector<double>& inv, double& rcond);
-void start_prep(Ctx& c);
+void start_prep(Ctx& c, bool forked = false);
+void size_eval_buffers(Ctx& c, int degree, int D, int64_t n);
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct = false);
 void launch_direct(Ctx& c, int kernel, int64_t n, double* d_out);

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
   const int tix = sel ? sel[blockIdx.x] : static_cast<int>(blockIdx.x);
   const Tile T = tiles[tix];
+  if (MODE == kFitMode && T.total == 0) return;  // a big node without CP/CC pairs (subtree lists)
   const int tc = T.tgt_count;
   SSUM_DCHECK(tc >= 1 && tc <= kTileTargets && T.tgt_begin >= 0 && T.tgt_begin + tc <= npts);
   SSUM_DCHECK(T.list_begin >= 0 && T.list_end >= T.list_begin && T.near_total <= T.total);

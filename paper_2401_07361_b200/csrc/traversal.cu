@@ -27,104 +27,11 @@
 #include <cmath>
 
 #include "internal.cuh"
+#include "travdev.cuh"
 
 namespace ssum {
 
 namespace {
-
-constexpr int kKeyStepBits = 2;
-constexpr int kKeyMaxSteps = 27;  // 9 bits root pair + 2 bits x 27 steps = 63 bits
-
-// classify (treecode.cpp:29-36); pc_only remaps CP -> PP and CC -> PC.
-__device__ __forceinline__ int classify_kind(int nt_, int ns_, int thr, int pc_only) {
-  const bool tb = nt_ > thr, sb = ns_ > thr;
-  int k = 0;
-  if (tb && sb) k = 3;
-  else if (sb) k = 1;
-  else if (tb) k = 2;
-  if (pc_only) {
-    if (k == 2) k = 0;
-    if (k == 3) k = 1;
-  }
-  return k;
-}
-
-// MAC decisions exact by construction. R and the radii come from CUDA's
-// atan2 (<= 2 ulp) where the reference uses glibc's (< 1 ulp), so the
-// quotient (r_t + r_s)/R may differ from the reference's by a few ulp
-// (<= ~1e-15 relative). A decision can therefore differ only when the quotient
-// lies that close to theta. Every pair whose device quotient falls in the
-// guard band theta (1 +- band) (band = 1e-12 by default, ~5000 ulp) is looked
-// up in a table of host-made decisions; a pair missing from it is recorded,
-// takes the device decision provisionally, and the traversal is redone once
-// the host (glibc atan2, the reference's expressions: great_circle_distance,
-// triangle_radius, mac_well_separated, treecode.cpp:22-25) has decided it
-// (resolve_mac below). Outside the band the device decision is the
-// reference's; inside it the host's is.
-struct MacCtl {
-  const unsigned long long* keys;  // sorted (t << 33 | s << 1 | well)
-  int n;
-  double lo, hi;                   // theta (1 - band), theta (1 + band)
-  int2* amb;                       // undecided pairs (first amb_cap)
-  int* amb_n;
-  int amb_cap;
-};
-
-__device__ __noinline__ bool mac_lookup(const MacCtl& m, int t, int s, bool provisional) {
-  const unsigned long long k = (static_cast<unsigned long long>(t) << 33) | (static_cast<unsigned long long>(s) << 1);
-  int lo = 0, hi = m.n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((m.keys[mid] | 1ull) < k) lo = mid + 1;
-    else hi = mid;
-  }
-  if (lo < m.n && (m.keys[lo] >> 1) == (k >> 1)) return (m.keys[lo] & 1ull) != 0;
-  const int i = atomicAdd(m.amb_n, 1);
-  if (i < m.amb_cap) m.amb[i] = make_int2(t, s);
-  return provisional;
-}
-
-// action: bit0-1 kind, bit2 emit, bit3 refine, bit4 refine target
-// [rlo, rhi): the tree-position range whose targets this call evaluates
-// (restricted multi-part call; [0, INT_MAX) otherwise): a pair whose target
-// bin misses it only feeds other parts' targets and is dropped.
-__device__ __forceinline__ int pair_action(int t, int s, const int* __restrict__ cnt, const int* __restrict__ off,
-                                           int rlo, int rhi, const double* __restrict__ center,
-                                           const double* __restrict__ radius, const int* __restrict__ level,
-                                           const int* __restrict__ child_base, double theta, int thr, int max_depth,
-                                           int pc_only, const MacCtl* __restrict__ mac) {
-  const int ct = cnt[t], cs = cnt[s];
-  int a = 0;
-  if (ct > 0 && cs > 0 && off[t] < rhi && off[t] + ct > rlo) {
-    // two small bins interact directly whatever the MAC says: a
-    // well-separated pair is emitted with classify()'s kind, which is PP for
-    // two small bins (and stays PP in PC-only mode), the other case is the
-    // both-small PP rule (treecode.cpp:43-50) — so the MAC (an atan2, a
-    // square root, a division) is evaluated only where it can change the
-    // outcome (at C4 the last BFS step alone holds 3.6M leaf pairs)
-    if (ct <= thr && cs <= thr) return 4;
-    const d3 a3{center[3 * t], center[3 * t + 1], center[3 * t + 2]};
-    const d3 b3{center[3 * s], center[3 * s + 1], center[3 * s + 2]};
-    const double R = arc_dist(a3, b3);
-    bool well = false;
-    if (R > 0.0) {
-      const double qv = div_rn(add_rn(radius[t], radius[s]), R);
-      well = qv < theta;
-      if (qv > __ldg(&mac->lo) && qv < __ldg(&mac->hi)) well = mac_lookup(*mac, t, s, well);
-    }
-    if (well) {
-      a = 4 | classify_kind(ct, cs, thr, pc_only);
-    } else {
-      const bool rt = ct > cs;
-      const int r = rt ? t : s;
-      if (child_base[r] < 0 || level[r] >= max_depth)
-        a = 4;  // PP fallback
-      else
-        a = 8 | (rt ? 16 : 0);
-    }
-  }
-  return a;
-}
 
 // Emission / refinement of frontier entry p with action a at exclusive
 // prefix pos = (emissions before << 32) | (children slots before).
@@ -161,15 +68,15 @@ __global__ void k_trav_eval(const PairEntry* __restrict__ F, int m, const int* _
                             const double* __restrict__ radius,
                             const int* __restrict__ level, const int* __restrict__ child_base, double theta, int thr,
                             int max_depth, int pc_only, const MacCtl* mac, int* __restrict__ action,
-                            unsigned long long* __restrict__ packed) {
+                            unsigned long long* __restrict__ packed, const NodeRec* __restrict__ rec, double pi_theta) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k > m) return;
   if (k == m) {
     packed[k] = 0;
     return;
   }
-  const int a = pair_action(F[k].t, F[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
-                            max_depth, pc_only, mac);
+  int cb, tl;
+  const int a = pair_action_rec(F[k].t, F[k].s, rec, rlo, rhi, theta, pi_theta, thr, max_depth, pc_only, mac, &cb, &tl);
   action[k] = a;
   packed[k] = ((a & 4) ? (1ull << 32) : 0ull) | ((a & 8) ? 4ull : 0ull);
 }
@@ -217,7 +124,7 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
           int pc_only, const MacCtl* mac, PairEntry* F0, PairEntry* F1, int fcap, int4* __restrict__ E,
           unsigned long long* __restrict__ K, long long ecap, int* __restrict__ action,
           unsigned long long* __restrict__ loc, unsigned long long* btot, int* out, long long* ne_out,
-          int* flags) {
+          int* flags, const NodeRec* __restrict__ rec, double pi_theta) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   typedef cub::BlockScan<unsigned long long, kBfsThreads> BS;
@@ -238,9 +145,11 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
     // decide the whole slice first (no block-wide sync between pairs, so
     // each thread keeps several pairs' node loads in flight), then scan it
 #pragma unroll 4
-    for (int k = lo + tid; k < hi; k += kBfsThreads)
-      action[k] = pair_action(Fc[k].t, Fc[k].s, cnt, off, rlo, rhi, center, radius, level, child_base, theta, thr,
-                              max_depth, pc_only, mac);
+    for (int k = lo + tid; k < hi; k += kBfsThreads) {
+      int cb, tl;
+      action[k] = pair_action_rec(Fc[k].t, Fc[k].s, rec, rlo, rhi, theta, pi_theta, thr, max_depth, pc_only, mac, &cb,
+                                  &tl);
+    }
     for (int base = lo; base < hi; base += kBfsThreads) {
       const int k = base + tid;
       unsigned long long v = 0;
@@ -387,79 +296,6 @@ __global__ void k_leaf_count(const int* __restrict__ leaves, int nl, const int* 
   }
   n_ranges[k] = r;
   n_tiles[k] = (cnt[leaf] + kTileTargets - 1) / kTileTargets;
-}
-
-// May a pair (x in leaf, y in node s) have 1 - x.y < 2^-20? Only if the two
-// circumcircles come within kNearArc of each other (every binned point lies
-// in its node's circumcircle, up to the -1e-10 containment tolerance). The
-// test is on the chord (<= the arc), so it errs only towards "near".
-__device__ __forceinline__ bool near_possible(int leaf, int s, const double* __restrict__ center,
-                                              const double* __restrict__ radius) {
-  if (leaf == s) return true;
-  const double dx = center[3 * leaf] - center[3 * s], dy = center[3 * leaf + 1] - center[3 * s + 1],
-               dz = center[3 * leaf + 2] - center[3 * s + 2];
-  const double lim = radius[leaf] + radius[s] + kNearArc;
-  return fma(dx, dx, fma(dy, dy, dz * dz)) < lim * lim;
-}
-
-// Warp-cooperative append of one round of ranges (lane order = list order)
-// to a tile's range list. A range that continues the previous one in memory
-// with the same near flag is merged into it: the flattened source sequence
-// is unchanged, the list (and the kernels' binary searches) shorter —
-// sibling leaves' bins and sibling nodes' proxy blocks are contiguous.
-// Returns this lane's flattened-list prefix (valid for selected lanes).
-struct ListCursor {
-  int w = 0;          // ranges written
-  int src = 0;        // flattened sources so far
-  int last_end = -1;  // end (begin + count) and near flag of the last range
-  int last_near = -1;
-};
-__device__ __forceinline__ int append_ranges(bool sel, const SrcRange& r, SrcRange* __restrict__ out,
-                                             ListCursor& cur, int lane) {
-  const unsigned full = 0xffffffffu;
-  const unsigned bal = __ballot_sync(full, sel);
-  const int cnt = sel ? r.count : 0;
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(full, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int excl = incl - cnt;
-  const int total = __shfl_sync(full, incl, 31);
-  const int end = r.begin + r.count;
-  const unsigned below = bal & ((1u << lane) - 1u);
-  const int pl = below ? 31 - __clz(below) : -1;  // previous selected lane
-  const int pend = __shfl_sync(full, end, pl < 0 ? 0 : pl);
-  const int pnear = __shfl_sync(full, r.near, pl < 0 ? 0 : pl);
-  const int prev_end = pl < 0 ? cur.last_end : pend, prev_near = pl < 0 ? cur.last_near : pnear;
-  const bool cont = sel && (pl >= 0 || cur.w > 0) && prev_end == r.begin && prev_near == r.near;
-  const bool head = sel && !cont;
-  const unsigned hb = __ballot_sync(full, head);
-  const unsigned after = hb & ~((2u << lane) - 1u);  // heads after this lane (none for lane 31)
-  const int nh = after ? __ffs(after) - 1 : -1;
-  const int nh_excl = __shfl_sync(full, excl, nh < 0 ? 0 : nh);
-  if (head) {
-    SrcRange h = r;
-    h.count = (nh < 0 ? total : nh_excl) - excl;  // this range and its continuations
-    h.pad = cur.src + excl;
-    out[cur.w + __popc(hb & ((1u << lane) - 1u))] = h;
-  }
-  // continuations before this round's first head extend the last range
-  const int fh = hb ? __ffs(hb) - 1 : -1;
-  const int lead = fh < 0 ? total : __shfl_sync(full, excl, fh);
-  __syncwarp();
-  if (lane == 0 && lead > 0) out[cur.w - 1].count += lead;
-  __syncwarp();
-  const int ls = bal ? 31 - __clz(bal) : -1;  // last selected lane
-  if (ls >= 0) {
-    cur.last_end = __shfl_sync(full, end, ls);
-    cur.last_near = __shfl_sync(full, r.near, ls);
-  }
-  const int pad = cur.src + excl;
-  cur.w += __popc(hb);
-  cur.src += total;
-  return pad;
 }
 
 // Range list of one leaf, one warp per leaf: PP and PC entries of every node
@@ -682,6 +518,7 @@ static const MacCtl* mac_ctl(Ctx& c) {
   m.amb = g.amb.p;
   m.amb_n = g.amb_n.p;
   m.amb_cap = MacGuard::kAmbCap;
+  m.screen = std::max(1e-9, 4.0 * g.band);
   // pageable source: staged before the call returns, so m may go out of scope
   SSUM_CUDA_CHECK(cudaMemcpyAsync(g.ctl.p, &m, sizeof(m), cudaMemcpyHostToDevice, c.stream));
   SSUM_CUDA_CHECK(cudaMemsetAsync(g.amb_n.p, 0, sizeof(int), c.stream));
@@ -750,6 +587,39 @@ static bool resolve_mac(Ctx& c) {
   return true;
 }
 
+const void* mac_ctl_device(Ctx& c) { return mac_ctl(c); }
+
+namespace {
+__global__ void k_node_records(int nn, const double* __restrict__ center, const double* __restrict__ radius,
+                               const int* __restrict__ cnt, const int* __restrict__ off, const int* __restrict__ level,
+                               const int* __restrict__ child_base, double half_inv_theta, NodeRec* __restrict__ rec) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  NodeRec r;
+  r.cx = center[3 * i];
+  r.cy = center[3 * i + 1];
+  r.cz = center[3 * i + 2];
+  r.r = radius[i];
+  sincos(r.r * half_inv_theta, &r.sh, &r.ch);
+  r.cnt = cnt[i];
+  r.off = off[i];
+  r.level = level[i];
+  r.child_base = child_base[i];
+  rec[i] = r;
+}
+}  // namespace
+
+void build_node_records(Ctx& c, double theta) {
+  const int nn = c.nodes.count;
+  c.trav.rec.ensure(size_t(std::max(nn, 1)));
+  k_node_records<<<grid_for(nn, 256), 256, 0, c.stream>>>(nn, c.nodes.center.p, c.nodes.radius.p, c.bins.cnt.p,
+                                                          c.bins.off.p, c.nodes.level.p, c.nodes.child_base.p,
+                                                          0.5 / theta, c.trav.rec.p);
+  SSUM_LAUNCH_CHECK();
+  c.launches++;
+}
+bool resolve_mac_host(Ctx& c) { return resolve_mac(c); }
+
 // Breadth-first traversal with one host read per step (the frontier size
 // sizes the next step). Records the step sizes as the plan for the next call.
 static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
@@ -778,7 +648,7 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
                                                            c.nodes.radius.p,
                                                            c.nodes.level.p, c.nodes.child_base.p, cfg.theta,
                                                            cfg.n_threshold, cfg.max_depth, cfg.pc_only, mac,
-                                                           S.action.p, S.packed.p);
+                                                           S.action.p, S.packed.p, S.rec.p, kPi * cfg.theta * (1.0 - 1e-12));
     SSUM_LAUNCH_CHECK();
     c.launches++;
     exclusive_scan(c, S.packed.p, S.scan.p, m + 1);  // packed[m] = 0: totals at scan[m]
@@ -864,9 +734,11 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
   int* out = S.dm.p;
   long long* ne = S.debase.p;
   int* flags = c.d_flags.p;
+  const NodeRec* rec = S.rec.p;
+  double pi_theta = kPi * cfg.theta * (1.0 - 1e-12);
   void* args[] = {&cnt, &off, &rlo, &rhi, &center, &radius, &level, &child_base, &theta, &thr, &max_depth,
                   &pc_only, &mac, &f0, &f1,
-                  &fcap, &e, &k, &ecap, &action, &loc, &btot, &out, &ne, &flags};
+                  &fcap, &e, &k, &ecap, &action, &loc, &btot, &out, &ne, &flags, &rec, &pi_theta};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs), dim3(nb), dim3(kBfsThreads), args, 0, c.stream) !=
       cudaSuccess) {
     (void)cudaGetLastError();
@@ -905,6 +777,7 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     g.keys.clear();
     g.theta = cfg.theta;
   }
+  build_node_records(c, cfg.theta);
   for (int round = 0;; ++round) {
     static const bool stepwise = [] {  // SSUM_BFS_STEPWISE=1: step by step, frontier sizes traced
       const char* e = std::getenv("SSUM_BFS_STEPWISE");
@@ -1116,7 +989,8 @@ void finalize_counts(Ctx& c) {
 // every cut position x = pos[r] (r = 0 .. m-1): out[r] its tree position,
 // out[m + r] its leaf index.
 __global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* __restrict__ off, long long n,
-                            const long long* __restrict__ pos, int m, long long* out) {
+                            const long long* __restrict__ pos, int m, long long* out,
+                            const int* __restrict__ tile_off, long long* tout) {
   const int r = threadIdx.x;
   if (r >= m) return;
   const long long x = pos[r];
@@ -1130,6 +1004,7 @@ __global__ void k_snap_cuts(const int* __restrict__ leaves, int nl, const int* _
   }
   out[r] = lo < nl ? off[leaves[lo]] : n;
   out[m + r] = lo;
+  if (tile_off) tout[r] = tile_off[lo];  // subtree plan: the leaf's first tile
 }
 
 // Restricted multi-part call: once a full multi-part call has placed the
@@ -1146,15 +1021,19 @@ bool plan_restriction(Ctx& c) {
   c.part_pos.assign({0, B.n});
   if (c.nparts <= 1 || c.cuts.n != B.n || c.cuts.nparts != c.nparts || B.n_leaves == 0) return false;
   const int m = c.nparts + 1;
-  c.snap.ensure(size_t(3 * m));
-  std::vector<long long> h(size_t(2 * m));
+  c.snap.ensure(size_t(4 * m));
+  std::vector<long long> h(size_t(3 * m));
   for (int r = 0; r < m; ++r) h[size_t(r)] = c.cuts.pos[size_t(r)];
   SSUM_CUDA_CHECK(cudaMemcpyAsync(c.snap.p + 2 * m, h.data(), size_t(m) * 8, cudaMemcpyHostToDevice, c.stream));
+  const int* tile_off = c.sub.valid ? c.sub.tile_off.p : nullptr;
   k_snap_cuts<<<1, ((m + 31) / 32) * 32, 0, c.stream>>>(B.d_leaves.p, B.n_leaves, B.off.p, B.n, c.snap.p + 2 * m, m,
-                                                        c.snap.p);
+                                                        c.snap.p, tile_off, c.snap.p + 3 * m);
   SSUM_LAUNCH_CHECK();
   c.launches++;
   SSUM_CUDA_CHECK(cudaMemcpyAsync(h.data(), c.snap.p, size_t(2 * m) * 8, cudaMemcpyDeviceToHost, c.stream));
+  if (tile_off)
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(h.data() + 2 * m, c.snap.p + 3 * m, size_t(m) * 8, cudaMemcpyDeviceToHost,
+                                    c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   c.part_pos.assign(h.begin(), h.begin() + m);
   c.part_pos.front() = 0;
@@ -1162,6 +1041,10 @@ bool plan_restriction(Ctx& c) {
   c.rp1 = h[size_t(c.part) + 1];
   c.rl0 = static_cast<int>(h[size_t(m + c.part)]);
   c.rl1 = static_cast<int>(h[size_t(m + c.part) + 1]);
+  if (tile_off) {
+    c.rt0 = static_cast<int>(h[size_t(2 * m + c.part)]);
+    c.rt1 = static_cast<int>(h[size_t(2 * m + c.part) + 1]);
+  }
   c.restrict_on = true;
   return true;
 }

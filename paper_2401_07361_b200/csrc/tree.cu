@@ -548,8 +548,10 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   B.d_leaves.ensure(size_t(nn));
   B.leaf_pos.ensure(size_t(nn));
   B.leaf_flag.ensure(size_t(n));
-  int* d_cnt = c.d_flags.p + 16;  // [0] splits needed, [1] leaves, [2] input-order coherence
-  SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 3 * sizeof(int), c.stream));
+  // [0] splits needed, [1] leaves, [2] input-order coherence, [3..5] the
+  // subtree list plan's big nodes, cut nodes, leaf tiles
+  int* d_cnt = c.d_flags.p + 16;
+  SSUM_CUDA_CHECK(cudaMemsetAsync(d_cnt, 0, 6 * sizeof(int), c.stream));
   // Walk order: input order when the input is spatially coherent (the last
   // call found most consecutive particles in one leaf) — a host-pointer call
   // then walks each input piece as soon as it has landed — else the previous
@@ -604,16 +606,18 @@ static bool bin_reuse(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_de
   k_pos_leaf<<<grid_for(n, bs), bs, 0, c.stream>>>(B.perm.p, n, B.leaf_of.p, B.pos_leaf.p);
   SSUM_LAUNCH_CHECK();
   c.launches += 12;
+  plan_subtrees(c, nt, d_cnt + 1, d_cnt + 3);
   SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   k_coherence<<<grid_for(n, 1024), 1024, 0, c.stream>>>(B.leaf_of.p, n, d_cnt + 2);
   SSUM_LAUNCH_CHECK();
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, d_cnt, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(B.h_small + 1, d_cnt, 6 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
   if (B.h_small[0] & kFlagGeometry) check_flags(c, "bin_particles: particle contained in no root face");
   if (B.h_small[1] > 0) return false;
   B.n_leaves = B.h_small[2];
   B.input_coherent = 2 * int64_t(B.h_small[3]) > n;
   B.perm_n = n;
+  plan_subtrees_done(c, B.h_small + 4);
   return true;
 }
 
@@ -653,6 +657,7 @@ void tree_bin(Ctx& c, const double* d_xyz, int64_t n, int nt, int max_depth) {
   B.perm_n = -1;
   c.call_index++;
   c.host.valid = false;
+  c.sub.valid = false;
   B.n = n;
   B.n_leaves = 0;
   B.level_span.clear();
