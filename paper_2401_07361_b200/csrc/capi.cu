@@ -380,6 +380,7 @@ int ssum_create(int device, ssum_ctx** out) {
     SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&c->prep_ev, cudaEventDisableTiming));
     if (const char* v = std::getenv("SSUM_OVERLAP_TILES")) c->overlap_tiles = std::atoi(v) != 0;
     if (const char* v = std::getenv("SSUM_EARLY_PREP")) c->early_prep = std::atoi(v) != 0;
+    if (const char* v = std::getenv("SSUM_PLAN_LISTS")) c->plan_lists_ok = std::atoi(v) != 0;
     if (const char* v = std::getenv("SSUM_MAC_BAND")) c->mac.band = std::atof(v);
     for (auto& e : c->io.xyz) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : c->io.out) SSUM_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(32 * kUpWarps, SSUM_UP_MINB) k_up_partial(cons
   constexpr int P = Sbb<DEG>::P;
   __shared__ double tr[kUpWarps][32][33];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int chunk = blockIdx.x * kUpWarps + wp;
-  if (chunk >= *nchunks) return;  // warp-uniform
+  // grid-stride over the chunks: a small grid leaves room on every SM for
+  // the latency-bound list kernels running beside the upward pass
+  const int nch = *nchunks;
+  for (int chunk = blockIdx.x * kUpWarps + wp; chunk < nch; chunk += gridDim.x * kUpWarps) {  // warp-uniform
   const int4 ch = chunks[chunk];  // node, begin, count
   const double* k = cramer + 12 * ch.x;
   double kc[10];
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(32 * kUpWarps, SSUM_UP_MINB) k_up_partial(cons
       wpart[size_t(chunk) * P + g + lane] = s;
     }
     __syncwarp();
+  }
   }
 }
 
@@ -415,7 +418,17 @@ void launch_finish(Ctx& c, int degree, double* d_out, const int* inv = nullptr, 
 
 // nchunks: host upper bound (grid size); d_nchunks: the device-side count.
 void launch_up_partial(Ctx& c, cudaStream_t stream, int degree, int nchunks, const int* d_nchunks) {
-  const unsigned grid = static_cast<unsigned>((nchunks + kUpWarps - 1) / kUpWarps);
+  unsigned grid = static_cast<unsigned>((nchunks + kUpWarps - 1) / kUpWarps);
+  // SSUM_UP_GRID=k: at most k blocks per SM (grid-stride over the chunks)
+  static const int per_sm = [] {
+    const char* v = std::getenv("SSUM_UP_GRID");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (per_sm > 0) {
+    int sms = 0;
+    SSUM_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    grid = std::min<unsigned>(grid, static_cast<unsigned>(sms * per_sm));
+  }
 #define SSUM_UP_CASE(DG)                                                                                  \
   case DG:                                                                                                \
     k_up_partial<DG><<<grid, 32 * kUpWarps, 0, stream>>>(c.wchunks.p, d_nchunks, c.pts.p, c.nodes.cramer.p,   \

@@ -385,6 +385,10 @@ struct Ctx {
     int degree = 0, dim = 0;
   } early;
   bool prep_started = false;
+  // global-path lists on the binning's plan (traversal.cu): proxy slots for
+  // every big node, upward pass started before the traversal
+  bool plan_lists = false;
+  bool plan_lists_ok = true;  // SSUM_PLAN_LISTS=0: slots from the traversal's marks
   bool early_prep = true;
   cudaEvent_t prep_ev = nullptr;
   DBuf<unsigned char> cub_tmp_side;

@@ -211,20 +211,30 @@ __global__ void __launch_bounds__(kBfsThreads, SSUM_BFS_MINB)
 
 // Upward / downward pass visits: bin sizes of the weight nodes and of the
 // fit nodes (counters[0], counters[1]).
+// is_fit (planned lists: fit_nodes lists every big node): only the fit
+// nodes count, and their number goes to counters[-2].
 __global__ void k_visits(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ fit_nodes, int nf,
-                         const int* __restrict__ cnt, unsigned long long* counters) {
+                         const int* __restrict__ cnt, unsigned long long* counters,
+                         const unsigned char* __restrict__ is_fit) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long up = 0, down = 0;
-  if (k < nw) up = static_cast<unsigned long long>(cnt[weight_nodes[k]]);
-  else if (k < nw + nf) down = static_cast<unsigned long long>(cnt[fit_nodes[k - nw]]);
+  unsigned long long up = 0, down = 0, nfit = 0;
+  if (k < nw) {
+    up = static_cast<unsigned long long>(cnt[weight_nodes[k]]);
+  } else if (k < nw + nf) {
+    const int id = fit_nodes[k - nw];
+    if (!is_fit || is_fit[id]) down = static_cast<unsigned long long>(cnt[id]), nfit = 1;
+  }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   up = BR(tmp).Sum(up);
   __syncthreads();
   down = BR(tmp).Sum(down);
+  __syncthreads();
+  nfit = BR(tmp).Sum(nfit);
   if (threadIdx.x == 0) {
     if (up) atomicAdd(&counters[0], up);
     if (down) atomicAdd(&counters[1], down);
+    if (is_fit && nfit) atomicAdd(&counters[-2], nfit);
   }
 }
 
@@ -689,7 +699,9 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
 #ifndef SSUM_BFS_PER_SM
 #define SSUM_BFS_PER_SM 4
 #endif
-    S.bfs_blocks = sms * std::min(per_sm, SSUM_BFS_PER_SM);
+    int want = SSUM_BFS_PER_SM;
+    if (const char* v = std::getenv("SSUM_BFS_PER_SM_RT")) want = std::max(1, std::atoi(v));
+    S.bfs_blocks = sms * std::min(per_sm, want);
     if (S.bfs_blocks <= 0) S.bfs_blocks = -1;
   }
   if (S.bfs_blocks < 0) return false;
@@ -778,6 +790,15 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     g.theta = cfg.theta;
   }
   build_node_records(c, cfg.theta);
+  // planned lists (the binning's subtree plan gave every big node a proxy
+  // slot): the upward pass needs nothing from the traversal, so it starts
+  // now and runs beside it; fit tiles are indexed by slot
+  c.plan_lists = !keep_order_keys && c.sub.valid && c.sub.thr == cfg.n_threshold && c.sub.n_big > 0 &&
+                 c.plan_lists_ok;
+  if (c.plan_lists) {
+    L.n_proxy = L.n_weight = c.sub.n_big;
+    start_prep(c);
+  }
   for (int round = 0;; ++round) {
     static const bool stepwise = [] {  // SSUM_BFS_STEPWISE=1: step by step, frontier sizes traced
       const char* e = std::getenv("SSUM_BFS_STEPWISE");
@@ -850,6 +871,15 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     c.launches++;
   }
 
+  const bool planned = c.plan_lists;
+  if (planned) {
+    // slots, weight nodes (every big node) from the plan; fit tiles for every
+    // big node, indexed by slot (a node without CP/CC pairs gets an empty tile)
+    L.n_proxy = L.n_weight = L.n_fit = c.sub.n_big;
+    L.fit_nodes.ensure(size_t(std::max(c.sub.n_big, 1)));
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(L.fit_nodes.p, L.weight_nodes.p, size_t(c.sub.n_big) * 4, cudaMemcpyDeviceToDevice,
+                                    c.stream));
+  } else {
   // ---- proxy slots (weight or fit nodes), slot-ordered node lists
   S.flag.ensure(size_t(nn));
   S.flag_scan.ensure(size_t(nn));
@@ -887,7 +917,8 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
     L.n_weight = tail[2];
     L.n_fit = tail[3];
   }
-  start_prep(c);  // gather + proxies + upward on side_stream, overlapping the rest
+  start_prep(c);  // gather + proxies + upward on the prep stream, overlapping the rest
+  }
 
   trace().mark("lists.group_slots");
   // ---- range and tile counts for leaves and fit nodes, one read-back
@@ -955,7 +986,8 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
   // downward passes
   if (L.n_weight + nf > 0) {
     k_visits<<<grid_for(L.n_weight + nf, 256), 256, 0, c.stream>>>(L.weight_nodes.p, L.n_weight, L.fit_nodes.p, nf,
-                                                                  B.cnt.p, S.counters.p + 10);
+                                                                  B.cnt.p, S.counters.p + 10,
+                                                                  planned ? L.is_fit.p : nullptr);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }
@@ -980,6 +1012,7 @@ void finalize_counts(Ctx& c) {
   }
   L.visits[0] = h[10];
   L.visits[1] = h[11];
+  if (c.plan_lists) L.n_fit = static_cast<int>(h[8]);  // fit nodes among the big nodes (k_visits)
   if (L.local_is_all)
     for (int k = 0; k < 4; ++k) L.local_evals[k] = L.evals[k];
   L.counts_pending = false;

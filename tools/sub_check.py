@@ -34,7 +34,10 @@ def inputs(case):
 
 
 def run(case, xyz0, q, calls, sub):
-    os.environ["SSUM_SUB_LISTS"] = "1" if sub else "0"
+    """sub: True the subtree builder, False the global path, "noplan" the
+    global path with traversal-marked slots (SSUM_PLAN_LISTS=0)."""
+    os.environ["SSUM_SUB_LISTS"] = "1" if sub is True else "0"
+    os.environ["SSUM_PLAN_LISTS"] = "0" if sub == "noplan" else "1"
     dev = torch.device("cuda", 0)
     tree = ss.FaceTree(0)
     tree.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -71,10 +74,12 @@ def main():
         t0 = time.time()
         a, ta = run(case, xyz, q, 6, True)
         b, tb = run(case, xyz, q, 6, False)
-        same = [bool(np.array_equal(x, y)) for x, y in zip(a, b)]
+        c, tc = run(case, xyz, q, 6, "noplan")
+        same = [bool(np.array_equal(x, y) and np.array_equal(x, z)) for x, y, z in zip(a, b, c)]
         ok &= all(same)
         print(f"{name}: N={xyz.shape[0]} bitwise {same} | sub ms {[round(t, 3) for t in ta]} | "
-              f"global ms {[round(t, 3) for t in tb]} ({time.time() - t0:.1f} s)", flush=True)
+              f"global ms {[round(t, 3) for t in tb]} | global unplanned ms {[round(t, 3) for t in tc]} "
+              f"({time.time() - t0:.1f} s)", flush=True)
         if not all(same):
             for k, (x, y) in enumerate(zip(a, b)):
                 if not np.array_equal(x, y):
