@@ -231,6 +231,15 @@ int ssum_rk4_step_end(ssum_ctx* ctx, double dt, int64_t n, double* d_x0, double*
  * assembled field. */
 int ssum_rk4_stage_end_rows(ssum_ctx* ctx, int stage, double omega, int64_t n, const double* d_rows,
                             int64_t width, double* d_k, double* d_kz, double* d_acc, double* d_accz);
+/* ssum_rk4_stage_end_rows of `stage` fused with ssum_rk4_stage_begin of
+ * stage + 1 (none after stage 3): per particle, its row gathered through the
+ * inverse permutation, the accumulators advanced and the next stage's
+ * positions / strengths formed; d_k / d_kz (both or neither) receive k and
+ * kz when given. Bitwise the two calls. */
+int ssum_rk4_stage_advance_rows(ssum_ctx* ctx, int stage, double dt, double omega, int64_t n, const double* d_rows,
+                                int64_t width, const double* d_x0, const double* d_z0, const double* d_area,
+                                double* d_k, double* d_kz, double* d_acc, double* d_accz, double* d_xs,
+                                double* d_q);
 
 /* ---- measurement --------------------------------------------------------- */
 /* FP64 roofline denominator: DFMA-chain throughput of this device in TFLOP/s

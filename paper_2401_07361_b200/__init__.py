@@ -120,7 +120,7 @@ EXPORTED_SYMBOLS = (
     "ssum_tree_perm", "ssum_eval_interaction", "ssum_rk4_stage_begin", "ssum_rk4_stage_end",
     "ssum_rk4_step_end", "ssum_compute_proxy_weights", "ssum_last_rcond", "ssum_lattice_fit",
     "ssum_proxy_points", "ssum_partition_cuts", "ssum_set_output_order", "ssum_rk4_stage_end_rows",
-    "ssum_trim_memory", "ssum_bin_walk_shard",
+    "ssum_trim_memory", "ssum_bin_walk_shard", "ssum_rk4_stage_advance_rows",
 )
 
 
@@ -177,6 +177,8 @@ def load_library():
                                                ctypes.POINTER(ctypes.c_int)]),
         "ssum_set_output_order": (ctypes.c_int, [_P, ctypes.c_int]),
         "ssum_rk4_stage_end_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, _I64, _P, _I64] + [_P] * 4),
+        "ssum_rk4_stage_advance_rows": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_double, ctypes.c_double, _I64, _P,
+                                                       _I64] + [_P] * 9),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -433,6 +435,17 @@ class FaceTree:
         v = ctypes.c_void_p
         self._check(self._lib.ssum_rk4_stage_end_rows(self._h, int(stage), float(omega), int(n), v(rows),
                                                       int(width), v(k), v(kz), v(acc), v(accz)))
+
+    def rk4_stage_advance_rows(self, stage: int, dt: float, omega: float, n: int, rows: int, width: int, x0: int,
+                               z0: int, area: int, acc: int, accz: int, xs: int, q: int, k: int = 0,
+                               kz: int = 0) -> None:
+        """rk4_stage_end_rows of `stage` fused with rk4_stage_begin of stage + 1
+        (device pointers; k / kz optional, 0 = not written; see
+        ssum_rk4_stage_advance_rows)."""
+        v = lambda p: ctypes.c_void_p(p or None)  # noqa: E731
+        self._check(self._lib.ssum_rk4_stage_advance_rows(self._h, int(stage), float(dt), float(omega), int(n),
+                                                          v(rows), int(width), v(x0), v(z0), v(area), v(k), v(kz),
+                                                          v(acc), v(accz), v(xs), v(q)))
 
     def perm(self, device_ptr: Optional[int] = None) -> Optional[np.ndarray]:
         """Tree position -> particle index of the last binning (host copy, or

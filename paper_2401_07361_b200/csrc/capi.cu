@@ -312,6 +312,70 @@ __global__ void k_rk4_accum_rows(int64_t n, int stage, double omega, const doubl
   accz[i] = stage == 0 ? kzv : add_rn(accz[i], mul_rn(w, kzv));
 }
 
+// k_rk4_accum_rows fused with the next stage's k_rk4_stage (cs >= 0): one
+// thread per PARTICLE i, its row gathered from tree position inv[i] (one
+// scattered 24-byte read instead of four scattered read-modify-writes), all
+// other arrays coalesced; k / kz written only when given. Same arithmetic in
+// the same order as the two kernels.
+__global__ void k_rk4_advance_rows(int64_t n, int stage, double omega, double cs, const double* __restrict__ rows,
+                                   int64_t W, const long long* __restrict__ cuts, int np, const int* __restrict__ inv,
+                                   const double* __restrict__ x0, const double* __restrict__ z0,
+                                   const double* __restrict__ area, double* __restrict__ acc,
+                                   double* __restrict__ accz, double* __restrict__ k, double* __restrict__ kz,
+                                   double* __restrict__ xs, double* __restrict__ q, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* u = rows + 3 * i;  // no inv: the velocities in the caller's order (ssum_rk4)
+  if (inv) {
+    const int64_t j = inv[i];
+    int lo = 0, hi = np - 1;  // the part holding tree position j
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cuts[mid] <= j)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    u = rows + 3 * (lo * W + (j - cuts[lo]));
+  }
+  const double u0 = u[0], u1 = u[1], u2 = u[2];
+  const double w = (stage == 1 || stage == 2) ? 2.0 : 1.0;
+  const double kzv = mul_rn(mul_rn(-2.0, omega), u2);
+  if (stage == 0) {
+    acc[3 * i] = u0;
+    acc[3 * i + 1] = u1;
+    acc[3 * i + 2] = u2;
+    accz[i] = kzv;
+  } else {
+    acc[3 * i] = add_rn(acc[3 * i], mul_rn(w, u0));
+    acc[3 * i + 1] = add_rn(acc[3 * i + 1], mul_rn(w, u1));
+    acc[3 * i + 2] = add_rn(acc[3 * i + 2], mul_rn(w, u2));
+    accz[i] = add_rn(accz[i], mul_rn(w, kzv));
+  }
+  if (k) {
+    k[3 * i] = u0;
+    k[3 * i + 1] = u1;
+    k[3 * i + 2] = u2;
+    kz[i] = kzv;
+  }
+  if (cs >= 0.0) {  // k_rk4_stage of the next stage (stage + 1 >= 1)
+    int bad = 0;
+    const d3 v{add_rn(x0[3 * i], mul_rn(cs, u0)), add_rn(x0[3 * i + 1], mul_rn(cs, u1)),
+               add_rn(x0[3 * i + 2], mul_rn(cs, u2))};
+    const d3 un = unit_rn(v, &bad);
+    if (bad) atomicOr(flags, kFlagGeometry);
+    xs[3 * i] = un.x;
+    xs[3 * i + 1] = un.y;
+    xs[3 * i + 2] = un.z;
+    q[i] = mul_rn(add_rn(z0[i], mul_rn(cs, kzv)), area[i]);
+  }
+}
+
+__global__ void k_inv_of(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) inv[perm[j]] = static_cast<int>(j);
+}
+
 // particles [i0, i1)
 __global__ void k_rk4_final(int64_t i0, int64_t i1, double h6, double* __restrict__ x0, double* __restrict__ z0,
                             const double* __restrict__ acc, const double* __restrict__ accz, int* flags) {
@@ -783,22 +847,30 @@ int ssum_rk4(ssum_ctx* h, const ssum_config* cfg, double* xyz, double* zeta, con
       io.dim = 3;
     }
     for (int step = 0; step < steps; ++step) {
+      // Each stage's accumulation is fused with the next stage's positions
+      // and strengths (k_rk4_advance_rows on the caller-order velocities,
+      // bitwise k_rk4_accum + k_rk4_stage); a geometry error it flags is
+      // raised by the next evaluation's check (or the step's).
       for (int s = 0; s < 4; ++s) {
-        SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
+        if (s == 0) SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, 4, c.stream));
         if (io.active) {  // first stage of the call: x0 and q as they land
           treecode_device(c, SSUM_BIOT_SAVART, *cfg, x0, q, n, u, st);
           SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, io.q, 0));  // zeta and A for the next stages
           io.active = false;
         } else {
-          k_rk4_stage<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, cs[s], x0, z0, ar, k, kz, xs, q, c.d_flags.p);
-          SSUM_LAUNCH_CHECK();
-          c.launches++;
+          if (s == 0) {  // stage 0 of a step: xs = x0, q = zeta A
+            k_rk4_stage<<<grid_for(n, bs), bs, 0, c.stream>>>(n, 0, 0.0, x0, z0, ar, k, kz, xs, q, c.d_flags.p);
+            SSUM_LAUNCH_CHECK();
+            c.launches++;
+          }
           if (direct)
             direct_sum_device(c, SSUM_BIOT_SAVART, xs, q, n, u);
           else
             treecode_device(c, SSUM_BIOT_SAVART, *cfg, xs, q, n, u, st);
         }
-        k_rk4_accum<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, omega, u, k, kz, acc, accz);
+        k_rk4_advance_rows<<<grid_for(n, bs), bs, 0, c.stream>>>(n, s, omega, s < 3 ? cs[s + 1] : -1.0, u, 0,
+                                                                 nullptr, 1, nullptr, x0, z0, ar, acc, accz,
+                                                                 nullptr, nullptr, xs, q, c.d_flags.p);
         SSUM_LAUNCH_CHECK();
         c.launches++;
       }
@@ -913,6 +985,37 @@ int ssum_rk4_stage_end_rows(ssum_ctx* h, int stage, double omega, int64_t n, con
                                                              c.bins.perm.p, d_k, d_kz, d_acc, d_accz);
     SSUM_LAUNCH_CHECK();
     c.launches++;
+  });
+}
+
+int ssum_rk4_stage_advance_rows(ssum_ctx* h, int stage, double dt, double omega, int64_t n, const double* d_rows,
+                                int64_t width, const double* d_x0, const double* d_z0, const double* d_area,
+                                double* d_k, double* d_kz, double* d_acc, double* d_accz, double* d_xs, double* d_q) {
+  return guarded(h, [&](Ctx& c) {
+    check_n(n);
+    if (stage < 0 || stage > 3) throw Error(SSUM_INVALID, "RK4 stage must be 0..3");
+    if ((d_k == nullptr) != (d_kz == nullptr)) throw Error(SSUM_INVALID, "rk4_stage_advance_rows: k and kz together");
+    if (stage < 3 && (!d_x0 || !d_z0 || !d_area || !d_xs || !d_q))
+      throw Error(SSUM_INVALID, "rk4_stage_advance_rows: the next stage needs x0, z0, area, xs, q");
+    if (n == 0) return;
+    if (n != c.bins.n || c.bins.perm_n != n || int64_t(c.part_pos.size()) != c.nparts + 1 || c.part_pos.back() != n)
+      throw Error(SSUM_INVALID, "rk4_stage_advance_rows: no partitioned evaluation of these particles");
+    const int np = c.nparts;
+    for (int r = 0; r < np; ++r)
+      if (c.part_pos[size_t(r) + 1] - c.part_pos[size_t(r)] > width)
+        throw Error(SSUM_INVALID, "rk4_stage_advance_rows: a part has more rows than the slot width");
+    c.cut_dev.ensure(size_t(np) + 1);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(c.cut_dev.p, c.part_pos.data(), (size_t(np) + 1) * 8, cudaMemcpyHostToDevice,
+                                    c.stream));
+    c.inv_perm.ensure(size_t(n));
+    k_inv_of<<<grid_for(n, 256), 256, 0, c.stream>>>(c.bins.perm.p, n, c.inv_perm.p);
+    SSUM_LAUNCH_CHECK();
+    const double cs_next[4] = {0.5 * dt, 0.5 * dt, dt, -1.0};  // stage + 1's offset (none after stage 3)
+    k_rk4_advance_rows<<<grid_for(n, 256), 256, 0, c.stream>>>(
+        n, stage, omega, cs_next[stage], d_rows, width, c.cut_dev.p, np, c.inv_perm.p, d_x0, d_z0, d_area, d_acc,
+        d_accz, d_k, d_kz, d_xs, d_q, c.d_flags.p);
+    SSUM_LAUNCH_CHECK();
+    c.launches += 2;
   });
 }
 

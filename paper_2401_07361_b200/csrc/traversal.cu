@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(32 * kFillWarps)
                 const double* __restrict__ center, const double* __restrict__ radius,
                 const int* __restrict__ range_off, const int* __restrict__ tile_off, int64_t N, int P,
                 SrcRange* __restrict__ ranges, Tile* __restrict__ tiles, ulonglong2* __restrict__ tile_cost,
-                unsigned long long* __restrict__ evals) {
-  __shared__ int spath[kFillWarps][48];
+                unsigned long long* __restrict__ evals, const NodeRec* __restrict__ rec) {
+  __shared__ int sseg[kFillWarps][48];  // first sorted entry of each path node's segment (root first)
   __shared__ int sbeg[kFillWarps][49];  // first flattened entry of each path node (root first)
   __shared__ int spl[kFillWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       for (int q = 0; q < pl; ++q) {
         const int node = tmp[pl - 1 - q];
         const int2 sg = seg[2 * node];
-        spath[wid][q] = node;
+        sseg[wid][q] = sg.x;
         sbeg[wid][q] = run;
         run += sg.y - sg.x;
       }
@@ -348,7 +348,8 @@ __global__ void __launch_bounds__(32 * kFillWarps)
     __syncwarp();
     const int pl = spl[wid];
     const int T = sbeg[wid][pl];
-    const int offl = off[leaf];
+    const NodeRec Lr = rec[leaf];
+    const int offl = Lr.off;
     const int w0 = range_off[k];
     ListCursor cur;
     int src_pp = 0, src_pc = 0, near_total = 0, self_shift = 0, has_self = 0;
@@ -361,14 +362,14 @@ __global__ void __launch_bounds__(32 * kFillWarps)
         if (idx < T) {
           int q = 0;
           while (sbeg[wid][q + 1] <= idx) ++q;
-          const int node = spath[wid][q];
-          const int4 it = E[sorted_e[seg[2 * node].x + (idx - sbeg[wid][q])]];
-          const bool nr = it.z == 0 && near_possible(leaf, it.y, center, radius);
+          const int4 it = E[sorted_e[sseg[wid][q] + (idx - sbeg[wid][q])]];
+          const NodeRec Sr = rec[it.y];
+          const bool nr = it.z == 0 && near_possible_rec(it.y == leaf, Lr, Sr);
           sel = nr == (pass == 0);
           if (sel) {
             if (it.z == 0) {
-              r.begin = off[it.y];
-              r.count = cnt[it.y];
+              r.begin = Sr.off;
+              r.count = Sr.cnt;
               r.near = nr ? 1 : 0;
               self = r.begin <= offl && offl < r.begin + r.count;  // holds the leaf's own particles
               cpp = r.count;
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(32 * kFillWarps)
       t.self_shift = self_shift;
       // dense leaf: estimated point spacing sqrt(area / count), area ~ 1.3 r^2
       // of the leaf triangle in its circumcircle of angular radius r
-      const double rl = radius[leaf];
+      const double rl = Lr.r;
       const bool dense = near_total > 0 && 1.3 * rl * rl < kDenseSpacing * kDenseSpacing * double(c);
       t.has_self = has_self | (dense ? kTileDense : 0);
       t.total = cur.src;
@@ -966,7 +967,7 @@ void build_lists(Ctx& c, const ssum_config& cfg) {
                                                         L.inter.p, B.cnt.p, B.off.p, L.pslot.p, c.nodes.center.p,
                                                         c.nodes.radius.p, S.nr_off.p, S.nt_off.p, N, P,
                                                         L.leaf_ranges.p, L.leaf_tiles.p, L.leaf_cost.p,
-                                                        S.counters.p + 4);
+                                                        S.counters.p + 4, S.rec.p);
   SSUM_LAUNCH_CHECK();
   c.launches++;
 

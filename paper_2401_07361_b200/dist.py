@@ -212,11 +212,11 @@ class TreecodeRK4Ops:
         st["rows"] = torch.zeros((self.ws * n, 3), dtype=x.dtype, device=x.device) if self.ws > 1 else st["slot"]
         return st
 
-    def stage(self, s: int, dt: float, omega: float, st: dict) -> int:
+    def _evaluate(self, st: dict):
+        """This rank's partitioned evaluation at st["xs"], st["q"] and the one
+        all-gather of the slots: (rows, width, our kernel launches)."""
         n = st["n"]
         t = self.tree
-        t.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
-                          st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
         stats = self._stats()
         if self.shard_binning:  # each rank walks 1/ws of the particles, one all-gather of the keys
             sharded_walk(t, st["xs"].data_ptr(), n, self.group, st["xs"].device)
@@ -227,17 +227,35 @@ class TreecodeRK4Ops:
         cuts = t.partition_cuts()
         width = slot_width(cuts) if self.ws > 1 else n
         rows = exchange_rows(st["slot"], st["rows"], width, self.group)
+        return rows, width, stats.gpu_launches
+
+    def stage(self, s: int, dt: float, omega: float, st: dict) -> int:
+        """One stage with the separate begin / end kernels (k, kz kept)."""
+        n = st["n"]
+        t = self.tree
+        t.rk4_stage_begin(s, dt, n, st["x0"].data_ptr(), st["z0"].data_ptr(), st["area"].data_ptr(),
+                          st["k"].data_ptr(), st["kz"].data_ptr(), st["xs"].data_ptr(), st["q"].data_ptr())
+        rows, width, launches = self._evaluate(st)
         t.rk4_stage_end_rows(s, omega, n, rows.data_ptr(), width, st["k"].data_ptr(), st["kz"].data_ptr(),
                              st["acc"].data_ptr(), st["accz"].data_ptr())
-        return stats.gpu_launches + 2
+        return launches + 2
 
     def step(self, dt: float, st: dict, omega: float = 2.0 * 3.141592653589793) -> int:
-        """One RK4 step in place on st["x0"], st["z0"]; returns our kernel launches."""
-        launches = 0
+        """One RK4 step in place on st["x0"], st["z0"]; returns our kernel
+        launches. Between two evaluations one fused kernel pair
+        (ssum_rk4_stage_advance_rows) ends a stage and begins the next —
+        bitwise the separate stage() kernels."""
+        n = st["n"]
+        t = self.tree
+        p = {k: st[k].data_ptr() for k in ("x0", "z0", "area", "acc", "accz", "xs", "q", "k", "kz")}
+        t.rk4_stage_begin(0, dt, n, p["x0"], p["z0"], p["area"], p["k"], p["kz"], p["xs"], p["q"])
+        launches = 1
         for s in range(4):
-            launches += self.stage(s, dt, omega, st)
-        self.tree.rk4_step_end(dt, st["n"], st["x0"].data_ptr(), st["z0"].data_ptr(), st["acc"].data_ptr(),
-                               st["accz"].data_ptr())
+            rows, width, nl = self._evaluate(st)
+            t.rk4_stage_advance_rows(s, dt, omega, n, rows.data_ptr(), width, p["x0"], p["z0"], p["area"],
+                                     p["acc"], p["accz"], p["xs"], p["q"])
+            launches += nl + 2
+        t.rk4_step_end(dt, n, p["x0"], p["z0"], p["acc"], p["accz"])
         return launches + 1
 
 
