@@ -165,18 +165,21 @@ __global__ void __launch_bounds__(32 * kUpWarps, SSUM_UP_MINB) k_up_partial(cons
 #endif
 constexpr int kUpChunk = SSUM_UP_CHUNK;  // particles per upward chunk (one warp each)
 
+// d_nw (optional): the device-side weight-node count (<= the host bound nw,
+// which sizes the grids); entries past it contribute nothing.
 __global__ void k_up_nchunks(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ cnt,
-                             int* __restrict__ nch) {
+                             int* __restrict__ nch, const int* __restrict__ d_nw) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w < nw) nch[w] = (cnt[weight_nodes[w]] + kUpChunk - 1) / kUpChunk;
-  if (w == nw) nch[w] = 0;
+  const int nwe = d_nw ? min(*d_nw, nw) : nw;
+  if (w < nwe) nch[w] = (cnt[weight_nodes[w]] + kUpChunk - 1) / kUpChunk;
+  else if (w <= nw) nch[w] = 0;
 }
 
 __global__ void k_up_fill(const int* __restrict__ weight_nodes, int nw, const int* __restrict__ off,
                           const int* __restrict__ cnt, const int* __restrict__ chunk_off, int4* __restrict__ chunks,
-                          int2* __restrict__ crange) {
+                          int2* __restrict__ crange, const int* __restrict__ d_nw) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= nw) return;
+  if (w >= (d_nw ? min(*d_nw, nw) : nw)) return;
   const int id = weight_nodes[w], o = off[id], cn = cnt[id];
   int k = chunk_off[w];
   crange[w] = make_int2(k, chunk_off[w + 1]);
@@ -188,10 +191,10 @@ __global__ void k_up_fill(const int* __restrict__ weight_nodes, int nw, const in
 __global__ void k_up_final(const int* __restrict__ weight_nodes, int nw, const int2* __restrict__ chunk_range,
                            const double* __restrict__ wpart, const double* __restrict__ vinv, int P,
                            const int* __restrict__ pslot, int64_t N, double4* __restrict__ pts,
-                           double* __restrict__ raw = nullptr) {
+                           double* __restrict__ raw = nullptr, const int* __restrict__ d_nw = nullptr) {
   extern __shared__ double ws[];
   const int w = blockIdx.x;
-  if (w >= nw) return;
+  if (w >= (d_nw ? min(*d_nw, nw) : nw)) return;
   const int2 cr = chunk_range[w];
   for (int m = threadIdx.x; m < P; m += blockDim.x) {
     double s = 0.0;
@@ -584,11 +587,15 @@ void launch_prep(Ctx& c, cudaStream_t s, DBuf<unsigned char>& tmp, int degree, c
 
   // ---- upward pass: chunk table (weight node bins cut into <= 1024-particle
   // chunks) built on the device
+  // weight nodes: L.weight_nodes (host count), or the subtree builder's
+  // marked subset (c.up_list with its device count c.up_count, <= n_weight)
+  const int* wl = c.up_list ? c.up_list : L.weight_nodes.p;
+  const int* d_nw = c.up_list ? c.up_count : nullptr;
   if (L.n_weight > 0) {
     const int nw = L.n_weight;
     c.wcount.ensure(size_t(nw) + 1, false, s);
     c.wcount_off.ensure(size_t(nw) + 1, false, s);
-    k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.cnt.p, c.wcount.p);
+    k_up_nchunks<<<grid_for(nw + 1, 256), 256, 0, s>>>(wl, nw, B.cnt.p, c.wcount.p, d_nw);
     SSUM_LAUNCH_CHECK();
     size_t tb = 0;
     SSUM_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, c.wcount.p, c.wcount_off.p, nw + 1, s));
@@ -602,14 +609,14 @@ void launch_prep(Ctx& c, cudaStream_t s, DBuf<unsigned char>& tmp, int degree, c
     c.wchunks.ensure(size_t(nch) + size_t(nw), false, s);
     c.wpart.ensure(size_t(nch) * P, false, s);
     int2* d_crange = reinterpret_cast<int2*>(c.wchunks.p + nch);
-    k_up_fill<<<grid_for(nw, 256), 256, 0, s>>>(L.weight_nodes.p, nw, B.off.p, B.cnt.p, c.wcount_off.p,
-                                                 c.wchunks.p, d_crange);
+    k_up_fill<<<grid_for(nw, 256), 256, 0, s>>>(wl, nw, B.off.p, B.cnt.p, c.wcount_off.p, c.wchunks.p, d_crange,
+                                                 d_nw);
     SSUM_LAUNCH_CHECK();
     c.launches += 4;
     if (nch > 0) launch_up_partial(c, s, degree, nch, c.wcount_off.p + nw);
     const int bt = ((P + 31) / 32) * 32;
-    k_up_final<<<L.n_weight, bt, size_t(P) * 8, s>>>(L.weight_nodes.p, L.n_weight, d_crange, c.wpart.p, c.vinv.p,
-                                                      P, L.pslot.p, n, c.pts.p);
+    k_up_final<<<L.n_weight, bt, size_t(P) * 8, s>>>(wl, L.n_weight, d_crange, c.wpart.p, c.vinv.p, P, L.pslot.p, n,
+                                                      c.pts.p, nullptr, d_nw);
     SSUM_LAUNCH_CHECK();
     c.launches++;
   }

@@ -300,6 +300,7 @@ struct SubPlan {
   int smem = 0;
   DBuf<unsigned char> big_flag, cut_flag;
   DBuf<int> cut, tpl, tile_off;
+  DBuf<int> wsel;  // [0] count, [1..] marked weight nodes (restricted calls)
   DBuf<unsigned long long> up_visits, cursor;
   int64_t leaf_cap = 0, fit_cap = 0;  // range buffer sizes
   int64_t max_emit = 0, max_front = 0;  // last call's largest block emission count / frontier
@@ -388,6 +389,10 @@ struct Ctx {
   // global-path lists on the binning's plan (traversal.cu): proxy slots for
   // every big node, upward pass started before the traversal
   bool plan_lists = false;
+  // upward pass on a subset of the weight nodes (subtree builder, restricted
+  // call: only the sources this part's lists use): list + device count
+  const int* up_list = nullptr;
+  const int* up_count = nullptr;
   bool plan_lists_ok = true;  // SSUM_PLAN_LISTS=0: slots from the traversal's marks
   bool early_prep = true;
   cudaEvent_t prep_ev = nullptr;

@@ -112,6 +112,7 @@ struct SubArgs {
   Tile* fit_tiles;
   ulonglong2* fit_cost;
   unsigned char* is_fit;
+  unsigned char* is_weight;  // optional: marks the PC / CC sources of the lists built
   unsigned long long* counters;  // traversal.cu layout + [8] fit nodes, [12] max emissions, [13] max frontier
   int* flags;
 };
@@ -409,6 +410,7 @@ __global__ void __launch_bounds__(kSubThreads, SSUM_SUB_MINB) k_sub_lists(SubArg
               r.begin = static_cast<int>(a.N + static_cast<int64_t>(a.pslot[s]) * a.P);
               r.count = a.P;
               cpc = a.P;
+              if (a.is_weight && pass == 1) a.is_weight[s] = 1;
             }
           }
         }
@@ -496,6 +498,7 @@ __global__ void __launch_bounds__(kSubThreads, SSUM_SUB_MINB) k_sub_lists(SubArg
           r.begin = static_cast<int>(a.N + static_cast<int64_t>(a.pslot[s]) * a.P);
           r.count = a.P;
           is_cc = 1;
+          if (a.is_weight) a.is_weight[s] = 1;
         }
       }
       append_ranges(i < e_end, r, out, lc, lane);
@@ -676,6 +679,16 @@ void build_lists_subtree(Ctx& c, const ssum_config& cfg) {
   L.n_fit_tiles = S.n_big;
   L.n_leaf_tiles = S.n_leaf_tiles;
   S.used = true;
+  // restricted (multi-part) call: the upward pass only for the sources this
+  // part's lists use, marked by the builder (it then follows the builder);
+  // otherwise every big node's, beside the builder
+  const bool lean_up = c.restrict_on;
+  c.up_list = nullptr;
+  c.up_count = nullptr;
+  if (lean_up) {
+    L.is_weight.ensure(size_t(nn));
+    SSUM_CUDA_CHECK(cudaMemsetAsync(L.is_weight.p, 0, size_t(nn), c.stream));
+  }
 
   const MacCtl* mac = reinterpret_cast<const MacCtl*>(mac_ctl_device(c));
   build_node_records(c, cfg.theta);
@@ -745,17 +758,32 @@ void build_lists_subtree(Ctx& c, const ssum_config& cfg) {
   a.fit_tiles = L.fit_tiles.p;
   a.fit_cost = L.fit_cost.p;
   a.is_fit = L.is_fit.p;
+  a.is_weight = lean_up ? L.is_weight.p : nullptr;
   a.counters = TS.counters.p;
   a.flags = c.d_flags.p;
   // the prep stream forks here (its inputs exist; buffers sized before), so
   // the proxy points + upward pass of every big node (low-priority stream)
   // run beside the list builder's latency-bound blocks
   if (c.early.xyz) size_eval_buffers(c, c.early.degree, c.early.dim, N);
-  SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+  if (!lean_up) SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
   k_sub_lists<<<S.n_cut, kSubThreads, S.smem, c.stream>>>(a);
   SSUM_LAUNCH_CHECK();
   c.launches++;
-  start_prep(c, true);
+  if (lean_up) {
+    // the marked sources, in node-id order, with their device count
+    S.wsel.ensure(size_t(nn) + 1);
+    cub::CountingInputIterator<int> ids(0);
+    size_t tb = 0;
+    SSUM_CUDA_CHECK(
+        cub::DeviceSelect::Flagged(nullptr, tb, ids, L.is_weight.p, S.wsel.p + 1, S.wsel.p, nn, c.stream));
+    c.cub_tmp.ensure(tb);
+    SSUM_CUDA_CHECK(
+        cub::DeviceSelect::Flagged(c.cub_tmp.p, tb, ids, L.is_weight.p, S.wsel.p + 1, S.wsel.p, nn, c.stream));
+    c.launches += 2;
+    c.up_list = S.wsel.p + 1;
+    c.up_count = S.wsel.p;
+  }
+  start_prep(c, !lean_up);
   // counts, evaluations, visits and the range use: read back with the
   // evaluation's final sync (finalize_counts / sub_lists_check)
   SSUM_CUDA_CHECK(cudaMemcpyAsync(TS.h_small + 8, TS.counters.p, 21 * sizeof(unsigned long long),

@@ -791,6 +791,8 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
     g.theta = cfg.theta;
   }
   build_node_records(c, cfg.theta);
+  c.up_list = nullptr;  // the upward pass covers every weight node
+  c.up_count = nullptr;
   // planned lists (the binning's subtree plan gave every big node a proxy
   // slot): the upward pass needs nothing from the traversal, so it starts
   // now and runs beside it; fit tiles are indexed by slot
