@@ -82,6 +82,9 @@ constexpr int kFastUnroll = SSUM_FAST_UNROLL, kNearUnroll = SSUM_NEAR_UNROLL;
 #ifndef SSUM_TPT
 #define SSUM_TPT 2
 #endif
+#ifndef SSUM_NEAR_HIT
+#define SSUM_NEAR_HIT 0  // 1: record which near steps met a masked pair (repair only those)
+#endif
 #ifndef SSUM_RANGE_CAP
 #define SSUM_RANGE_CAP 128
 #endif
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(NTH, MINB)
     }
 #else
     if (it < near_steps) {
+#if SSUM_NEAR_HIT
       // bit `it` of hit: step `it` met a masked pair (self or near); steps
       // past 64 are all re-walked when a repair is needed
       int ncnt = 0;
@@ -325,6 +329,29 @@ __global__ void __launch_bounds__(NTH, MINB)
         far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, B + it * kStep, G, a, &ncnt, ltab);
         hit |= static_cast<unsigned long long>(ncnt != before) << (it & 63);
       }
+#else
+      // masked pairs counted, recorded per PAIR of steps in 32 bits (fewer
+      // live registers and instructions than a per-step 64-bit record); a
+      // repair re-walks only the flagged step pairs (beyond 64 steps: all)
+      int ncnt = 0;
+      unsigned hit2 = 0;
+      const double4* Bn = B + it * kStep;
+      for (; it + 1 < near_steps; it += 2, Bn += 2 * kStep) {
+        const int before = ncnt;
+        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, Bn, G, a, &ncnt, ltab);
+        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, Bn + kStep, G, a, &ncnt, ltab);
+        hit2 |= static_cast<unsigned>(ncnt != before) << ((it >> 1) & 31);
+      }
+      if (it < near_steps) {
+        const int before = ncnt;
+        far_block<KER, kTpt, kNs, true, MODE == kDirectMode>(x, Bn, G, a, &ncnt, ltab);
+        hit2 |= static_cast<unsigned>(ncnt != before) << ((it >> 1) & 31);
+        ++it;
+      }
+      unsigned long long hit = 0;  // per step, for the repair below
+      for (unsigned m2 = hit2; m2; m2 &= m2 - 1) hit |= 3ull << (2 * (__ffs(static_cast<int>(m2)) - 1));
+      if (near_steps < 64) hit &= (1ull << near_steps) - 1ull;
+#endif
       // self pairs this lane walked in this chunk's near steps: the self
       // source of target ti sits at flattened position ti + T.self_shift
       const int o_end = min(n, near_steps * kStep);

@@ -1,7 +1,7 @@
 """One warm-up + `reps` config-4 treecode evaluations on device-resident
 inputs — the command profiled by ncu (profiles/README.md). No output checks.
 
-    python tools/profile_step.py [reps] [level] [degree]
+    python tools/profile_step.py [reps] [level] [degree] [theta]
 """
 import sys
 
@@ -13,6 +13,7 @@ import paper_2401_07361_b200 as ss  # noqa: E402
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 9
 degree = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+theta = float(sys.argv[4]) if len(sys.argv) > 4 else 0.7
 xyz, area = ss.make_icosa_mesh(level)
 q = ss.rh4_vorticity(xyz) * area
 dev = torch.device("cuda", 0)
@@ -21,7 +22,7 @@ d_q = torch.from_numpy(q).to(dev)
 d_out = torch.zeros((xyz.shape[0], 3), dtype=torch.float64, device=dev)
 tree = ss.FaceTree(0)
 tree.set_stream(torch.cuda.current_stream().cuda_stream)
-cfg = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=degree, max_depth=10)
+cfg = ss.TraversalConfig(theta=theta, n_threshold=64, degree=degree, max_depth=10)
 for _ in range(1 + reps):
     st = ss.TreecodeStats()
     ss.treecode_sum_device(tree, ss.BiotSavartKernel, cfg, d_xyz.data_ptr(), d_q.data_ptr(), xyz.shape[0],

@@ -19,8 +19,8 @@ CASES = {
     "l7": dict(mesh=7, degree=8, theta=0.7),
     "c2": dict(mesh=8, degree=8, theta=0.7),
     "c4": dict(mesh=9, degree=8, theta=0.7),
-    "c3s": dict(cap=1 << 20, degree=8, theta=0.7),
-    "c5": dict(mesh=10, degree=8, theta=0.8),
+    "c3s": dict(cap=1 << 20, degree=8, theta=0.7, step=1e-8),
+    "c5": dict(mesh=10, degree=8, theta=0.8, step=2e-5),
 }
 
 
@@ -49,7 +49,7 @@ def run(case, xyz0, q, calls, sub):
     x = xyz0.copy()
     for k in range(calls):
         if k >= 2:  # moving particles: a small random step, renormalised
-            x = x + 2e-4 * rng.standard_normal(x.shape)
+            x = x + case.get("step", 2e-4) * rng.standard_normal(x.shape)
             x /= np.linalg.norm(x, axis=1, keepdims=True)
         d_x = torch.from_numpy(x).to(dev)
         d_out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
