@@ -116,7 +116,9 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
   // Lists per target subtree (sublists.cu) when the binning made a plan;
   // if they came out incomplete (a buffer outgrew, undecided MAC pairs) the
   // evaluation is redone on the global traversal path (traversal.cu).
-  const bool sub = sub_lists_usable(c, cfg);
+  const int choice = sub_lists_choice(c, cfg);
+  const bool sub = (choice & 1) != 0, trial = choice >= 2;
+  if (trial) SSUM_CUDA_CHECK(cudaEventRecord(c.ev[6], c.stream));
   auto t2 = clk::now();
   for (int attempt = 0;; ++attempt) {
     c.early = Ctx::Early{d_xyz, d_q, cfg.degree, kernel == SSUM_BIOT_SAVART ? 3 : 1};
@@ -130,6 +132,13 @@ void treecode_device(Ctx& c, int kernel, const ssum_config& cfg, const double* d
     evaluate(c, kernel, cfg, d_xyz, d_q, n, d_out, st);
     if (!sub_lists_redo(c, c.last_flags)) break;
     SSUM_CUDA_CHECK(cudaMemsetAsync(c.d_flags.p, 0, sizeof(int), c.stream));
+  }
+  if (trial) {  // the stream has drained (the evaluation's final check)
+    SSUM_CUDA_CHECK(cudaEventRecord(c.ev[7], c.stream));
+    SSUM_CUDA_CHECK(cudaEventSynchronize(c.ev[7]));
+    float ms = 0.f;
+    SSUM_CUDA_CHECK(cudaEventElapsedTime(&ms, c.ev[6], c.ev[7]));
+    sub_lists_timed(c, sub ? 1 : 0, ms);
   }
   finalize_counts(c);
   tr.mark("eval.done");

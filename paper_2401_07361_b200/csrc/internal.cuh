@@ -313,6 +313,13 @@ struct SubPlan {
   int64_t leaf_cap = 0, fit_cap = 0;  // range buffer sizes
   int64_t max_emit = 0, max_front = 0;  // last call's largest block emission count / frontier
   int64_t redos = 0;
+  // measured choice between the two list builders (sub_lists_choice)
+  int64_t bad_n = -1;  // particle count whose subtree blocks overflowed
+  int64_t trial_n = -1;
+  double trial_theta = -1.0;
+  int trial_calls = 0;
+  int trial_cnt[2] = {0, 0};      // [0] global, [1] subtree
+  double trial_ms[2] = {0.0, 0.0};
 };
 
 struct Ctx {
@@ -452,7 +459,8 @@ void finalize_counts(Ctx& c);
 // subtree list builder (sublists.cu)
 void plan_subtrees(Ctx& c, int thr, const int* d_nl, int* d_out);
 void plan_subtrees_done(Ctx& c, const int* h);
-bool sub_lists_usable(const Ctx& c, const ssum_config& cfg);
+int sub_lists_choice(Ctx& c, const ssum_config& cfg);  // 0 global, 1 subtree; +2: timed trial
+void sub_lists_timed(Ctx& c, int used_sub, double ms);
 void build_lists_subtree(Ctx& c, const ssum_config& cfg);
 bool sub_lists_redo(Ctx& c, int flags);
 // MAC guard band (traversal.cu): the device control block for a traversal

@@ -76,10 +76,7 @@ typedef cub::BlockScan<int, kSubThreads> SubScan;
 #define SSUM_SUB_PER 2
 #endif
 constexpr int kPer = SSUM_SUB_PER;  // frontier entries per thread per round
-#ifndef SSUM_SUB_AUTO_N
-#define SSUM_SUB_AUTO_N 1500000
-#endif
-constexpr int64_t kSubAutoN = SSUM_SUB_AUTO_N;
+constexpr int kSubRetrial = 512;  // calls before the builders are timed again
 
 // the four ints of a node record (cnt, off, level, child_base): one 16-byte load
 __device__ __forceinline__ int4 rec_ints(const NodeRec* __restrict__ rec, int t) {
@@ -655,11 +652,51 @@ void plan_subtrees_done(Ctx& c, const int* h) {
   S.valid = true;
 }
 
-bool sub_lists_usable(const Ctx& c, const ssum_config& cfg) {
-  const SubPlan& S = c.sub;
-  const bool wanted = S.forced || c.restrict_on || c.bins.n <= kSubAutoN;
-  return wanted && S.valid && !S.disabled && S.thr == cfg.n_threshold && c.bins.n > 0 && c.bins.n_leaves > 0 &&
-         S.n_cut > 0 && c.nodes.max_level < kMaxChain - 1 && c.nodes.count < (1 << 30);
+// Which list builder this call uses: 0 the global path, 1 the subtree
+// builder; +2: a timed trial (sub_lists_timed reports its device time).
+// Restricted (multi-part) calls always take the subtree builder (it
+// traverses only the part's subtrees). Otherwise the choice is measured:
+// which builder is faster depends on the tree's shape (the subtree
+// builder's blocks replay their ancestor paths; the global traversal pays
+// grid-wide steps and read-backs) — on the BASELINE meshes it wins up to
+// C2's size and loses at C4's, on the random cap it loses at 2^20 — so the
+// first evaluations of a particle count alternate the two, timing each
+// twice, and the faster one serves the next kSubRetrial calls.
+int sub_lists_choice(Ctx& c, const ssum_config& cfg) {
+  SubPlan& S = c.sub;
+  const bool usable = S.valid && !S.disabled && S.thr == cfg.n_threshold && c.bins.n > 0 && c.bins.n_leaves > 0 &&
+                      S.n_cut > 0 && c.nodes.max_level < kMaxChain - 1 && c.nodes.count < (1 << 30);
+  if (!usable) return 0;
+  if (S.forced) return 1;
+  // a block outgrew its shared memory for this particle count (deep or
+  // dense trees: long replayed paths): the global path from now on
+  if (S.bad_n == c.bins.n) return 0;
+  if (c.restrict_on) return 1;
+  if (S.trial_n != c.bins.n || S.trial_calls >= kSubRetrial || S.trial_theta != cfg.theta) {
+    S.trial_n = c.bins.n;
+    S.trial_theta = cfg.theta;
+    S.trial_calls = 0;
+    S.trial_cnt[0] = S.trial_cnt[1] = 0;
+    S.trial_ms[0] = S.trial_ms[1] = 0.0;
+  }
+  ++S.trial_calls;
+  // one sample each decides when they differ by more than 25%; otherwise a
+  // second (warm) sample each is compared
+  const bool clear = S.trial_cnt[0] >= 1 && S.trial_cnt[1] >= 1 &&
+                     (S.trial_ms[0] > 1.25 * S.trial_ms[1] || S.trial_ms[1] > 1.25 * S.trial_ms[0]);
+  if (!clear && (S.trial_cnt[0] < 2 || S.trial_cnt[1] < 2)) return 2 + (S.trial_cnt[1] <= S.trial_cnt[0] ? 1 : 0);
+  return S.trial_ms[1] <= S.trial_ms[0] ? 1 : 0;
+}
+
+// A trial's device time (lists + evaluation); the second sample of each
+// builder is the one compared (the first may include buffer growth).
+void sub_lists_timed(Ctx& c, int used_sub, double ms) {
+  SubPlan& S = c.sub;
+  S.trial_ms[used_sub] = ms;
+  S.trial_cnt[used_sub]++;
+  if (trace().on)
+    std::fprintf(stderr, "[ssum sub] trial %s %.3f ms (global %.3f x%d, subtree %.3f x%d)\n",
+                 used_sub ? "subtree" : "global", ms, S.trial_ms[0], S.trial_cnt[0], S.trial_ms[1], S.trial_cnt[1]);
 }
 
 // The lists of this call from the plan (see the file comment); no host
@@ -825,7 +862,10 @@ bool sub_lists_redo(Ctx& c, int flags) {
   if (fu + fu / 4 > S.fit_cap) S.fit_cap = fu + fu / 2 + 65536, grown = true;
   bool redo = (flags & kFlagListsRedo) != 0;
   // a block outgrew its shared memory: smaller subtrees next time
-  if (redo && !ranges_out) S.cmax = std::max(16, S.cmax / 2);
+  if (redo && !ranges_out) {
+    S.bad_n = c.bins.n;  // auto mode: the global path for this particle count
+    if (S.forced) S.cmax = std::max(16, S.cmax / 2);  // forced: retry with smaller cuts
+  }
   const int amb = *reinterpret_cast<const int*>(h + 31);  // undecided MAC pairs met
   if (amb > 0 && resolve_mac_host(c)) redo = true;
   if (trace().on)

@@ -16,7 +16,10 @@ def _run(ss, xyz0, q, cfg, calls, mode, cmax=None, kernel=None, seed=7, step=3e-
     the list builder selected by SSUM_SUB_LISTS (read when the tree makes its
     first plan)."""
     old = {k: os.environ.get(k) for k in ("SSUM_SUB_LISTS", "SSUM_SUB_CMAX")}
-    os.environ["SSUM_SUB_LISTS"] = mode
+    if mode == "auto":  # measured choice between the builders
+        os.environ.pop("SSUM_SUB_LISTS", None)
+    else:
+        os.environ["SSUM_SUB_LISTS"] = mode
     if cmax is not None:
         os.environ["SSUM_SUB_CMAX"] = str(cmax)
     try:
@@ -85,3 +88,18 @@ def test_subtree_lists_guard_band(ss, mesh_fixture, monkeypatch):
     xyz, q, _ = mesh_fixture(6)
     c = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=4, max_depth=10)
     assert _same(_run(ss, xyz, q, c, 3, "1"), _run(ss, xyz, q, c, 3, "0"))
+
+
+@pytest.mark.parametrize("which", ["mesh", "cap"])
+def test_subtree_lists_auto_choice(ss, mesh_fixture, which):
+    """Default mode: the first evaluations time both builders (on the cap the
+    subtree blocks overflow and the call is redone on the global path) and
+    keep the faster; every call's result is bitwise the global path's."""
+    if which == "mesh":
+        xyz, q, _ = mesh_fixture(7)
+    else:
+        xyz, zeta, area = ss.make_random_cap(1 << 18, 5)
+        q = zeta * area
+    c = ss.TraversalConfig(theta=0.7, n_threshold=64, degree=8, max_depth=10)
+    step = 3e-4 if which == "mesh" else 1e-8
+    assert _same(_run(ss, xyz, q, c, 8, "auto", step=step), _run(ss, xyz, q, c, 8, "0", step=step))
