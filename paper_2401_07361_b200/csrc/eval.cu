@@ -569,23 +569,27 @@ void ensure_vinv(Ctx& c, int degree) {
 
 // Particle gather, proxy points and the upward pass (Phases 1-2), on stream
 // s: everything the tile kernels read from pts. tmp: cub scratch private to s.
+// stages: bit 0 the gather + proxy points, bit 1 the upward pass.
 void launch_prep(Ctx& c, cudaStream_t s, DBuf<unsigned char>& tmp, int degree, const double* d_xyz,
-                 const double* d_q, int64_t n) {
+                 const double* d_q, int64_t n, int stages) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   const int P = (degree + 1) * (degree + 2) / 2;
   const int bs = 256;
-  cudaEventRecord(c.ev[0], s);
-  k_gather<<<grid_for(n, bs), bs, 0, s>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
-  SSUM_LAUNCH_CHECK();
-  c.launches++;
-  if (L.n_proxy > 0) {
-    k_proxy<<<grid_for(int64_t(L.n_proxy) * P, bs), bs, 0, s>>>(c.trav.slot_node.p, L.n_proxy, degree,
-                                                                  c.nodes.tri.p, n, c.pts.p);
+  if (stages & 1) {
+    cudaEventRecord(c.ev[0], s);
+    k_gather<<<grid_for(n, bs), bs, 0, s>>>(d_xyz, d_q, B.perm.p, n, c.pts.p);
     SSUM_LAUNCH_CHECK();
     c.launches++;
+    if (L.n_proxy > 0) {
+      k_proxy<<<grid_for(int64_t(L.n_proxy) * P, bs), bs, 0, s>>>(c.trav.slot_node.p, L.n_proxy, degree,
+                                                                    c.nodes.tri.p, n, c.pts.p);
+      SSUM_LAUNCH_CHECK();
+      c.launches++;
+    }
+    cudaEventRecord(c.ev[1], s);
   }
-  cudaEventRecord(c.ev[1], s);
+  if (!(stages & 2)) return;
 
   // ---- upward pass: chunk table (weight node bins cut into <= 1024-particle
   // chunks) built on the device
@@ -641,7 +645,9 @@ void size_eval_buffers(Ctx& c, int degree, int D, int64_t n) {
 // so they run on side_stream while the main stream builds the range lists
 // and tiles (k_leaf_fill / k_fit_fill are latency-bound; the upward pass is
 // FP64 work). evaluate() joins on prep_ev.
-void start_prep(Ctx& c, bool forked) {
+// stages: as launch_prep's (a call with stage 2 only follows one with stage
+// 1 on the same evaluation).
+void start_prep(Ctx& c, bool forked, int stages) {
   if (!c.early.xyz || !c.early_prep || c.bins.n == 0) return;
   const int64_t n = c.bins.n;
   size_eval_buffers(c, c.early.degree, c.early.dim, n);
@@ -649,8 +655,9 @@ void start_prep(Ctx& c, bool forked) {
   // launching work the prep stream need not wait for
   if (!forked) SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
   SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.prep_stream, c.fork_ev, 0));
-  if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.prep_stream, c.io.q, 0));  // q of a host-pointer call
-  launch_prep(c, c.prep_stream, c.cub_tmp_side, c.early.degree, c.early.xyz, c.early.q, n);
+  if (c.io.active && (stages & 1))  // q of a host-pointer call
+    SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.prep_stream, c.io.q, 0));
+  launch_prep(c, c.prep_stream, c.cub_tmp_side, c.early.degree, c.early.xyz, c.early.q, n, stages);
   SSUM_CUDA_CHECK(cudaEventRecord(c.prep_ev, c.prep_stream));
   c.prep_started = true;
 }
@@ -673,7 +680,7 @@ void evaluate(Ctx& c, int kernel, const ssum_config& cfg, const double* d_xyz, c
     c.prep_started = false;
   } else {
     if (c.io.active) SSUM_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.io.q, 0));  // q of a host-pointer call
-    launch_prep(c, c.stream, c.cub_tmp, degree, d_xyz, d_q, n);
+    launch_prep(c, c.stream, c.cub_tmp, degree, d_xyz, d_q, n, 3);
   }
   trace().mark("eval.upward_host");
 

@@ -489,7 +489,8 @@ void proxy_weights(Ctx& c, int degree, const double* xyz, const double* q, int n
 // V^-1 of the degree-d lattice Vandermonde (row-major, P x P) and its exact
 // 1-norm reciprocal condition number (no throw; eval.cu)
 void lattice_inverse(int degree, std::vector<double>& inv, double& rcond);
-void start_prep(Ctx& c, bool forked = false);
+// stages: bit 0 gather + proxy points, bit 1 upward pass
+void start_prep(Ctx& c, bool forked = false, int stages = 3);
 void size_eval_buffers(Ctx& c, int degree, int D, int64_t n);
 void launch_leaf_tiles(Ctx& c, cudaStream_t stream, int kernel, const Tile* tiles, int ntl, const SrcRange* ranges, double* S,
                        bool direct = false);

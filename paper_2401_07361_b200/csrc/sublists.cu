@@ -63,7 +63,7 @@ constexpr int kSubWarps = kSubThreads / 32;
 constexpr int kEcap = SSUM_SUB_ECAP;  // emissions per block
 constexpr int kFcap = SSUM_SUB_FCAP;  // frontier entries per step
 constexpr int kIpt = kEcap / kSubThreads;
-constexpr int kIdxBits = 12;          // emission index bits of a sort key (kEcap <= 4096)
+constexpr int kIdxBits = kEcap <= 1024 ? 10 : 12;  // emission index bits of a sort key
 static_assert(kEcap <= (1 << kIdxBits), "emission index bits");
 constexpr int kLvlBits = 6;           // level below R (< 64: max_depth <= 40)
 constexpr int kMaxChain = 48;         // root-to-leaf path nodes (max_depth <= 40)
@@ -301,7 +301,11 @@ __global__ void __launch_bounds__(kSubThreads, SSUM_SUB_MINB) k_sub_lists(SubArg
       }
     }
     __syncthreads();  // frontier storage becomes the sort's scratch
-    SubSort(sm.u.sort).Sort(kk, 0, 32);
+    // only the key bits in use (+1, so the all-ones padding sorts last):
+    // 27 instead of 32 at cmax 256, seven 4-bit passes instead of eight
+    const unsigned loc_max = 64u + (static_cast<unsigned>(max(cntR, 1)) << kLvlBits) + 63u;
+    const unsigned key_max = (((loc_max << 1) | 1u) << kIdxBits) | ((1u << kIdxBits) - 1u);
+    SubSort(sm.u.sort).Sort(kk, 0, min(32, 32 - __clz(key_max) + 1));
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kIpt; ++i) sm.u.keys[tid * kIpt + i] = kk[i];
@@ -802,7 +806,9 @@ void build_lists_subtree(Ctx& c, const ssum_config& cfg) {
   // the proxy points + upward pass of every big node (low-priority stream)
   // run beside the list builder's latency-bound blocks
   if (c.early.xyz) size_eval_buffers(c, c.early.degree, c.early.dim, N);
-  if (!lean_up) SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+  SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+  // restricted call: the prep follows the builder (the upward pass needs its
+  // marks; running the gather and proxy points beside it measured no faster)
   k_sub_lists<<<S.n_cut, kSubThreads, S.smem, c.stream>>>(a);
   SSUM_LAUNCH_CHECK();
   c.launches++;
@@ -819,8 +825,10 @@ void build_lists_subtree(Ctx& c, const ssum_config& cfg) {
     c.launches += 2;
     c.up_list = S.wsel.p + 1;
     c.up_count = S.wsel.p;
+    start_prep(c, false, 3);
+  } else {
+    start_prep(c, true, 3);
   }
-  start_prep(c, !lean_up);
   // counts, evaluations, visits and the range use: read back with the
   // evaluation's final sync (finalize_counts / sub_lists_check)
   SSUM_CUDA_CHECK(cudaMemcpyAsync(TS.h_small + 8, TS.counters.p, 21 * sizeof(unsigned long long),
