@@ -310,8 +310,19 @@ __global__ void __launch_bounds__(32 * kFinWarps) k_finish_tree(
       const bool mine = fit && a == an;
       SSUM_DCHECK(pslot[an] >= 0);
       const double* c = coeff + size_t(pslot[an]) * D * P;
-      for (int i = lane; i < D * P; i += 32) cs[w][(i % P) * DP + i / P] = c[i];
-      if (lane < 12) cr[w][lane] = cramer[12 * an + lane];
+      // every load of the staging issued before its first store (one
+      // latency per staged node, not one per 32 coefficients)
+      constexpr int kIt = (D * P + 31) / 32;
+      double tmp[kIt];
+#pragma unroll
+      for (int j = 0; j < kIt; ++j) tmp[j] = lane + 32 * j < D * P ? c[lane + 32 * j] : 0.0;
+      const double crv = lane < 12 ? cramer[12 * an + lane] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kIt; ++j) {
+        const int i = lane + 32 * j;
+        if (i < D * P) cs[w][(i % P) * DP + i / P] = tmp[j];
+      }
+      if (lane < 12) cr[w][lane] = crv;
       __syncwarp();
       if (mine) {
         double b1, b2, b3;
