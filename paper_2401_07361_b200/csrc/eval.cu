@@ -543,12 +543,29 @@ void lattice_inverse(int degree, std::vector<double>& inv, double& rcond) {
   rcond = (an > 0.0 && std::isfinite(in) && in > 0.0) ? 1.0 / (an * in) : 0.0;
 }
 
-// The far-pair log table (kernels.cuh log_tab): (1 / c_j, log c_j) for the
-// 512 bucket centres, each correctly rounded from 80-bit precision.
+// The far-pair log table (kernels.cuh log_tab): per bucket centre c_j a double
+// r_j near 1 / c_j and L_j = RN(-log r_j). r_j is searched (Gal's accurate
+// tables) outward from 1 / c_j in relative steps of 1e-9 for a double whose
+// -log r_j lies within 2^-6 ulp of its double L_j (80-bit logl resolves
+// ~2^-11 ulp). Steps of one ulp would not do: c_j has ~11 significant bits,
+// so near 1 an ulp of r moves -log r by an integer number of L's ulps. ~35
+// tries per bucket (tools/log_coeffs.py), at most 4096 (a 2e-6 relative move:
+// inside the 2^-12 slack the polynomial range allows). c = 1: r = 1, L = 0.
 void log_table(double2* tab) {
   for (int j = 0; j < kLogTabN; ++j) {
     const long double c = static_cast<long double>(log_tab_node(j));
-    tab[j] = make_double2(static_cast<double>(1.0L / c), static_cast<double>(logl(c)));
+    const long double r0 = 1.0L / c;
+    double best_r = static_cast<double>(r0), best_e = 1.0;
+    for (int i = 0; i < 4096 && best_e > 1.0 / 64; ++i) {
+      const long double step = 1e-9L * static_cast<long double>((i & 1) ? -((i + 1) / 2) : i / 2);
+      const double r = static_cast<double>(r0 * (1.0L + step));
+      const long double L = -logl(static_cast<long double>(r));
+      const double Ld = static_cast<double>(L);
+      const long double u = Ld == 0.0 ? 1.0L : static_cast<long double>(std::nextafter(std::fabs(Ld), 1.0) - std::fabs(Ld));
+      const double e = static_cast<double>(fabsl(L - static_cast<long double>(Ld)) / u);
+      if (e < best_e) best_e = e, best_r = r;
+    }
+    tab[j] = make_double2(best_r, static_cast<double>(-logl(static_cast<long double>(best_r))));
   }
 }
 

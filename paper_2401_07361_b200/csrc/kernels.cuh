@@ -66,51 +66,74 @@ __device__ __forceinline__ double q_over(double q, double den) {
 //   t1 = hi(x) - kLogTabK (kLogTabK = hi word just above sqrt(2)/2), so
 //   k = t1 >> 20 is the exponent with x = 2^k m, m in [0.7072, 1.4143), and
 //   hi(m) = hi(x) - (t1 & 0xfff00000) (integer ops only);
-//   j = the next 9 bits of t1: 512 buckets of m, bucket j centred on
-//   c_j = (hi word kLogTabK + 2048 j + 1024, low word 0) — the bucket of m = 1
+//   j = the next 7 bits of t1: 128 buckets of m, bucket j centred on
+//   c_j = (hi word kLogTabK + 8192 j + 4096, low word 0) — the bucket of m = 1
 //   has c = 1 exactly, so x near 1 keeps full relative accuracy;
-//   t = (m - c_j) / c_j with |t| <= 2^-10 (m - c_j exact by Sterbenz);
-//   log m = log c_j + log1p(t), log1p through t^6 (truncation < 2^-60 t);
-//   log x = k ln2_hi + (log c_j + (k ln2_lo + log1p t)), ln 2 split into a
-//   21-bit head (k ln2_hi exact) and a tail; |log x| >= ~0.35 whenever k != 0,
-//   so the sum never cancels. (1 / c_j, log c_j) come from a 512-entry table
-//   (log_table, correctly rounded from 80-bit precision) staged in shared
-//   memory. 15 FP64 and ~9 integer instructions per pair including the
-//   denominator and the accumulation, against 17 + ~14 for the 65-entry,
-//   degree-8 version before it; <= 1.5 ulp (tests/test_gpu_parity.py
-//   test_log_far_accuracy bounds it by 2 ulp over [2^-20, 4]).
-constexpr int kLogTabN = 512;
-constexpr int kLogTabK = 0x3FE6A400;  // (0x3FF00000 - kLogTabK) % 2048 == 1024: c = 1 is a bucket centre
-void log_table(double2* tab);         // host: kLogTabN entries (1 / c_j, log c_j)
+//   with r_j a double within 2^-12 of 1 / c_j (r = 1 for the bucket of m = 1):
+//   t = RN(m r_j - 1) in one FMA (|t| <= 2^-8 + 2^-12, relative rounding
+//   error 2^-53) and log m = log1p(m r_j - 1) - log r_j exactly. The table
+//   holds L_j = RN(-log r_j); r_j is chosen (log_table: Gal's accurate-table
+//   search) so that -log r_j lies within 2^-6 ulp of L_j, so the table adds
+//   no rounding of its own where log c_j and log1p t cancel (x near 1);
+//   log1p t = t + t^2 p(t), p the quartic Chebyshev fit of (log1p t - t) / t^2
+//   on |t| <= 2^-8 (tools/log_coeffs.py: |error| < 2^-54.8 |t|);
+//   log x = k ln2 + (L_j + log1p t) in one FMA: |log x| >= ~0.34 whenever
+//   k != 0, so nothing cancels, and k (ln2 - RN(ln2)) <= 0.3 ulp for
+//   |k| <= 20. 13 FP64 and ~8 integer instructions per pair including the
+//   denominator and the accumulation; <= 1.2 ulp against 80-bit logl over 8M
+//   points and every bucket edge (host emulation in tools/log_coeffs.py: 1.18;
+//   tests/test_gpu_parity.py test_log_far_accuracy bounds it by 2 ulp over
+//   [2^-20, 4] on the device).
+// Shared-memory layout: the 16-byte entry (r_j, L_j) is stored 8 times, copy
+// s in bank group s (address (8 j + s) * 16): lane l reads copy l & 7, so the
+// 8 lanes of each quarter-warp that one LDS.128 serves always hit 8 distinct
+// bank groups — conflict-free whatever buckets the lanes' denominators fall
+// in. With one copy, ncu measured 10.2 wavefronts per table load instead of
+// 4 (a warp's denominators span ~a factor 2, i.e. random buckets), and the
+// log tiles were shared-memory-bandwidth bound (~92% of the SM's wavefronts).
+constexpr int kLogTabBits = 7;
+constexpr int kLogTabN = 1 << kLogTabBits;
+constexpr int kLogTabCopies = 8;
+constexpr int kLogTabShift = 20 - kLogTabBits;
+// (0x3FF00000 - kLogTabK) % 8192 == 4096: c = 1 is a bucket centre; m in [0.709, 1.418)
+constexpr int kLogTabK = 0x3FE6B000;
+void log_table(double2* tab);  // host: kLogTabN entries (r_j, L_j = RN(-log r_j))
 __host__ __device__ __forceinline__ double log_tab_node(int j) {
+  const unsigned hi = static_cast<unsigned>(kLogTabK + (j << kLogTabShift) + (1 << (kLogTabShift - 1)));
 #if defined(__CUDA_ARCH__)
-  return __hiloint2double(kLogTabK + (j << 11) + 1024, 0);
+  return __hiloint2double(static_cast<int>(hi), 0);
 #else
-  const unsigned long long bits = static_cast<unsigned long long>(static_cast<unsigned>(kLogTabK + (j << 11) + 1024))
-                                  << 32;
+  const unsigned long long bits = static_cast<unsigned long long>(hi) << 32;
   double d;
   __builtin_memcpy(&d, &bits, 8);
   return d;
 #endif
 }
 
-__device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab) {
-  constexpr double kLn2Hi = 0x1.62e42p-1;           // ln 2, low 32 mantissa bits cleared
-  constexpr double kLn2Lo = 0x1.fdf473de6af28p-22;  // ln 2 - kLn2Hi
-  const int hi = __double2hiint(x);
-  const int t1 = hi - kLogTabK;
+// log_tab in two halves: the table slot of x, and the rest given its entry.
+// `tab` is the staged table already offset by this lane's copy (lane & 7).
+__device__ __forceinline__ int log_tab_slot(int t1) {
+  return ((t1 >> kLogTabShift) & (kLogTabN - 1)) * kLogTabCopies;
+}
+__device__ __forceinline__ double log_tab_fin(double x, int t1, double2 e) {
+  constexpr double kLn2 = 0x1.62e42fefa39efp-1;
   const int kk = t1 >> 20;  // arithmetic shift: the exponent of x relative to m
-  const int j = (t1 >> 11) & (kLogTabN - 1);
-  const double m = __hiloint2double(hi - (t1 & static_cast<int>(0xfff00000u)), __double2loint(x));
-  const double2 e = tab[j];
-  const double t = (m - log_tab_node(j)) * e.x;
-  double p = fma(t, -1.0 / 6.0, 1.0 / 5.0);
-  p = fma(t, p, -0.25);
-  p = fma(t, p, 1.0 / 3.0);
+  const double m = __hiloint2double(__double2hiint(x) - (t1 & static_cast<int>(0xfff00000u)), __double2loint(x));
+  const double t = fma(m, e.x, -1.0);
+  double p = fma(t, -0x1.555695a65ad63p-3, 0x1.999b07ad05760p-3);
+  p = fma(t, p, -0x1.ffffffffafd7bp-3);
+  p = fma(t, p, 0x1.5555555527877p-2);
   p = fma(t, p, -0.5);
   const double l1p = fma(t * t, p, t);
-  const double dk = static_cast<double>(kk);
-  return fma(dk, kLn2Hi, e.y) + fma(dk, kLn2Lo, l1p);
+  return fma(static_cast<double>(kk), kLn2, e.y + l1p);
+}
+__device__ __forceinline__ double log_tab(double x, const double2* __restrict__ tab) {
+  const int t1 = __double2hiint(x) - kLogTabK;  // one subtraction for the slot, m and k
+  return log_tab_fin(x, t1, tab[log_tab_slot(t1)]);
+}
+// stage the table for log_tab (every copy), then offset it by the lane's copy
+__device__ __forceinline__ void log_tab_stage(double2* dst, const double2* __restrict__ src, int tid, int nth) {
+  for (int i = tid; i < kLogTabN * kLogTabCopies; i += nth) dst[i] = src[i / kLogTabCopies];
 }
 
 template <int KER>
@@ -224,6 +247,44 @@ __device__ __forceinline__ void far_block(const double4* x, const double4* __res
       a[c % NT].s[0] = fma(y[c / NT].w, l, a[c % NT].s[0]);
     }
   }
+}
+
+// far_block<kLOG> (well-separated steps, not CUBIC) in two halves for a
+// software-pipelined loop: log_step_pre forms one step's denominators and
+// issues its table loads, log_step_post finishes the logs and accumulates.
+// The table slot depends on the denominator, so in far_block every pair
+// waited on a dependent shared-memory load in mid-chain (ncu: short-scoreboard
+// stalls at the first DFMA after it); issuing step s + 1's loads before
+// finishing step s hides that latency. Same operations per pair, bitwise
+// far_block's sums.
+template <int NT, int NS>
+struct LogStep {
+  double den[NT * NS];
+  double2 e[NT * NS];
+  double q[NS];
+};
+template <int NT, int NS>
+__device__ __forceinline__ void log_step_pre(const double4* x, const double4* __restrict__ B, int G,
+                                             const double2* __restrict__ tab, LogStep<NT, NS>& st) {
+  constexpr int C = NT * NS;
+  double4 y[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) y[s] = B[s * G];
+#pragma unroll
+  for (int c = 0; c < C; ++c) st.den[c] = fma(-x[c % NT].x, y[c / NT].x, 1.0);
+#pragma unroll
+  for (int c = 0; c < C; ++c) st.den[c] = fma(-x[c % NT].y, y[c / NT].y, st.den[c]);
+#pragma unroll
+  for (int c = 0; c < C; ++c) st.den[c] = fma(-x[c % NT].z, y[c / NT].z, st.den[c]);
+#pragma unroll
+  for (int c = 0; c < C; ++c) st.e[c] = tab[log_tab_slot(__double2hiint(st.den[c]) - kLogTabK)];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) st.q[s] = y[s].w;
+}
+template <int NT, int NS>
+__device__ __forceinline__ void log_step_post(const LogStep<NT, NS>& st, Acc<kLOG>* a) {
+#pragma unroll
+  for (int c = 0; c < NT * NS; ++c) a[c % NT].s[0] = fma(st.q[c / NT], log_tab_fin(st.den[c], __double2hiint(st.den[c]) - kLogTabK, st.e[c]), a[c % NT].s[0]);
 }
 
 // One step of a near-possible range, decided per warp by a vote (the

@@ -31,11 +31,11 @@ __global__ void k_dfma_chain(double* out, int iters, double a, double b) {
 
 __global__ void k_log_far(const double* __restrict__ x, int64_t n, const double2* __restrict__ tab_g,
                           double* __restrict__ out) {
-  __shared__ double2 tab[kLogTabN];  // as the log tiles stage it
-  for (int j = threadIdx.x; j < kLogTabN; j += blockDim.x) tab[j] = tab_g[j];
+  __shared__ double2 tab[kLogTabN * kLogTabCopies];  // as the log tiles stage it
+  log_tab_stage(tab, tab_g, threadIdx.x, blockDim.x);
   __syncthreads();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = log_tab(x[i], tab);
+  if (i < n) out[i] = log_tab(x[i], tab + (threadIdx.x & (kLogTabCopies - 1)));
 }
 
 }  // namespace

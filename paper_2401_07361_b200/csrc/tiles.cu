@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(NTH, MINB)
   constexpr int kChunk = CHUNK;
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
   int2* rtab = reinterpret_cast<int2*>(smem + kStages * sizeof(double4) * (kChunk + kPad));
-  double2* ltab = reinterpret_cast<double2*>(rtab + kRangeCap);  // log kernel: log_table staged
+  // log kernel: log_table staged, kLogTabCopies copies (kernels.cuh log_tab)
+  double2* ltab_s = reinterpret_cast<double2*>(rtab + kRangeCap);
+  const double2* ltab = ltab_s + (threadIdx.x & (kLogTabCopies - 1));  // this lane's copy
   static_assert(sizeof(double) * NTH * D * kTpt <= kStages * sizeof(double4) * (kChunk + kPad), "red alias");
   static_assert(kPad <= NTH, "zero tail");
   double* red = reinterpret_cast<double*>(&buf[0][0]);  // group partials, after the source loop
@@ -172,8 +174,7 @@ __global__ void __launch_bounds__(NTH, MINB)
 #pragma unroll
     for (int st = 0; st < kStages; ++st) buf[st][kChunk + tid] = zero4;
   }
-  if constexpr (KER == kLOG)
-    for (int j = tid; j < kLogTabN; j += NTH) ltab[j] = ltab_g[j];
+  if constexpr (KER == kLOG) log_tab_stage(ltab_s, ltab_g, tid, NTH);
   if (tid == 0) {
 #pragma unroll
     for (int st = 0; st < kStages; ++st) {
@@ -383,6 +384,23 @@ __global__ void __launch_bounds__(NTH, MINB)
     // well-separated sources only: branch-free, kNs sources x kTpt targets
     // of independent chains per step (zero-padded tail contributes 0)
     const double4* Bp = B + it * kStep;
+#ifdef SSUM_LOG_PIPE  // measured: no gain (the table loads were bandwidth-, not latency-bound)
+    if constexpr (KER == kLOG && MODE != kDirectMode) {
+      // log: software-pipelined (kernels.cuh log_step_pre / log_step_post)
+      if (it < steps) {
+        LogStep<kTpt, kNs> cur, nxt;
+        log_step_pre(x, Bp, G, ltab, cur);
+#pragma unroll 2
+        for (++it; it < steps; ++it) {
+          Bp += kStep;
+          log_step_pre(x, Bp, G, ltab, nxt);
+          log_step_post(cur, a);
+          cur = nxt;
+        }
+        log_step_post(cur, a);
+      }
+    } else
+#endif
 #pragma unroll kFU
     for (; it < steps; ++it, Bp += kStep) far_block<KER, kTpt, kNs, false, MODE == kDirectMode>(x, Bp, G, a, nullptr, ltab);
     __syncwarp();
@@ -479,12 +497,12 @@ __global__ void k_direct_tiles(int64_t n, Tile* tiles, SrcRange* range) {
 template <int KER, int CHUNK>
 constexpr size_t tile_smem() {
   return kStages * sizeof(double4) * (CHUNK + kPad) + sizeof(int2) * kRangeCap +
-         (KER == kLOG ? sizeof(double2) * kLogTabN : 0);
+         (KER == kLOG ? sizeof(double2) * kLogTabN * kLogTabCopies : 0);
 }
-// the log tiles stream smaller chunks so that the 8 KB log table still fits
-// four blocks per SM
+// the log tiles stream smaller chunks so that the 16 KB log table (8 copies)
+// still fits four blocks per SM
 #ifndef SSUM_LOG_CHUNK
-#define SSUM_LOG_CHUNK 640
+#define SSUM_LOG_CHUNK 512
 #endif
 constexpr int kLogChunk = SSUM_LOG_CHUNK;
 
