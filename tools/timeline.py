@@ -94,6 +94,11 @@ out = {
     "config": args.config, "steps": args.steps,
     "span_ms_per_step": span / per / 1e3, "busy_union_ms_per_step": union / per / 1e3,
     "idle_ms_per_step": (span - union) / per / 1e3, "n_gaps": len(gaps),
+    # host round trips (read-backs) leave long gaps; back-to-back dependent
+    # launches short ones
+    "idle_by_gap_size_ms_per_step": {
+        lbl: sum(g[0] for g in gaps if lo <= g[0] < hi) / per / 1e3
+        for lbl, lo, hi in (("<5us", 0, 5), ("5-10us", 5, 10), ("10-30us", 10, 30), (">=30us", 30, 1e18))},
     "kernels": sorted(({"kernel": k, "ms_per_step": v / per / 1e3, "launches_per_step": cnt[k] / per}
                        for k, v in busy.items()), key=lambda d: -d["ms_per_step"]),
     "largest_gaps_us": [{"us": g, "after": a, "before": b, "at_ms": t / 1e3}
@@ -101,6 +106,7 @@ out = {
 }
 print(f"span {out['span_ms_per_step']:.3f} ms/step, busy union {out['busy_union_ms_per_step']:.3f}, "
       f"idle {out['idle_ms_per_step']:.3f} in {len(gaps)} gaps")
+print("idle by gap size (ms/step):", {k: round(v, 3) for k, v in out["idle_by_gap_size_ms_per_step"].items()})
 for d in out["kernels"][:40]:
     print(f"  {d['ms_per_step']:8.3f} ms  x{d['launches_per_step']:5.1f}  {d['kernel']}")
 print("largest gaps:")

@@ -41,17 +41,30 @@ for k in range(8):
         rows.append((e0.elapsed_time(e1), st.pp_pc_ms, st.cp_cc_fit_ms, st.upward_ms, st.finish_ms,
                      st.bin_seconds * 1e3, st.traversal_seconds * 1e3))
 med = [statistics.median(c) for c in zip(*rows)]
-print(json.dumps(dict(zip(['step', 'pp_pc', 'fit', 'up', 'finish', 'bin', 'trav'], med))))
+res = dict(zip(['step', 'pp_pc', 'fit', 'up', 'finish', 'bin', 'trav'], med))
+# relative L2 of this library's velocities against the first (default) library's
+import os, numpy as np
+u = out.cpu().numpy()
+ref = sys.argv[2]
+if os.path.exists(ref):
+    b = np.load(ref)
+    res['rel_l2_vs_default'] = float(np.linalg.norm(u - b) / np.linalg.norm(b))
+else:
+    np.save(ref, u)
+print(json.dumps(res))
 """
 
 
 def main():
     lvl = sys.argv[1] if len(sys.argv) > 1 else "9"
+    ref = os.path.join("/tmp", f"variant_default_{lvl}.npy")
+    if os.path.exists(ref):
+        os.remove(ref)
     libs = [os.path.join(ROOT, "paper_2401_07361_b200", "lib", "libspheresum_b200.so")]
     libs += sorted(glob.glob(os.path.join(ROOT, "paper_2401_07361_b200", "lib", "variants", "*.so")))
     for lib in libs:
         env = dict(os.environ, SSUM_LIBRARY=lib)
-        r = subprocess.run([sys.executable, "-c", CHILD, lvl], cwd=ROOT, env=env, capture_output=True, text=True)
+        r = subprocess.run([sys.executable, "-c", CHILD, lvl, ref], cwd=ROOT, env=env, capture_output=True, text=True)
         tail = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr.strip()[-300:]
         print(os.path.basename(lib), tail, flush=True)
 
