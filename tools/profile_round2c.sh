@@ -17,7 +17,10 @@ timeout 600 python tools/timeline.py 1 --config c5 --json $P/timeline_config5.js
 timeout 900 python tools/part_bench.py 1 2 4 8 --shard-bin --phases > $P/parts_config4.jsonl 2>&1
 timeout 900 python tools/part_bench.py 1 2 4 8 --shard-bin --phases --config c5 > $P/parts_config5.jsonl 2>&1
 SSUM_TRACE=1 timeout 600 python tools/sub_check.py l5 l7 c2 c4 c3s > $P/sub_check.txt 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $P/launches_config4.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-error > $P/ncu_launch.log 2>&1
+# under ncu every launch is serialised and slowed, so the measured list-builder
+# choice would pick the one-launch subtree builder; pin the builder the live
+# bench uses at this size (the global traversal, see timeline_config4.txt)
+SSUM_SUB_LISTS=0 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $P/launches_config4.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-error > $P/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_tiles|k_finish|k_up_partial|k_walk|k_bfs|k_leaf_fill|k_rk4|k_sub_lists" -c 12 -o $P/full python tools/profile_step.py 1 > $P/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_tiles" -c 2 -o $P/full_log python tools/profile_step.py 1 8 8 0.7 log > $P/ncu_full_log.log 2>&1
 timeout 600 python tools/host_overhead.py 4 > $P/host_overhead.txt 2>&1

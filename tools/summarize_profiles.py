@@ -34,7 +34,13 @@ def launches(path):
     starts = [i for i, (n, _) in enumerate(seq) if n in ("k_walk", "k_bin_roots")] + [len(seq)]
     calls = [seq[a:b] for a, b in zip(starts[:-1], starts[1:])]
     device_calls = [c for c in calls if sum(1 for n, _ in c if n.startswith("k_finish")) == 1]
-    step = (device_calls or calls)[-1]
+    # the capture's last calls may be a list-builder trial (k_sub_lists timed
+    # against k_bfs every 512 calls): report the last call on the chosen
+    # builder, i.e. the kind the majority of the device calls used
+    pool = device_calls or calls
+    sub = [c for c in pool if any(n == "k_sub_lists" for n, _ in c)]
+    glob = [c for c in pool if not any(n == "k_sub_lists" for n, _ in c)]
+    step = (glob if len(glob) >= len(sub) else sub)[-1]
     ends = calls
     agg = OrderedDict()
     for name, ms in step:
