@@ -402,6 +402,86 @@ __device__ __forceinline__ void near_exact_block(const double4* x, const double4
   }
 }
 
+// hi word of 2^-30: den < 2^-30 ~ 9.3e-10 (or negative) <=> (int)hi(den) < kCloseHi
+constexpr int kCloseHi = 0x3E100000;
+
+// Near-possible block of a dense leaf tile, lean form (the default): the
+// denominator with the reference's rounding for EVERY pair (6 FP64
+// instructions, stage by stage across the NT*NS chains like far_block), the
+// reciprocal by MUFU seed + one Newton step (relative error <= 1e-12 per
+// term, far_block's) and S += r y — 12 FP64 instructions per pair against
+// near_exact_block's 18. A pair's term is x cross (r y): accumulating r y
+// instead of r (y - x) leaves an absolute rounding error of ~1e-16 r in S,
+// the reference's own (it rounds cross(x, y) to ~1e-16 absolute before the
+// division, kernels.hpp:26-32), harmless while r stays moderate. Pairs
+// closer than den < 2^-30 (arc < 4.3e-5: the self pair, a singular pair, or
+// a genuinely close pair of a dense cloud, r up to q 1e14) are masked out of
+// those sums and taken one by one on near_exact_block's arithmetic (self
+// pair by list position, singular guard, ~1 ulp q / den, r (y - x)); on a
+// mesh (config 5) that is the self pair only.
+template <int NT, int NS>
+__device__ __forceinline__ void near_lean_block(const double4* x, const double4* __restrict__ B, int G,
+                                                Acc<kBS>* a, int f0, const int* selfpos, int* flags) {
+  // one source at a time (NT chains interleaved): the 64-register leaf
+  // kernel has no room for NT*NS chains of den / product / reciprocal here
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const double4 y = B[s * G];
+    double den[NT], p[NT], r[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) den[t] = __dmul_rn(x[t].x, y.x);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) p[t] = __dmul_rn(x[t].y, y.y);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) den[t] = __dadd_rn(den[t], p[t]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) p[t] = __dmul_rn(x[t].z, y.z);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) den[t] = __dadd_rn(den[t], p[t]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) den[t] = __dsub_rn(1.0, den[t]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) r[t] = rcp_approx(den[t]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) p[t] = fma(-den[t], r[t], 1.0);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) r[t] = __dmul_rn(y.w, r[t]);
+#pragma unroll
+    for (int t = 0; t < NT; ++t) r[t] = fma(r[t], p[t], r[t]);
+    bool close = false;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if (__double2hiint(den[t]) < kCloseHi) {  // the masked term's high word cleared: <= 2^-1022, never NaN/inf
+        close = true;
+        r[t] = __hiloint2double(0, __double2loint(r[t]));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      a[t].s[0] = fma(r[t], y.x, a[t].s[0]);
+      a[t].s[1] = fma(r[t], y.y, a[t].s[1]);
+      a[t].s[2] = fma(r[t], y.z, a[t].s[2]);
+    }
+    if (close) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        if (f0 + s * G == selfpos[t]) continue;  // treecode.cpp:388
+        const double d = __dsub_rn(1.0, __dadd_rn(__dadd_rn(__dmul_rn(x[t].x, y.x), __dmul_rn(x[t].y, y.y)),
+                                                  __dmul_rn(x[t].z, y.z)));
+        if (__double2hiint(d) >= kCloseHi) continue;
+        if (d <= kSingularTol) {  // kernels.hpp:19,27-29
+          atomicOr(flags, kFlagSingular);
+          continue;
+        }
+        const double rr = q_over(y.w, d);
+        a[t].s[0] = fma(rr, __dsub_rn(y.x, x[t].x), a[t].s[0]);
+        a[t].s[1] = fma(rr, __dsub_rn(y.y, x[t].y), a[t].s[1]);
+        a[t].s[2] = fma(rr, __dsub_rn(y.z, x[t].z), a[t].s[2]);
+      }
+    }
+  }
+}
+
 // Second walk over one far_block<..., true> block whose warp saw a near pair
 // other than its self pairs: adds the reference-rounded contribution of each
 // near pair of distinct points (pair_slow, which also raises the singular

@@ -301,7 +301,12 @@ __global__ void __launch_bounds__(NTH, MINB)
         for (int q = 0; q < kTpt; ++q) selfpos[q] = (T.has_self & 1) ? ti[q] + T.self_shift : -1;
         const int f0 = c * kChunk + g;
 #pragma unroll 1
-        for (; it < near_steps; ++it) near_exact_block<kTpt, kNs>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos, flags);
+        for (; it < near_steps; ++it)
+#ifdef SSUM_DENSE_EXACT18  // tuning variant: every near-possible pair on the 18-instruction exact form
+          near_exact_block<kTpt, kNs>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos, flags);
+#else
+          near_lean_block<kTpt, kNs>(x, B + it * kStep, G, a, f0 + it * kStep, selfpos, flags);
+#endif
       }
     }
 #ifdef SSUM_NEAR_VOTE
