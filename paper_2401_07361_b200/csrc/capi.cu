@@ -34,9 +34,12 @@ Trace& trace() {
 }
 
 void check_flags(Ctx& c, const char* where) {
-  int f = 0;
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  // pinned destination: a copy into pageable memory takes the driver's staged
+  // path, which stalled the host ~0.1 ms per call (CUPTI timeline)
+  if (!c.h_pinned) SSUM_CUDA_CHECK(cudaMallocHost(&c.h_pinned, 64 * sizeof(int)));
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(c.h_pinned, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  const int f = c.h_pinned[0];
   c.last_flags = f;
   if (f & kFlagGeometry) throw Error(SSUM_GEOMETRY, std::string(where) + ": degenerate geometry");
   if (f & kFlagSingular)
@@ -499,6 +502,7 @@ void ssum_destroy(ssum_ctx* h) {
   if (c->bins.h_small) cudaFreeHost(c->bins.h_small);
   if (c->trav.h_small) cudaFreeHost(c->trav.h_small);
   if (c->trav.h_plan) cudaFreeHost(c->trav.h_plan);
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
   dbuf_stream() = nullptr;  // the buffers go back to the pool in legacy-stream order
   cudaStream_t own = c->own_stream;
   delete c;
@@ -953,9 +957,11 @@ int ssum_bin_walk_shard(ssum_ctx* h, const double* d_xyz, int64_t n, int64_t i0,
     *keys = c.bins.wkey.p;
     *leaf_of = c.bins.leaf_of.p;
     if (*walked) {
-      int f = 0;  // a particle in no root face: the same GeometryError as the binning
-      SSUM_CUDA_CHECK(cudaMemcpyAsync(&f, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      // a particle in no root face: the same GeometryError as the binning
+      if (!c.h_pinned) SSUM_CUDA_CHECK(cudaMallocHost(&c.h_pinned, 64 * sizeof(int)));
+      SSUM_CUDA_CHECK(cudaMemcpyAsync(c.h_pinned + 1, c.d_flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
       SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      const int f = c.h_pinned[1];
       if (f & kFlagGeometry) {
         c.bins.walked_n = -1;
         throw Error(SSUM_GEOMETRY, "bin_particles: particle contained in no root face");

@@ -269,6 +269,7 @@ struct TravScratch {
   DBuf<int> nr, nt, nr_off, nt_off, fnr, fnr_off;
   DBuf<unsigned long long> counters;  // [0..3] kinds, [4..7] kernel evals
   unsigned long long* h_small = nullptr;  // pinned: [0..7] scratch, [8..15] counters read-back
+  int bfs_namb = -1;  // k_bfs's read-back of the MAC guard band's undecided-pair count (-1: not read)
   // single-launch traversal (traversal.cu bfs_persistent): the last call's
   // frontier sizes and emission count size the next call's buffers
   std::vector<int> plan_m;

@@ -552,11 +552,20 @@ static bool host_mac(const double* ct, const double* v1t, const double* cs, cons
 // After a traversal: decide the pairs it met inside the guard band on the
 // host, add them to the table and report whether the traversal must be
 // redone (a provisional decision may have differed).
-static bool resolve_mac(Ctx& c) {
+// known_namb >= 0: the undecided-pair count already read back (k_bfs's own
+// read-back carries it: a separate copy into pageable memory stalled the host
+// ~115 us per evaluation on the staged-copy path, CUPTI timeline).
+static bool resolve_mac(Ctx& c, int known_namb = -1) {
   MacGuard& g = c.mac;
-  int namb = 0;
-  SSUM_CUDA_CHECK(cudaMemcpyAsync(&namb, g.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-  SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  int namb = known_namb;
+  if (namb < 0) {
+    TravScratch& S = c.trav;
+    if (!S.h_small) SSUM_CUDA_CHECK(cudaMallocHost(&S.h_small, 32 * sizeof(unsigned long long)));
+    int* h = reinterpret_cast<int*>(S.h_small + 30);
+    SSUM_CUDA_CHECK(cudaMemcpyAsync(h, g.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    namb = *h;
+  }
   if (namb == 0) return false;
   const int m = std::min(namb, static_cast<int>(MacGuard::kAmbCap));
   std::vector<int2> pairs(static_cast<size_t>(m));
@@ -689,7 +698,8 @@ static long long bfs_synchronous(Ctx& c, const ssum_config& cfg) {
 // the end. False (nothing committed) when there is no previous call, the
 // launch is refused, or a step outgrew the capacities: the caller then runs
 // the step-by-step traversal, which also refreshes the sizes.
-static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
+template <class AfterLaunch>
+static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out, AfterLaunch&& after_launch) {
   Lists& L = c.lists;
   Binned& B = c.bins;
   TravScratch& S = c.trav;
@@ -759,10 +769,14 @@ static bool bfs_persistent(Ctx& c, const ssum_config& cfg, long long& ne_out) {
     return false;
   }
   c.launches += 2;
+  after_launch();  // host work that need not precede the traversal (the prep stream's launches)
   int* h = reinterpret_cast<int*>(S.h_plan);
   SSUM_CUDA_CHECK(cudaMemcpyAsync(h, S.dm.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaMemcpyAsync(S.h_plan + 128, S.debase.p, sizeof(long long), cudaMemcpyDeviceToHost, c.stream));
+  int* h_amb = reinterpret_cast<int*>(S.h_plan + 129);  // the MAC guard band's undecided pairs, same read-back
+  SSUM_CUDA_CHECK(cudaMemcpyAsync(h_amb, c.mac.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SSUM_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  S.bfs_namb = *h_amb;
   if (h[1] != 0) return false;
   S.plan_m.assign(1, h[2]);
   S.plan_ne = S.h_plan[128];
@@ -798,22 +812,49 @@ void traverse_and_build_lists(Ctx& c, const ssum_config& cfg, bool keep_order_ke
   // now and runs beside it; fit tiles are indexed by slot
   c.plan_lists = !keep_order_keys && c.sub.valid && c.sub.thr == cfg.n_threshold && c.sub.n_big > 0 &&
                  c.plan_lists_ok;
+  // The prep stream forks here but its launches are queued behind k_bfs's:
+  // nothing else starts while the cooperative kernel is resident anyway, and
+  // queuing the prep's ~8 launches first kept the traversal waiting ~60 us
+  // on the host (CUPTI timeline). SSUM_PREP_FIRST=1: the earlier order.
+  static const bool prep_first = [] {
+    const char* e = std::getenv("SSUM_PREP_FIRST");
+    return e && *e == '1';
+  }();
+  bool prep_pending = false;
   if (c.plan_lists) {
     L.n_proxy = L.n_weight = c.sub.n_big;
-    start_prep(c);
+    if (prep_first || !c.early.xyz || !c.early_prep) {
+      start_prep(c);
+    } else {
+      size_eval_buffers(c, c.early.degree, c.early.dim, N);
+      SSUM_CUDA_CHECK(cudaEventRecord(c.fork_ev, c.stream));
+      prep_pending = true;
+    }
   }
+  auto prep_now = [&] {
+    if (prep_pending) {
+      prep_pending = false;
+      start_prep(c, true);
+    }
+  };
   for (int round = 0;; ++round) {
     static const bool stepwise = [] {  // SSUM_BFS_STEPWISE=1: step by step, frontier sizes traced
       const char* e = std::getenv("SSUM_BFS_STEPWISE");
       return e && *e == '1';
     }();
-    if (stepwise || !bfs_persistent(c, cfg, ne)) ne = bfs_synchronous(c, cfg);
+    S.bfs_namb = -1;
+    if (stepwise) prep_now();
+    if (stepwise || !bfs_persistent(c, cfg, ne, prep_now)) {
+      prep_now();
+      ne = bfs_synchronous(c, cfg);
+      S.bfs_namb = -1;  // the step-by-step traversal may have met other pairs
+    }
     if (stepwise && trace().on) {
       std::fprintf(stderr, "[ssum bfs] %zu steps, frontier:", S.plan_m.size());
       for (const int m : S.plan_m) std::fprintf(stderr, " %d", m);
       std::fprintf(stderr, " emissions %lld\n", ne);
     }
-    if (!resolve_mac(c)) break;
+    if (!resolve_mac(c, S.bfs_namb)) break;
     if (round > 64) throw Error(SSUM_INTERNAL, "dual traversal: MAC guard band did not settle");
   }
   L.n_inter = ne;
