@@ -164,6 +164,48 @@ def test_random_cap_parity_dense(ss, ol):
     assert np.isfinite(d).all()
 
 
+@pytest.mark.slow
+def test_dense_leaves_close_pairs_and_singular(ss, ol):
+    """Dense leaves take the lean reference-rounded block (kernels.cuh
+    near_lean_block): pairs with 1 - x.y < 2^-30 leave its sums and are taken
+    one by one on the exact form. 2^18 cap points (spacing ~8.5e-4 rad: dense
+    leaves) plus 96 twins at arcs 5e-7 .. 2e-4 from a cap point
+    (1 - x.y = 1.3e-13 .. 2e-8, both sides of the switch, all above the
+    reference's singular tolerance) against the reference; then an exact
+    duplicate inside a dense leaf must raise like the reference does.
+    Measured 1.5e-12 overall and 2.8e-11 on the twins' own rows — with the
+    lean block and with the 18-instruction exact block alike (SSUM_DENSE_EXACT18
+    build): at 1 - x.y ~ 1e-13 the reference's own term carries ~1e-16 /
+    sqrt(2 (1 - x.y)) ~ 2e-10 relative rounding from cross(x, y), so that is
+    the floor of any comparison with it, not this path's error."""
+    xyz, z, a = ss.make_random_cap(1 << 18, 11)
+    q = z * a
+    rng = np.random.default_rng(3)
+    x0 = np.array([np.cos(np.radians(40.0)), 0.0, np.sin(np.radians(40.0))])
+    inside = np.flatnonzero(xyz @ x0 > np.cos(np.radians(8.0)))
+    pick = rng.choice(inside, 96, replace=False)
+    t = rng.standard_normal((96, 3))
+    t -= (t * xyz[pick]).sum(1, keepdims=True) * xyz[pick]
+    t /= np.linalg.norm(t, axis=1, keepdims=True)
+    arc = 10.0 ** rng.uniform(np.log10(5e-7), np.log10(2e-4), 96)
+    twins = xyz[pick] + arc[:, None] * t
+    twins /= np.linalg.norm(twins, axis=1, keepdims=True)
+    den = 1.0 - (twins * xyz[pick]).sum(1)
+    assert den.min() > 5e-14 and (den < 2.0 ** -30).sum() > 20 and (den > 2.0 ** -30).sum() > 5
+    x2 = np.vstack([xyz, twins])
+    q2 = np.append(q, rng.uniform(0.5, 1.5, 96) * q[pick])
+    mine = ss.treecode_sum(ss.BiotSavartKernel, x2, q2, cfg(ss))
+    ref, _ = ol.ref_treecode(0, x2, q2, 0.7, 64, 8, 10, NCPU)
+    err = ol.rel_l2(mine, ref)
+    rows = np.append(pick, np.arange(xyz.shape[0], x2.shape[0]))  # the close pairs' own rows
+    err_rows = ol.rel_l2(mine[rows], ref[rows])
+    print(f"\ndense leaves with close pairs: rel_l2 {err:.3e}, on the twins' rows {err_rows:.3e}")
+    assert err < REL_TOL and err_rows < REL_TOL
+    dup = np.vstack([x2, xyz[pick[:1]]])
+    with pytest.raises(ss.SingularKernelError):
+        ss.treecode_sum(ss.BiotSavartKernel, dup, np.append(q2, 1e-6), cfg(ss))
+
+
 def test_direct_parity(ss, ol, mesh_fixture):
     xyz, q, a = mesh_fixture(5)
     for kernel, k in ((0, ss.BiotSavartKernel), (1, ss.LogPotentialKernel)):
