@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   // full[s]: the stage's bytes landed (producer arrival + transaction
   // count); empty[s]: every warp is done reading it (one arrival per warp)
   __shared__ unsigned long long full[kStages], empty[kStages];
+  __shared__ unsigned step_inv;  // ceil(2^32 / (kNs G)), see steps_of below
   constexpr int kChunk = CHUNK;
   auto buf = reinterpret_cast<double4(*)[kChunk + kPad]>(smem);
   int2* rtab = reinterpret_cast<int2*>(smem + kStages * sizeof(double4) * (kChunk + kPad));
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(NTH, MINB)
   }
   if constexpr (KER == kLOG) log_tab_stage(ltab_s, ltab_g, tid, NTH);
   if (tid == 0) {
+    step_inv = 0xffffffffu / static_cast<unsigned>(kNs * G) + 1u;  // kNs G >= 2
 #pragma unroll
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
@@ -270,8 +272,19 @@ __global__ void __launch_bounds__(NTH, MINB)
   // steps of kNs sources per lane per chunk: a chunk of n sources takes
   // ceil(n / (kNs G)) steps (the zero-padded tail contributes nothing)
   const int kStep = kNs * G;
+#ifdef SSUM_STEPS_HWDIV  // the earlier form: ptxas re-did both divisions in every chunk (~100 instructions per tile)
   const int steps_full = (kChunk + kStep - 1) / kStep;
   const int steps_last = (total - (nch - 1) * kChunk + kStep - 1) / kStep;
+#else
+  // ceil(n / kStep) for n <= kChunk + kStep as one multiply-high: for m, d <
+  // 2^16, m / d == umulhi(m, ceil(2^32 / d)). The multiplier is divided out
+  // once per tile (thread 0, before the prologue's barrier) and read back
+  // from shared memory where it is used: held in a register it cost the
+  // 64-register loops moves, and left to ptxas it was re-divided per chunk.
+  auto steps_of = [&](int m) {
+    return static_cast<int>(__umulhi(static_cast<unsigned>(m + kStep - 1), *static_cast<volatile unsigned*>(&step_inv)));
+  };
+#endif
   if (tid < 32)
     for (int cc = 1; cc < min(nch, kStages - 1); ++cc) issue(cc, false);
   for (int c = 0; c < nch; ++c) {
@@ -280,14 +293,22 @@ __global__ void __launch_bounds__(NTH, MINB)
     mbar_wait(&full[c % kStages], (c / kStages) & 1);
     const int n = min(kChunk, total - c * kChunk);
     const double4* B = buf[c % kStages] + g;  // this lane's sources: B[m G], m = 0, 1, ...
+#ifdef SSUM_STEPS_HWDIV
     const int steps = more ? steps_full : steps_last;
+#else
+    const int steps = steps_of(n);
+#endif
     // steps covering the chunk's near-possible prefix [0, near_total - c kChunk):
     // the same staged blocks with near pairs masked and counted, checked
     // against the lane's self pairs once per chunk
     int near_steps = 0;
     if (MODE != kFitMode) {
       const int nn = min(n, T.near_total - c * kChunk);
+#ifdef SSUM_STEPS_HWDIV
       near_steps = nn > 0 ? (nn + kStep - 1) / kStep : 0;
+#else
+      near_steps = nn > 0 ? steps_of(nn) : 0;
+#endif
     }
 #ifdef SSUM_TIMING_NO_NEAR  // timing experiment only: wrong results for near/self pairs
     near_steps = 0;
@@ -365,7 +386,14 @@ __global__ void __launch_bounds__(NTH, MINB)
 #pragma unroll
       for (int q = 0; q < kTpt; ++q) {
         const int o = ti[q] + T.self_shift - c * kChunk;
+#ifdef SSUM_STEPS_HWDIV
         nself += ((T.has_self & 1) && o >= 0 && o < o_end && o % G == g) ? 1 : 0;
+#else
+        // o % G == g  <=>  o % (kNs G) is g, g + G, ... (kNs = 2: g or g + G); o < 2^16 here
+        static_assert(kNs == 2, "self position test");
+        const int orem = o - static_cast<int>(__umulhi(static_cast<unsigned>(o), *static_cast<volatile unsigned*>(&step_inv))) * kStep;
+        nself += ((T.has_self & 1) && o >= 0 && o < o_end && (orem == g || orem == g + G)) ? 1 : 0;
+#endif
       }
       if (__any_sync(0xffffffffu, ncnt != nself)) {
         // only the steps that met a masked pair (dense inputs: a handful of

@@ -6,7 +6,7 @@
 # check, the ncu launch list of the headline command and one ncu --set full
 # capture of the hot kernels. Raw outputs in gpurun_out/prof2c/ (summarised
 # into profiles/r2c/).
-P=gpurun_out/prof2c
+P=${1:-gpurun_out/prof2c}
 mkdir -p $P
 nvidia-smi -q -d CLOCK,POWER > $P/smi.txt 2>&1
 python bench.py --steps 20 --warmup 5 > $P/bench_config4.json 2> $P/c4.err
